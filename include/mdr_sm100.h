@@ -1,0 +1,148 @@
+/*
+ * mdr_sm100.h -- C-ABI of libmdr_sm100.so, the B200 (sm_100a) implementation
+ * of the reference's batched local search (mdroute, arxiv 2605.05208).
+ *
+ * The reference is pure Python; its "FFI" for this path is its Python API.
+ * Each entry point below replaces one reference interface (file:line under
+ * /root/reference/pkg/src/mdroute/); the Python package
+ * paper_2605_05208_b200 binds them with ctypes and re-exposes the reference
+ * signatures (INTEGRATION.md shows the binding).
+ *
+ *   mdr_instance_create   Instance + ScalingConstants + NeighborLists upload
+ *                         (model.py:39-154, evaluation.py:109-132, neighborhood.py:45-57)
+ *   mdr_pop_create/upload SolutionCache per individual (batch.py:48-158),
+ *                         SolutionIndex (moves.py:151-171)
+ *   mdr_count/enumerate   enumerate_candidates (moves.py:444-464)
+ *   mdr_evaluate          evaluate_candidates (batch.py:365-553)
+ *   mdr_leader_followers  leader_and_followers (batch.py:578-614)
+ *   mdr_totals            SolutionCache.totals (batch.py:161-165)
+ *   mdr_local_search      local_search (localsearch.py:97-140), population-batched:
+ *                         B independent descents advance together on the device
+ *
+ * Conventions: plain pointers and sizes, host buffers unless stated, return
+ * int status (MDR_OK ...), no C++ exceptions cross the ABI, a handle is used
+ * from one host thread at a time.  `stream` is a cudaStream_t (NULL = legacy
+ * default stream).  There is no CPU fallback: without a CUDA device every
+ * call fails with MDR_ERR_CUDA.
+ */
+#ifndef MDR_SM100_H
+#define MDR_SM100_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MDR_OK 0
+#define MDR_ERR_ARG 1      /* invalid argument (ValueError in the reference)      */
+#define MDR_ERR_CONFLICT 2 /* conflicting move set (localsearch.py:63-64)         */
+#define MDR_ERR_CAPACITY 3 /* route/position/follower capacity exceeded: caller
+                              re-creates the population with larger caps and retries */
+#define MDR_ERR_CUDA 4     /* CUDA error or no device                              */
+#define MDR_ERR_PERMS 5    /* operator-permutation stream exhausted                */
+
+/* operator codes = moves.Op (moves.py:24-30) */
+#define MDR_RELOCATE 0
+#define MDR_SWAP 1
+#define MDR_TWO_OPT_STAR 2
+#define MDR_TWO_OPT 3
+#define MDR_DEPOT_INSERT 4
+#define MDR_DEPOT_REPLACE 5
+
+typedef struct mdr_instance mdr_instance;
+typedef struct mdr_pop mdr_pop;
+
+typedef struct mdr_instance_desc {
+  int32_t n_nodes, n_depots;
+  const double *dist, *time; /* [n*n] row-major; time == dist means "time is dist" */
+  const double *demand, *service, *tw_early, *tw_late; /* [n] */
+  double capacity, max_duration, fleet_per_depot;     /* +inf allowed */
+  int32_t open_routes, has_windows;
+  double gamma, theta;   /* ScalingConstants */
+  const int32_t *lists;  /* [n * width] NeighborLists.lists, -1 padded */
+  int32_t width;
+} mdr_instance_desc;
+
+/* candidate SoA in moves._FIELDS order (moves.py:174-176) */
+typedef struct mdr_cands {
+  int64_t n;
+  int64_t *r1, *p1, *r2, *p2, *len1, *len2, *depot, *mode;
+  uint8_t *rev1, *rev2;
+} mdr_cands;
+
+typedef struct mdr_deltas {
+  double *dD, *dV1, *dV2, *dV3, *dV4, *dF;
+  uint8_t *fleet_neutral;
+} mdr_deltas;
+
+typedef struct mdr_ls_cfg {
+  int32_t depth, multi_move;       /* SearchConfig (localsearch.py:24-31) */
+  double kappa, lam_min, lam_max;  /* PenaltyState (evaluation.py:135-150) */
+  int32_t max_passes, n_ops;
+  const uint8_t *perms;            /* [B][max_passes][n_ops]: rng.shuffle results, host */
+  double deadline_s;               /* <0: none; else seconds from the call (checked between rounds) */
+  int32_t rounds_per_sync;         /* device rounds per host poll (0 = default) */
+  int32_t use_graph;               /* capture the rounds in a CUDA graph */
+} mdr_ls_cfg;
+
+typedef struct mdr_ls_stats {
+  int32_t passes, accepted, op_evals, status;
+  int64_t cands[6];       /* candidates scored per operator (duplicates included) */
+  int64_t moves_applied;
+  int32_t n_feasible;     /* feasible post-step states */
+  int32_t n_improving;    /* feasible states that lowered the running minimum D */
+  double best_feasible_D; /* +inf if none */
+} mdr_ls_stats;
+
+typedef struct mdr_timing {
+  double eval_ms, select_ms, plan_ms, total_ms; /* summed CUDA-event times */
+  int64_t eval_launches, rounds;
+  int64_t cands_total;
+} mdr_timing;
+
+const char *mdr_last_error(void);
+int mdr_device_count(void);
+const char *mdr_build_info(void);
+
+int mdr_instance_create(const mdr_instance_desc *desc, int32_t device, mdr_instance **out);
+void mdr_instance_destroy(mdr_instance *inst);
+
+/* B_cap individuals, at most J_cap routes and K_cap customers per route,
+ * F_cap follower entries per individual per operator evaluation. */
+int mdr_pop_create(mdr_instance *inst, int32_t B_cap, int32_t J_cap, int32_t K_cap, int32_t F_cap,
+                   mdr_pop **out);
+void mdr_pop_destroy(mdr_pop *pop);
+
+/* Solutions of B individuals: individual b owns routes rbase[b]..rbase[b+1]-1;
+ * route r has customers cust[coff[r]..coff[r+1]), endpoints dep[r], arr[r].
+ * lam: [B*4]. Builds all tables on the device. */
+int mdr_pop_upload(mdr_pop *pop, int32_t B, const int32_t *rbase, const int32_t *coff,
+                   const int32_t *cust, const int32_t *dep, const int32_t *arr, const double *lam,
+                   void *stream);
+/* inverse of upload; capacities in *n_routes / *n_cust on input, sizes on output */
+int mdr_pop_download(mdr_pop *pop, int32_t *rbase, int32_t *coff, int32_t *cust, int32_t *dep,
+                     int32_t *arr, double *lam, int32_t *n_routes, int32_t *n_cust, void *stream);
+/* best feasible snapshot per individual (routes when D improved); same layout */
+int mdr_pop_download_best(mdr_pop *pop, int32_t *rbase, int32_t *coff, int32_t *cust, int32_t *dep,
+                          int32_t *arr, double *bestD, int32_t *n_routes, int32_t *n_cust,
+                          void *stream);
+
+int64_t mdr_count(mdr_pop *pop, int32_t b, int32_t op);
+/* out->n holds the capacity on input and the count on output */
+int mdr_enumerate(mdr_pop *pop, int32_t b, int32_t op, mdr_cands *out);
+int mdr_evaluate(mdr_pop *pop, int32_t b, int32_t op, const mdr_cands *cs, const double lam[4],
+                 mdr_deltas *out);
+/* leader index (-1 if none); followers sorted by (dF, key, index) */
+int mdr_leader_followers(mdr_pop *pop, const mdr_cands *cs, const mdr_deltas *d, int32_t multi_move,
+                         int64_t *leader, int64_t *followers, int64_t *n_followers);
+int mdr_totals(mdr_pop *pop, int32_t b, double out[5]);
+
+/* B_active = individuals 0..B-1 of the last upload. stats: [B] */
+int mdr_local_search(mdr_pop *pop, const mdr_ls_cfg *cfg, mdr_ls_stats *stats, void *stream);
+int mdr_get_timing(mdr_pop *pop, mdr_timing *out);
+int mdr_set_profiling(mdr_pop *pop, int32_t on);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,773 @@
+// mdr_api.cu -- host side of libmdr_sm100.so: the C-ABI of include/mdr_sm100.h.
+//
+// Owns all device memory (instance, population tables, round scratch) and
+// drives the population-batched local search: per device round one plan,
+// one fused evaluate and one select/apply launch, polled every few rounds
+// for completion and the caller's deadline (localsearch.py:116-117).
+#include <cub/cub.cuh>
+
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/mdr_sm100.h"
+#include "mdr_kernels.cuh"
+
+using namespace mdr;
+
+static thread_local std::string g_err;
+
+static int fail(int code, const std::string &msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CK(call)                                                                          \
+  do {                                                                                    \
+    cudaError_t e__ = (call);                                                             \
+    if (e__ != cudaSuccess) return fail(MDR_ERR_CUDA, std::string(#call ": ") + cudaGetErrorString(e__)); \
+  } while (0)
+
+struct mdr_instance {
+  int device;
+  DevInst I;
+  std::vector<void *> allocs;
+};
+
+struct mdr_pop {
+  mdr_instance *inst;
+  DevPop P;
+  int B;
+  int grid;
+  std::vector<void *> allocs;
+  size_t max_chunks;
+  // perms buffer
+  uint8_t *d_perms;
+  size_t perms_cap;
+  // transfer scratch
+  int *d_xfer;
+  size_t xfer_cap;
+  int *d_hdr;
+  int *h_hdr;  // pinned
+  // timing
+  int profiling;
+  mdr_timing tm;
+  cudaEvent_t ev[8];
+};
+
+template <typename T>
+static int dalloc(std::vector<void *> &owner, T **p, size_t n) {
+  if (n == 0) n = 1;
+  void *q = nullptr;
+  cudaError_t e = cudaMalloc(&q, n * sizeof(T));
+  if (e != cudaSuccess) return fail(MDR_ERR_CUDA, std::string("cudaMalloc: ") + cudaGetErrorString(e));
+  owner.push_back(q);
+  *p = reinterpret_cast<T *>(q);
+  return MDR_OK;
+}
+
+#define DA(owner, ptr, n)                        \
+  do {                                           \
+    int rc__ = dalloc(owner, &(ptr), (size_t)(n)); \
+    if (rc__) return rc__;                       \
+  } while (0)
+
+extern "C" {
+
+const char *mdr_last_error(void) { return g_err.c_str(); }
+
+int mdr_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
+  return n;
+}
+
+const char *mdr_build_info(void) {
+  return "libmdr_sm100: sm_100a (compute_100a), fp64 with -fmad=false";
+}
+
+int mdr_instance_create(const mdr_instance_desc *d, int32_t device, mdr_instance **out) {
+  if (!d || !out) return fail(MDR_ERR_ARG, "null argument");
+  int N = d->n_nodes, ND = d->n_depots;
+  if (ND < 1 || N - ND < 1) return fail(MDR_ERR_ARG, "instance needs at least one depot and one customer");
+  if (ND > 254) return fail(MDR_ERR_ARG, "at most 254 depots supported");
+  if (d->width < 1) return fail(MDR_ERR_ARG, "neighbour list width must be >= 1");
+  if (!d->dist || !d->demand || !d->service || !d->tw_early || !d->tw_late || !d->lists)
+    return fail(MDR_ERR_ARG, "null array in instance descriptor");
+  int ndev = mdr_device_count();
+  if (ndev <= 0) return fail(MDR_ERR_CUDA, "no CUDA device (the sm_100a library has no CPU path)");
+  if (device < 0 || device >= ndev) return fail(MDR_ERR_ARG, "bad device index");
+  CK(cudaSetDevice(device));
+  mdr_instance *I = new mdr_instance();
+  I->device = device;
+  DevInst &D = I->I;
+  D.N = N; D.ND = ND; D.NC = N - ND; D.W = d->width;
+  size_t nn = (size_t)N * N;
+  double *dist = nullptr, *time = nullptr;
+  int rc;
+  if ((rc = dalloc(I->allocs, &dist, nn))) { delete I; return rc; }
+  cudaMemcpy(dist, d->dist, nn * sizeof(double), cudaMemcpyHostToDevice);
+  D.talias = (d->time == nullptr || d->time == d->dist);
+  if (!D.talias) {
+    if ((rc = dalloc(I->allocs, &time, nn))) { delete I; return rc; }
+    cudaMemcpy(time, d->time, nn * sizeof(double), cudaMemcpyHostToDevice);
+  } else {
+    time = dist;
+  }
+  D.dist = dist; D.time = time;
+  std::vector<double4> node(N);
+  for (int v = 0; v < N; v++) node[v] = make_double4(d->demand[v], d->service[v], d->tw_early[v], d->tw_late[v]);
+  double4 *dnode = nullptr;
+  if ((rc = dalloc(I->allocs, &dnode, N))) { delete I; return rc; }
+  cudaMemcpy(dnode, node.data(), N * sizeof(double4), cudaMemcpyHostToDevice);
+  D.node = dnode;
+  int *lists = nullptr;
+  size_t nl = (size_t)(N - ND) * d->width;
+  if ((rc = dalloc(I->allocs, &lists, nl))) { delete I; return rc; }
+  cudaMemcpy(lists, d->lists + (size_t)ND * d->width, nl * sizeof(int), cudaMemcpyHostToDevice);
+  D.lists = lists;
+  D.Q = d->capacity; D.Dmax = d->max_duration; D.NV = d->fleet_per_depot;
+  D.d_on = !std::isinf(d->max_duration);
+  D.nv_on = !std::isinf(d->fleet_per_depot);
+  D.open = d->open_routes ? 1 : 0;
+  D.win = d->has_windows ? 1 : 0;
+  D.gamma = d->gamma; D.theta = d->theta;
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) {
+    for (void *p : I->allocs) cudaFree(p);
+    delete I;
+    return fail(MDR_ERR_CUDA, std::string("instance upload: ") + cudaGetErrorString(e));
+  }
+  *out = I;
+  return MDR_OK;
+}
+
+void mdr_instance_destroy(mdr_instance *I) {
+  if (!I) return;
+  cudaSetDevice(I->device);
+  for (void *p : I->allocs) cudaFree(p);
+  delete I;
+}
+
+int mdr_pop_create(mdr_instance *inst, int32_t Bcap, int32_t J, int32_t K, int32_t Fcap, mdr_pop **out) {
+  if (!inst || !out) return fail(MDR_ERR_ARG, "null argument");
+  if (Bcap < 1 || J < 1 || K < 1 || Fcap < 1) return fail(MDR_ERR_ARG, "capacities must be >= 1");
+  if (J > 2046) return fail(MDR_ERR_ARG, "J_cap must be <= 2046 (11-bit route field of the packed key)");
+  if (K > 500) return fail(MDR_ERR_ARG, "K_cap must be <= 500 (9-bit position field of the packed key)");
+  CK(cudaSetDevice(inst->device));
+  mdr_pop *p = new mdr_pop();
+  memset(&p->tm, 0, sizeof(p->tm));
+  p->inst = inst;
+  p->B = 0;
+  DevPop &P = p->P;
+  const DevInst &I = inst->I;
+  P.Bcap = Bcap; P.J = J; P.K = K; P.Kp = K + 2; P.Fcap = Fcap; P.FE = I.win ? 6 : 4;
+  P.N = I.N; P.ND = I.ND;
+  auto &A = p->allocs;
+  size_t rows = (size_t)Bcap * J, slots = rows * P.Kp;
+  DA(A, P.m, Bcap);
+  DA(A, P.rmeta, rows);
+  DA(A, P.seq, slots);
+  DA(A, P.loc, (size_t)Bcap * I.N);
+  DA(A, P.rcon, rows);
+  DA(A, P.tabP, slots * P.FE);
+  DA(A, P.tabS, slots * P.FE);
+  DA(A, P.fleet, (size_t)Bcap * I.ND);
+  DA(A, P.fexcess, Bcap);
+  DA(A, P.lam, (size_t)Bcap * 4);
+  DA(A, P.st, Bcap);
+  DA(A, P.cands, (size_t)Bcap * 6);
+  DA(A, P.op_cur, Bcap);
+  DA(A, P.wsize, Bcap);
+  DA(A, P.chunk_off, Bcap + 1);
+  DA(A, P.total_chunks, 1);
+  DA(A, P.active, 1);
+  long long wmax = 0;
+  for (int op = 0; op < 6; op++) {
+    long long w = op_items(op, J, I.NC, I.W, I.ND, I.win, I.open, K);
+    if (w > wmax) wmax = w;
+  }
+  if (wmax > 0x7fffffffLL) return fail(MDR_ERR_ARG, "candidate index space exceeds 2^31 per individual");
+  p->max_chunks = (size_t)Bcap * (size_t)((wmax + MDR_CHUNK - 1) / MDR_CHUNK);
+  DA(A, P.partial, p->max_chunks);
+  DA(A, P.fol, (size_t)Bcap * Fcap);
+  DA(A, P.fcount, Bcap);
+  DA(A, P.nanflag, Bcap);
+  DA(A, P.scratch_seq, slots);
+  DA(A, P.scratch_meta, rows);
+  DA(A, P.best_m, Bcap);
+  DA(A, P.best_meta, rows);
+  DA(A, P.best_seq, slots);
+  CK(cudaMemset(P.m, 0, sizeof(int) * Bcap));
+  CK(cudaMemset(P.best_m, 0, sizeof(int) * Bcap));
+  CK(cudaMemset(P.rmeta, 0, sizeof(int4) * rows));
+  CK(cudaMemset(P.st, 0, sizeof(LsState) * Bcap));
+  CK(cudaMemset(P.cands, 0, sizeof(unsigned long long) * Bcap * 6));
+  P.perms = nullptr; P.maxp = 0; P.nops = 0;
+  p->d_perms = nullptr; p->perms_cap = 0;
+  p->d_xfer = nullptr; p->xfer_cap = 0;
+  DA(A, p->d_hdr, 4);
+  CK(cudaMallocHost(&p->h_hdr, 4 * sizeof(int)));
+  p->grid = eval_grid_size(I.win);
+  p->profiling = 0;
+  for (int i = 0; i < 8; i++) CK(cudaEventCreate(&p->ev[i]));
+  *out = p;
+  return MDR_OK;
+}
+
+void mdr_pop_destroy(mdr_pop *p) {
+  if (!p) return;
+  cudaSetDevice(p->inst->device);
+  for (void *q : p->allocs) cudaFree(q);
+  if (p->d_perms) cudaFree(p->d_perms);
+  if (p->d_xfer) cudaFree(p->d_xfer);
+  if (p->h_hdr) cudaFreeHost(p->h_hdr);
+  for (int i = 0; i < 8; i++) cudaEventDestroy(p->ev[i]);
+  delete p;
+}
+
+static int ensure_xfer(mdr_pop *p, size_t n) {
+  if (p->xfer_cap >= n) return MDR_OK;
+  if (p->d_xfer) cudaFree(p->d_xfer);
+  p->d_xfer = nullptr;
+  size_t c = n + n / 2 + 1024;
+  CK(cudaMalloc(&p->d_xfer, c * sizeof(int)));
+  p->xfer_cap = c;
+  return MDR_OK;
+}
+
+int mdr_pop_upload(mdr_pop *p, int32_t B, const int32_t *rbase, const int32_t *coff, const int32_t *cust,
+                   const int32_t *dep, const int32_t *arr, const double *lam, void *stream) {
+  if (!p || B < 0 || B > p->P.Bcap) return fail(MDR_ERR_ARG, "B out of range");
+  cudaStream_t s = (cudaStream_t)stream;
+  CK(cudaSetDevice(p->inst->device));
+  const DevInst &I = p->inst->I;
+  int R = rbase[B];
+  int C = coff[R];
+  for (int b = 0; b < B; b++) {
+    int m = rbase[b + 1] - rbase[b];
+    if (m < 0) return fail(MDR_ERR_ARG, "rbase must be non-decreasing");
+    if (m > p->P.J) return fail(MDR_ERR_CAPACITY, "individual has more routes than J_cap");
+  }
+  for (int r = 0; r < R; r++) {
+    int k = coff[r + 1] - coff[r];
+    if (k < 0) return fail(MDR_ERR_ARG, "coff must be non-decreasing");
+    if (k > p->P.K) return fail(MDR_ERR_CAPACITY, "route longer than K_cap");
+    if (dep[r] < 0 || dep[r] >= I.ND || arr[r] < 0 || arr[r] >= I.ND)
+      return fail(MDR_ERR_ARG, "route endpoint is not a depot");
+  }
+  for (int c = 0; c < C; c++)
+    if (cust[c] < I.ND || cust[c] >= I.N) return fail(MDR_ERR_ARG, "customer id out of range");
+  size_t need = (size_t)(B + 1) + (R + 1) + C + 2 * (size_t)R;
+  int rc = ensure_xfer(p, need);
+  if (rc) return rc;
+  int *d_rbase = p->d_xfer, *d_coff = d_rbase + B + 1, *d_cust = d_coff + R + 1, *d_dep = d_cust + C,
+      *d_arr = d_dep + R;
+  CK(cudaMemcpyAsync(d_rbase, rbase, sizeof(int) * (B + 1), cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(d_coff, coff, sizeof(int) * (R + 1), cudaMemcpyHostToDevice, s));
+  if (C) CK(cudaMemcpyAsync(d_cust, cust, sizeof(int) * C, cudaMemcpyHostToDevice, s));
+  if (R) {
+    CK(cudaMemcpyAsync(d_dep, dep, sizeof(int) * R, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(d_arr, arr, sizeof(int) * R, cudaMemcpyHostToDevice, s));
+  }
+  CK(cudaMemcpyAsync(p->P.lam, lam, sizeof(double) * 4 * B, cudaMemcpyHostToDevice, s));
+  p->B = B;
+  if (B > 0) {
+    launch_unpack(I, p->P, B, d_rbase, d_coff, d_cust, d_dep, d_arr, s);
+    launch_rebuild(I, p->P, B, I.win, s);
+  }
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(s));
+  return MDR_OK;
+}
+
+static int download_impl(mdr_pop *p, int best, int32_t *rbase, int32_t *coff, int32_t *cust, int32_t *dep,
+                         int32_t *arr, int32_t *n_routes, int32_t *n_cust, cudaStream_t s) {
+  int B = p->B;
+  int cap_r = *n_routes, cap_c = *n_cust;
+  size_t need = (size_t)(B + 1) + (cap_r + 1) + cap_c + 2 * (size_t)cap_r;
+  int rc = ensure_xfer(p, need);
+  if (rc) return rc;
+  int *d_rbase = p->d_xfer, *d_coff = d_rbase + B + 1, *d_cust = d_coff + cap_r + 1, *d_dep = d_cust + cap_c,
+      *d_arr = d_dep + cap_r;
+  launch_pack(p->P, B, best, d_rbase, d_coff, d_cust, d_dep, d_arr, p->d_hdr, cap_r, cap_c, s);
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(p->h_hdr, p->d_hdr, 2 * sizeof(int), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  int R = p->h_hdr[0], C = p->h_hdr[1];
+  *n_routes = R;
+  *n_cust = C;
+  if (R > cap_r || C > cap_c) return fail(MDR_ERR_CAPACITY, "download buffers too small");
+  CK(cudaMemcpyAsync(rbase, d_rbase, sizeof(int) * (B + 1), cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(coff, d_coff, sizeof(int) * (R + 1), cudaMemcpyDeviceToHost, s));
+  if (C) CK(cudaMemcpyAsync(cust, d_cust, sizeof(int) * C, cudaMemcpyDeviceToHost, s));
+  if (R) {
+    CK(cudaMemcpyAsync(dep, d_dep, sizeof(int) * R, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(arr, d_arr, sizeof(int) * R, cudaMemcpyDeviceToHost, s));
+  }
+  CK(cudaStreamSynchronize(s));
+  if (R == 0) coff[0] = 0;
+  return MDR_OK;
+}
+
+int mdr_pop_download(mdr_pop *p, int32_t *rbase, int32_t *coff, int32_t *cust, int32_t *dep, int32_t *arr,
+                     double *lam, int32_t *n_routes, int32_t *n_cust, void *stream) {
+  if (!p) return fail(MDR_ERR_ARG, "null pop");
+  CK(cudaSetDevice(p->inst->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  int rc = download_impl(p, 0, rbase, coff, cust, dep, arr, n_routes, n_cust, s);
+  if (rc) return rc;
+  if (lam) {
+    CK(cudaMemcpyAsync(lam, p->P.lam, sizeof(double) * 4 * p->B, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+  }
+  return MDR_OK;
+}
+
+int mdr_pop_download_best(mdr_pop *p, int32_t *rbase, int32_t *coff, int32_t *cust, int32_t *dep, int32_t *arr,
+                          double *bestD, int32_t *n_routes, int32_t *n_cust, void *stream) {
+  if (!p) return fail(MDR_ERR_ARG, "null pop");
+  CK(cudaSetDevice(p->inst->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  int rc = download_impl(p, 1, rbase, coff, cust, dep, arr, n_routes, n_cust, s);
+  if (rc) return rc;
+  if (bestD) {
+    std::vector<LsState> st(p->B);
+    CK(cudaMemcpy(st.data(), p->P.st, sizeof(LsState) * p->B, cudaMemcpyDeviceToHost));
+    for (int b = 0; b < p->B; b++) bestD[b] = st[b].bestD;
+  }
+  return MDR_OK;
+}
+
+// ---------------------------------------------------------------------------
+// operator-level API
+// ---------------------------------------------------------------------------
+struct NonZero {
+  __host__ __device__ bool operator()(const unsigned long long &k) const { return k != 0ull; }
+};
+
+static int enumerate_keys(mdr_pop *p, int b, int op, unsigned long long **d_out, long long *n_out,
+                          std::vector<void *> &tmp, cudaStream_t s) {
+  const DevInst &I = p->inst->I;
+  int m = 0;
+  CK(cudaMemcpy(&m, p->P.m + b, sizeof(int), cudaMemcpyDeviceToHost));
+  long long items = op_items(op, m, I.NC, I.W, I.ND, I.win, I.open, p->P.K);
+  unsigned long long *keys = nullptr, *outk = nullptr;
+  int *nsel = nullptr;
+  DA(tmp, keys, items);
+  DA(tmp, outk, items);
+  DA(tmp, nsel, 1);
+  launch_emit(I, p->P, b, op, items, keys, s);
+  CK(cudaGetLastError());
+  size_t tb = 0;
+  CK(cub::DeviceSelect::If(nullptr, tb, keys, outk, nsel, (int)items, NonZero(), s));
+  void *tst = nullptr;
+  DA(tmp, tst, tb + 1);
+  CK(cub::DeviceSelect::If(tst, tb, keys, outk, nsel, (int)items, NonZero(), s));
+  int n = 0;
+  if (items) CK(cudaMemcpyAsync(&n, nsel, sizeof(int), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  *d_out = outk;
+  *n_out = n;
+  return MDR_OK;
+}
+
+static void free_all(std::vector<void *> &v) {
+  for (void *q : v) cudaFree(q);
+  v.clear();
+}
+
+int64_t mdr_count(mdr_pop *p, int32_t b, int32_t op) {
+  if (!p || b < 0 || b >= p->B || op < 0 || op > 5) {
+    fail(MDR_ERR_ARG, "bad individual or operator");
+    return -1;
+  }
+  if (cudaSetDevice(p->inst->device) != cudaSuccess) return -1;
+  std::vector<void *> tmp;
+  unsigned long long *k;
+  long long n;
+  int rc = enumerate_keys(p, b, op, &k, &n, tmp, 0);
+  free_all(tmp);
+  return rc ? -1 : n;
+}
+
+int mdr_enumerate(mdr_pop *p, int32_t b, int32_t op, mdr_cands *out) {
+  if (!p || !out || b < 0 || b >= p->B) return fail(MDR_ERR_ARG, "bad individual");
+  if (op < 0 || op > 5) return fail(MDR_ERR_ARG, "unknown operator");
+  CK(cudaSetDevice(p->inst->device));
+  std::vector<void *> tmp;
+  unsigned long long *dk;
+  long long n;
+  int rc = enumerate_keys(p, b, op, &dk, &n, tmp, 0);
+  if (rc) { free_all(tmp); return rc; }
+  if (n > out->n) {
+    out->n = n;
+    free_all(tmp);
+    return fail(MDR_ERR_CAPACITY, "candidate buffers too small");
+  }
+  std::vector<unsigned long long> hk(n);
+  if (n) cudaMemcpy(hk.data(), dk, n * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+  free_all(tmp);
+  for (long long i = 0; i < n; i++) {
+    Cand c = unpack_key(hk[i]);
+    out->r1[i] = c.r1; out->p1[i] = c.p1; out->r2[i] = c.r2; out->p2[i] = c.p2;
+    out->len1[i] = c.l1; out->len2[i] = c.l2; out->rev1[i] = (uint8_t)c.rev1; out->rev2[i] = (uint8_t)c.rev2;
+    out->depot[i] = c.depot; out->mode[i] = c.mode;
+  }
+  out->n = n;
+  return MDR_OK;
+}
+
+static int upload_cands(const mdr_cands *cs, MatCands &mc, std::vector<void *> &tmp, cudaStream_t s) {
+  long long n = cs->n;
+  long long *f[8];
+  const int64_t *src[8] = {cs->r1, cs->p1, cs->r2, cs->p2, cs->len1, cs->len2, cs->depot, cs->mode};
+  for (int i = 0; i < 8; i++) {
+    DA(tmp, f[i], n);
+    if (n) CK(cudaMemcpyAsync(f[i], src[i], n * sizeof(long long), cudaMemcpyHostToDevice, s));
+  }
+  unsigned char *r1 = nullptr, *r2 = nullptr;
+  DA(tmp, r1, n);
+  DA(tmp, r2, n);
+  if (n) {
+    CK(cudaMemcpyAsync(r1, cs->rev1, n, cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(r2, cs->rev2, n, cudaMemcpyHostToDevice, s));
+  }
+  mc.r1 = f[0]; mc.p1 = f[1]; mc.r2 = f[2]; mc.p2 = f[3]; mc.len1 = f[4]; mc.len2 = f[5]; mc.depot = f[6];
+  mc.mode = f[7]; mc.rev1 = r1; mc.rev2 = r2; mc.n = n;
+  return MDR_OK;
+}
+
+static int check_cands(mdr_pop *p, int b, int op, const mdr_cands *cs) {
+  int m = 0;
+  CK(cudaMemcpy(&m, p->P.m + b, sizeof(int), cudaMemcpyDeviceToHost));
+  std::vector<int4> meta(m > 0 ? m : 1);
+  if (m) CK(cudaMemcpy(meta.data(), p->P.rmeta + (size_t)b * p->P.J, sizeof(int4) * m, cudaMemcpyDeviceToHost));
+  const DevInst &I = p->inst->I;
+  for (long long i = 0; i < cs->n; i++) {
+    long long r1 = cs->r1[i], r2 = cs->r2[i];
+    bool two = (op == 0 || op == 1) ? r1 != r2 : op == 2;
+    if (r1 < 0 || r1 >= m) return fail(MDR_ERR_ARG, "candidate r1 out of range");
+    if ((two || op == 0 || op == 1) && (r2 < 0 || r2 >= m)) return fail(MDR_ERR_ARG, "candidate r2 out of range");
+    long long k1 = meta[r1].x;
+    long long p1 = cs->p1[i], p2 = cs->p2[i], l1 = cs->len1[i], l2 = cs->len2[i];
+    if (p1 < 0 || p1 > k1 || l1 < 0 || l1 > 2 || l2 < 0 || l2 > 2) return fail(MDR_ERR_ARG, "candidate position out of range");
+    if ((op == 0 || op == 1) && p1 + l1 > k1) return fail(MDR_ERR_ARG, "segment exceeds route");
+    if (op == 0 || op == 1 || op == 2) {
+      long long k2 = meta[r2].x;
+      if (p2 < 0 || p2 > k2) return fail(MDR_ERR_ARG, "candidate p2 out of range");
+      if (op == 1 && p2 + l2 > k2) return fail(MDR_ERR_ARG, "segment exceeds route");
+    }
+    if (op == 3 && (p2 < p1 || p2 >= k1)) return fail(MDR_ERR_ARG, "2-opt positions out of range");
+    if (op == 4 && (p1 >= k1 || cs->depot[i] < 0 || cs->depot[i] >= I.ND)) return fail(MDR_ERR_ARG, "depot-insert out of range");
+    if (op == 5 && (cs->depot[i] < 0 || cs->depot[i] >= I.ND || cs->mode[i] < 0 || cs->mode[i] > 2))
+      return fail(MDR_ERR_ARG, "depot-replace out of range");
+  }
+  return MDR_OK;
+}
+
+int mdr_evaluate(mdr_pop *p, int32_t b, int32_t op, const mdr_cands *cs, const double lam[4], mdr_deltas *out) {
+  if (!p || !cs || !out || b < 0 || b >= p->B) return fail(MDR_ERR_ARG, "bad individual");
+  if (op < 0 || op > 5) return fail(MDR_ERR_ARG, "unknown operator");
+  CK(cudaSetDevice(p->inst->device));
+  int rc = check_cands(p, b, op, cs);
+  if (rc) return rc;
+  cudaStream_t s = 0;
+  std::vector<void *> tmp;
+  MatCands mc;
+  rc = upload_cands(cs, mc, tmp, s);
+  if (rc) { free_all(tmp); return rc; }
+  long long n = cs->n;
+  double *dl = nullptr, *dd = nullptr;
+  unsigned char *fn = nullptr;
+  if ((rc = dalloc(tmp, &dl, 4)) || (rc = dalloc(tmp, &dd, 6 * n)) || (rc = dalloc(tmp, &fn, n))) {
+    free_all(tmp);
+    return rc;
+  }
+  cudaMemcpyAsync(dl, lam, 4 * sizeof(double), cudaMemcpyHostToDevice, s);
+  MatDeltas md{dd, dd + n, dd + 2 * n, dd + 3 * n, dd + 4 * n, dd + 5 * n, fn};
+  launch_eval_mat(p->inst->I, p->P, b, op, mc, dl, md, p->inst->I.win, s);
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) { free_all(tmp); return fail(MDR_ERR_CUDA, cudaGetErrorString(e)); }
+  double *hs[6] = {out->dD, out->dV1, out->dV2, out->dV3, out->dV4, out->dF};
+  for (int f = 0; f < 6; f++)
+    if (n) cudaMemcpy(hs[f], dd + f * n, n * sizeof(double), cudaMemcpyDeviceToHost);
+  if (n) cudaMemcpy(out->fleet_neutral, fn, n, cudaMemcpyDeviceToHost);
+  free_all(tmp);
+  return MDR_OK;
+}
+
+struct OKI {
+  unsigned long long o, k;
+  long long i;
+};
+struct OKIMin {
+  __host__ __device__ OKI operator()(const OKI &a, const OKI &b) const {
+    if (a.o != b.o) return a.o < b.o ? a : b;
+    if (a.k != b.k) return a.k < b.k ? a : b;
+    return a.i <= b.i ? a : b;
+  }
+};
+struct MakeOKI {
+  const unsigned long long *o, *k;
+  __host__ __device__ OKI operator()(long long i) const { return OKI{o[i], k[i], i}; }
+};
+
+__global__ void k_gather_u64(const unsigned long long *src, const long long *idx, unsigned long long *dst, long long n) {
+  long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) dst[i] = src[idx[i]];
+}
+
+int mdr_leader_followers(mdr_pop *p, const mdr_cands *cs, const mdr_deltas *d, int32_t multi_move, int64_t *leader,
+                         int64_t *followers, int64_t *n_followers) {
+  if (!p || !cs || !d || !leader) return fail(MDR_ERR_ARG, "null argument");
+  CK(cudaSetDevice(p->inst->device));
+  *leader = -1;
+  if (n_followers) *n_followers = 0;
+  long long n = cs->n;
+  if (n == 0) return MDR_OK;
+  for (long long i = 0; i < n; i++) {
+    if (cs->r1[i] < -1 || cs->r1[i] > 2045 || cs->r2[i] < -1 || cs->r2[i] > 2045 || cs->p1[i] < -1 ||
+        cs->p1[i] > 510 || cs->p2[i] < -1 || cs->p2[i] > 510 || cs->len1[i] < 0 || cs->len1[i] > 3 ||
+        cs->len2[i] < 0 || cs->len2[i] > 3 || cs->depot[i] < -1 || cs->depot[i] > 254 || cs->mode[i] < -1 ||
+        cs->mode[i] > 2)
+      return fail(MDR_ERR_ARG, "candidate field outside the packed-key range");
+  }
+  cudaStream_t s = 0;
+  std::vector<void *> tmp;
+  MatCands mc;
+  int rc = upload_cands(cs, mc, tmp, s);
+  if (rc) { free_all(tmp); return rc; }
+  double *dd = nullptr;
+  unsigned char *fn = nullptr, *flag = nullptr;
+  unsigned long long *ord = nullptr, *key = nullptr;
+  int *nan = nullptr;
+#define TA(ptr, cnt) if ((rc = dalloc(tmp, &(ptr), (cnt)))) { free_all(tmp); return rc; }
+  TA(dd, 6 * n);
+  TA(fn, n);
+  TA(flag, n);
+  TA(ord, n);
+  TA(key, n);
+  TA(nan, 1);
+  const double *hs[6] = {d->dD, d->dV1, d->dV2, d->dV3, d->dV4, d->dF};
+  for (int f = 0; f < 6; f++) cudaMemcpyAsync(dd + f * n, hs[f], n * sizeof(double), cudaMemcpyHostToDevice, s);
+  cudaMemcpyAsync(fn, d->fleet_neutral, n, cudaMemcpyHostToDevice, s);
+  cudaMemsetAsync(nan, 0, sizeof(int), s);
+  MatDeltas md{dd, dd + n, dd + 2 * n, dd + 3 * n, dd + 4 * n, dd + 5 * n, fn};
+  launch_lf_prep(mc, md, ord, key, flag, nan, s);
+  // leader: min (ord(dF), key, index)  (batch.py:587-597, lexsort tie-break)
+  OKI *dmin = nullptr;
+  TA(dmin, 1);
+  cub::CountingInputIterator<long long> cnt(0);
+  cub::TransformInputIterator<OKI, MakeOKI, cub::CountingInputIterator<long long>> it(cnt, MakeOKI{ord, key});
+  size_t tb = 0;
+  OKI init{~0ull, ~0ull, (long long)n};
+  CK(cub::DeviceReduce::Reduce(nullptr, tb, it, dmin, (int)n, OKIMin(), init, s));
+  void *tst = nullptr;
+  TA(tst, tb + 1);
+  CK(cub::DeviceReduce::Reduce(tst, tb, it, dmin, (int)n, OKIMin(), init, s));
+  OKI hmin;
+  int hnan = 0;
+  cudaMemcpyAsync(&hmin, dmin, sizeof(OKI), cudaMemcpyDeviceToHost, s);
+  cudaMemcpyAsync(&hnan, nan, sizeof(int), cudaMemcpyDeviceToHost, s);
+  CK(cudaStreamSynchronize(s));
+  auto unord_h = [](unsigned long long o) {
+    unsigned long long u = (o >> 63) ? (o & 0x7fffffffffffffffull) : ~o;
+    double x;
+    memcpy(&x, &u, 8);
+    return x;
+  };
+  if (hnan || hmin.o == ~0ull || !(unord_h(hmin.o) < -MDR_EPS)) {
+    free_all(tmp);
+    return MDR_OK;
+  }
+  *leader = hmin.i;
+  if (multi_move && followers && n_followers) {
+    // followers: flagged, minus the leader index, sorted by (dF, key, index) (batch.py:600-613)
+    cudaMemsetAsync(flag + hmin.i, 0, 1, s);
+    long long *fidx = nullptr, *fidx2 = nullptr;
+    int *nsel = nullptr;
+    unsigned long long *k1 = nullptr, *k2 = nullptr;
+    TA(fidx, n);
+    TA(fidx2, n);
+    TA(nsel, 1);
+    TA(k1, n);
+    TA(k2, n);
+    size_t t2 = 0;
+    CK(cub::DeviceSelect::Flagged(nullptr, t2, cnt, flag, fidx, nsel, (int)n, s));
+    void *ts2 = nullptr;
+    TA(ts2, t2 + 1);
+    CK(cub::DeviceSelect::Flagged(ts2, t2, cnt, flag, fidx, nsel, (int)n, s));
+    int nf = 0;
+    cudaMemcpyAsync(&nf, nsel, sizeof(int), cudaMemcpyDeviceToHost, s);
+    CK(cudaStreamSynchronize(s));
+    if (nf > 0) {
+      int gb = (nf + 255) / 256;
+      // stable LSD: sort by key, then by ord(dF)
+      k_gather_u64<<<gb, 256, 0, s>>>(key, fidx, k1, nf);
+      size_t t3 = 0;
+      CK(cub::DeviceRadixSort::SortPairs(nullptr, t3, k1, k2, fidx, fidx2, nf, 0, 56, s));
+      void *ts3 = nullptr;
+      TA(ts3, t3 + 1);
+      CK(cub::DeviceRadixSort::SortPairs(ts3, t3, k1, k2, fidx, fidx2, nf, 0, 56, s));
+      k_gather_u64<<<gb, 256, 0, s>>>(ord, fidx2, k1, nf);
+      CK(cub::DeviceRadixSort::SortPairs(ts3, t3, k1, k2, fidx2, fidx, nf, 0, 64, s));
+      CK(cudaMemcpyAsync(followers, fidx, sizeof(long long) * nf, cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+    }
+    *n_followers = nf;
+  }
+#undef TA
+  free_all(tmp);
+  return MDR_OK;
+}
+
+int mdr_totals(mdr_pop *p, int32_t b, double out[5]) {
+  if (!p || b < 0 || b >= p->B) return fail(MDR_ERR_ARG, "bad individual");
+  CK(cudaSetDevice(p->inst->device));
+  double *d = nullptr;
+  CK(cudaMalloc(&d, 5 * sizeof(double)));
+  launch_totals(p->inst->I, p->P, b, d, 0);
+  cudaError_t e = cudaMemcpy(out, d, 5 * sizeof(double), cudaMemcpyDeviceToHost);
+  cudaFree(d);
+  if (e != cudaSuccess) return fail(MDR_ERR_CUDA, cudaGetErrorString(e));
+  return MDR_OK;
+}
+
+// ---------------------------------------------------------------------------
+// population-batched local search
+// ---------------------------------------------------------------------------
+int mdr_set_profiling(mdr_pop *p, int32_t on) {
+  if (!p) return fail(MDR_ERR_ARG, "null pop");
+  p->profiling = on;
+  memset(&p->tm, 0, sizeof(p->tm));
+  return MDR_OK;
+}
+
+int mdr_get_timing(mdr_pop *p, mdr_timing *out) {
+  if (!p || !out) return fail(MDR_ERR_ARG, "null argument");
+  *out = p->tm;
+  return MDR_OK;
+}
+
+int mdr_local_search(mdr_pop *p, const mdr_ls_cfg *cfg, mdr_ls_stats *stats, void *stream) {
+  if (!p || !cfg) return fail(MDR_ERR_ARG, "null argument");
+  if (cfg->depth < 1) return fail(MDR_ERR_ARG, "depth must be >= 1");
+  if (!(cfg->kappa > 0.0 && cfg->kappa < 1.0)) return fail(MDR_ERR_ARG, "kappa must lie in (0, 1)");
+  if (cfg->n_ops < 1 || cfg->n_ops > 6 || cfg->max_passes < 1 || !cfg->perms)
+    return fail(MDR_ERR_ARG, "bad operator permutation stream");
+  const int B = p->B;
+  CK(cudaSetDevice(p->inst->device));
+  cudaStream_t s = (cudaStream_t)stream;
+  const DevInst &I = p->inst->I;
+  size_t np = (size_t)B * cfg->max_passes * cfg->n_ops;
+  for (size_t i = 0; i < np; i++)
+    if (cfg->perms[i] > 5 || (I.win && cfg->perms[i] == 3)) return fail(MDR_ERR_ARG, "bad operator in permutation");
+  if (np > p->perms_cap) {
+    if (p->d_perms) cudaFree(p->d_perms);
+    p->d_perms = nullptr;
+    CK(cudaMalloc(&p->d_perms, np + 1));
+    p->perms_cap = np;
+  }
+  if (np) CK(cudaMemcpyAsync(p->d_perms, cfg->perms, np, cudaMemcpyHostToDevice, s));
+  DevPop P = p->P;
+  P.perms = p->d_perms;
+  P.maxp = cfg->max_passes;
+  P.nops = cfg->n_ops;
+  std::vector<LsState> st0(B > 0 ? B : 1);
+  for (int b = 0; b < B; b++) {
+    memset(&st0[b], 0, sizeof(LsState));
+    st0[b].bestD = INFINITY;
+  }
+  if (B) {
+    CK(cudaMemcpyAsync(P.st, st0.data(), sizeof(LsState) * B, cudaMemcpyHostToDevice, s));
+    CK(cudaMemsetAsync(P.cands, 0, sizeof(unsigned long long) * B * 6, s));
+    CK(cudaMemsetAsync(P.best_m, 0, sizeof(int) * B, s));
+  }
+  LsParams L;
+  L.depth = cfg->depth;
+  L.multi_move = cfg->multi_move ? 1 : 0;
+  L.kappa = cfg->kappa;
+  L.lam_min = cfg->lam_min;
+  L.lam_max = cfg->lam_max;
+  L.B = B;
+  const int rps = cfg->rounds_per_sync > 0 ? cfg->rounds_per_sync : 8;
+  auto t0 = std::chrono::steady_clock::now();
+  int prof = p->profiling;
+  if (prof) CK(cudaEventRecord(p->ev[6], s));
+  long long rounds = 0;
+  while (B > 0) {
+    for (int r = 0; r < rps; r++) {
+      if (prof) cudaEventRecord(p->ev[0], s);
+      launch_plan(I, P, L, s);
+      if (prof) cudaEventRecord(p->ev[1], s);
+      launch_eval(I, P, L, p->grid, I.win, s);
+      if (prof) cudaEventRecord(p->ev[2], s);
+      launch_select(I, P, L, I.win, s);
+      if (prof) {
+        cudaEventRecord(p->ev[3], s);
+        cudaEventSynchronize(p->ev[3]);
+        float a = 0, b2 = 0, c = 0;
+        cudaEventElapsedTime(&a, p->ev[0], p->ev[1]);
+        cudaEventElapsedTime(&b2, p->ev[1], p->ev[2]);
+        cudaEventElapsedTime(&c, p->ev[2], p->ev[3]);
+        p->tm.plan_ms += a;
+        p->tm.eval_ms += b2;
+        p->tm.select_ms += c;
+        p->tm.eval_launches++;
+      }
+      rounds++;
+    }
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(p->h_hdr, P.active, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (p->h_hdr[0] == 0) break;
+    if (cfg->deadline_s >= 0) {
+      double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+      if (el > cfg->deadline_s) break;
+    }
+  }
+  if (prof) {
+    CK(cudaEventRecord(p->ev[7], s));
+    CK(cudaEventSynchronize(p->ev[7]));
+    float tot = 0;
+    cudaEventElapsedTime(&tot, p->ev[6], p->ev[7]);
+    p->tm.total_ms += tot;
+    p->tm.rounds += rounds;
+  }
+  std::vector<LsState> st(B > 0 ? B : 1);
+  std::vector<unsigned long long> cands((size_t)(B > 0 ? B : 1) * 6);
+  if (B) {
+    CK(cudaMemcpyAsync(st.data(), P.st, sizeof(LsState) * B, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(cands.data(), P.cands, sizeof(unsigned long long) * B * 6, cudaMemcpyDeviceToHost, s));
+  }
+  CK(cudaStreamSynchronize(s));
+  int worst = MDR_OK;
+  for (int b = 0; b < B; b++) {
+    if (stats) {
+      mdr_ls_stats &o = stats[b];
+      o.passes = st[b].pass + 1;
+      o.accepted = st[b].accepted;
+      o.op_evals = st[b].op_evals;
+      o.status = st[b].status;
+      for (int q = 0; q < 6; q++) {
+        o.cands[q] = (int64_t)cands[(size_t)b * 6 + q];
+        if (prof) p->tm.cands_total += o.cands[q];
+      }
+      o.moves_applied = st[b].moves_applied;
+      o.n_feasible = st[b].n_feasible;
+      o.n_improving = st[b].n_improving;
+      o.best_feasible_D = st[b].bestD;
+    }
+    if (st[b].status && !worst) worst = st[b].status;
+  }
+  if (worst == MDR_ERR_CAPACITY) return fail(worst, "capacity exceeded during local search (J_cap/K_cap/F_cap)");
+  if (worst) return fail(worst, "local search stopped with an error status");
+  return MDR_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,776 @@
+// mdr_kernels.cu -- sm_100a kernels of the population-batched local search.
+//
+//   k_rebuild      one CTA per individual: SolutionIndex + subsequence tables
+//                  + route contributions + fleet increments (batch.py:51-158)
+//   k_plan         one CTA: per individual the operator of this round
+//                  (pre-drawn rng.shuffle stream), its candidate index-space
+//                  size, and the chunk offsets of the flattened work list
+//   k_eval         persistent grid over all individuals' chunks: implicit
+//                  enumeration (moves.py) + fp64 evaluation (batch.py:365-553)
+//                  + (dF, key) min-reduction + follower compaction
+//   k_select       one CTA per individual: leader, greedy route-disjoint
+//                  follower selection, apply, drop empties, rebuild, totals,
+//                  penalty adaptation, state machine (localsearch.py:97-140)
+#include <cstdio>
+
+#include "mdr_kernels.cuh"
+
+namespace mdr {
+
+// ---------------------------------------------------------------------------
+// block helpers
+// ---------------------------------------------------------------------------
+struct OK {
+  unsigned long long o, k;
+};
+__device__ __forceinline__ bool ok_less(const OK &a, const OK &b) {
+  return a.o < b.o || (a.o == b.o && a.k < b.k);
+}
+__device__ __forceinline__ OK warp_min(OK v) {
+#pragma unroll
+  for (int s = 16; s > 0; s >>= 1) {
+    OK w;
+    w.o = __shfl_xor_sync(0xffffffffu, v.o, s);
+    w.k = __shfl_xor_sync(0xffffffffu, v.k, s);
+    if (ok_less(w, v)) v = w;
+  }
+  return v;
+}
+// block-wide min; result valid in all threads. sm needs blockDim/32 entries.
+__device__ __forceinline__ OK block_min(OK v, OK *sm) {
+  v = warp_min(v);
+  int w = threadIdx.x >> 5, l = threadIdx.x & 31, nw = blockDim.x >> 5;
+  __syncthreads();
+  if (l == 0) sm[w] = v;
+  __syncthreads();
+  if (w == 0) {
+    OK x = l < nw ? sm[l] : OK{~0ull, ~0ull};
+    x = warp_min(x);
+    if (l == 0) sm[0] = x;
+  }
+  __syncthreads();
+  OK r = sm[0];
+  __syncthreads();
+  return r;
+}
+
+// numpy pairwise summation (numpy/_core/src/umath/loops_utils.h.src), field f of rcon
+__device__ double pw_sum(const double4 *a, int f, int n) {
+  if (n < 8) {
+    double res = 0.0;
+    for (int i = 0; i < n; i++) res += (&a[i].x)[f];
+    return res;
+  } else if (n <= 128) {
+    double r[8];
+    for (int j = 0; j < 8; j++) r[j] = (&a[j].x)[f];
+    int i;
+    for (i = 8; i < n - (n % 8); i += 8)
+      for (int j = 0; j < 8; j++) r[j] += (&a[i + j].x)[f];
+    double res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+    for (; i < n; i++) res += (&a[i].x)[f];
+    return res;
+  }
+  int n2 = n / 2;
+  n2 -= n2 % 8;
+  return pw_sum(a, f, n2) + pw_sum(a + n2, f, n - n2);
+}
+
+// ---------------------------------------------------------------------------
+// rebuild one individual (whole block): loc, tables, route terms, fleet
+// ---------------------------------------------------------------------------
+template <bool WIN>
+__device__ void rebuild_block(const DevInst &I, const DevPop &P, int b, int *sm_cnt) {
+  const int m = P.m[b];
+  int *LOC = P.loc + (size_t)b * P.N;
+  int4 *RM = P.rmeta + (size_t)b * P.J;
+  double4 *RC = P.rcon + (size_t)b * P.J;
+  for (int v = threadIdx.x; v < P.N; v += blockDim.x) LOC[v] = -1;
+  for (int d = threadIdx.x; d < P.ND; d += blockDim.x) sm_cnt[d] = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int r = wid; r < m; r += nw) {
+    int4 mt = RM[r];
+    int k = mt.x, n = k + (I.open ? 1 : 2);
+    const int *sq = P.seq + row_base(P, b, r);
+    for (int p = lane; p < k; p += 32) LOC[sq[p + 1]] = (r << 9) | p;
+    // lane i folds positions i..n-1 (left fold from i, batch.py:99-124)
+    for (int i = lane; i < n; i += 32) {
+      At<WIN> acc = a_node<WIN>(I, sq[i]);
+      if (i == 0) tab_store<WIN>(P, P.tabP, b, r, 0, acc);
+      for (int j = i + 1; j < n; j++) {
+        acc = a_cat<WIN>(I, acc, a_node<WIN>(I, sq[j]));
+        if (i == 0) tab_store<WIN>(P, P.tabP, b, r, j, acc);
+      }
+      tab_store<WIN>(P, P.tabS, b, r, i, acc);
+      if (i == 0) {
+        double o[5];
+        contrib<WIN>(I, acc, mt.y, mt.z, k, o);
+        RC[r] = make_double4(acc.dist, o[1], o[2], o[3]);  // route_D is the raw table value
+        RM[r].w = (int)o[4];
+      }
+    }
+    if (lane == 0 && k > 0) atomicAdd(&sm_cnt[mt.y], 1);
+  }
+  __syncthreads();
+  if (I.nv_on) {
+    double2 *FL = P.fleet + (size_t)b * P.ND;
+    for (int d = threadIdx.x; d < P.ND; d += blockDim.x) {
+      double c = (double)sm_cnt[d];
+      double over = npmax(c - I.NV, 0.0);
+      FL[d] = make_double2(npmax((c + 1.0) - I.NV, 0.0) - over, npmax((c - 1.0) - I.NV, 0.0) - over);
+    }
+    if (threadIdx.x == 0) {
+      double ex = 0.0;
+      for (int d = 0; d < P.ND; d++) ex += npmax((double)sm_cnt[d] - I.NV, 0.0);
+      P.fexcess[b] = ex;
+    }
+  } else if (threadIdx.x == 0) {
+    P.fexcess[b] = 0.0;
+  }
+  __syncthreads();
+}
+
+template <bool WIN>
+__global__ void __launch_bounds__(256) k_rebuild(DevInst I, DevPop P, int B) {
+  extern __shared__ int sm_cnt[];
+  int b = blockIdx.x;
+  if (b >= B) return;
+  rebuild_block<WIN>(I, P, b, sm_cnt);
+}
+
+// ---------------------------------------------------------------------------
+// plan: operator of the round per individual, flattened chunk offsets
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(1024) k_plan(DevInst I, DevPop P, LsParams L) {
+  __shared__ int wsum[32];
+  __shared__ int carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int base = 0; base < L.B; base += blockDim.x) {
+    int b = base + threadIdx.x;
+    int chunks = 0;
+    if (b < L.B) {
+      LsState st = P.st[b];
+      P.fcount[b] = 0;
+      P.nanflag[b] = 0;
+      if (!st.done && st.pass >= P.maxp) {
+        st.done = 1;
+        st.status = 5;
+        P.st[b] = st;
+      }
+      if (!st.done) {
+        int op = P.perms[((size_t)b * P.maxp + st.pass) * P.nops + st.pos];
+        long long items = op_items(op, P.m[b], I.NC, I.W, I.ND, I.win, I.open, P.K);
+        P.op_cur[b] = op;
+        P.wsize[b] = (int)items;
+        chunks = (int)((items + MDR_CHUNK - 1) / MDR_CHUNK);
+      } else {
+        P.wsize[b] = 0;
+      }
+    }
+    // block exclusive scan of chunks
+    int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    int x = chunks;
+#pragma unroll
+    for (int s = 1; s < 32; s <<= 1) {
+      int y = __shfl_up_sync(0xffffffffu, x, s);
+      if (lane >= s) x += y;
+    }
+    if (lane == 31) wsum[w] = x;
+    __syncthreads();
+    if (w == 0) {
+      int t = lane < (int)(blockDim.x >> 5) ? wsum[lane] : 0;
+#pragma unroll
+      for (int s = 1; s < 32; s <<= 1) {
+        int y = __shfl_up_sync(0xffffffffu, t, s);
+        if (lane >= s) t += y;
+      }
+      wsum[lane] = t;
+    }
+    __syncthreads();
+    int excl = x - chunks + (w > 0 ? wsum[w - 1] : 0) + carry;
+    if (b < L.B) P.chunk_off[b] = excl;
+    __syncthreads();
+    if (threadIdx.x == blockDim.x - 1) carry = excl + chunks;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    P.chunk_off[L.B] = carry;
+    *P.total_chunks = carry;
+    *P.active = 0;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// fused enumerate + evaluate + reduce
+// ---------------------------------------------------------------------------
+template <bool WIN>
+__global__ void __launch_bounds__(256) k_eval(DevInst I, DevPop P, LsParams L) {
+  __shared__ OK red[8];
+  __shared__ int sb;
+  __shared__ int scount[8];
+  const int total = *P.total_chunks;
+  for (int c = blockIdx.x; c < total; c += gridDim.x) {
+    if (threadIdx.x == 0) {
+      int lo = 0, hi = L.B - 1;  // last b with chunk_off[b] <= c and chunks > 0
+      while (lo < hi) {
+        int mid = (lo + hi + 1) >> 1;
+        if (P.chunk_off[mid] <= c) lo = mid; else hi = mid - 1;
+      }
+      sb = lo;
+    }
+    __syncthreads();
+    const int b = sb;
+    const int op = P.op_cur[b];
+    const int M = P.m[b];
+    const long long item = (long long)(c - P.chunk_off[b]) * MDR_CHUNK + threadIdx.x;
+    double lam[4];
+#pragma unroll
+    for (int i = 0; i < 4; i++) lam[i] = P.lam[b * 4 + i];
+    Cand cd;
+    bool valid = item < P.wsize[b] && decode_item(I, P, b, op, item, M, cd);
+    OK v{~0ull, ~0ull};
+    bool fol = false, isnan_ = false;
+    if (valid) {
+      Delta D = eval_cand<WIN>(I, P, b, op, cd, lam);
+      if (D.dF != D.dF) {
+        isnan_ = true;
+      } else {
+        v.o = ord_of(D.dF);
+        v.k = pack_key(cd);
+        fol = L.multi_move && follower_ok(D);
+      }
+    }
+    unsigned fm = __ballot_sync(0xffffffffu, fol);
+    if (fm) {
+      int lane = threadIdx.x & 31;
+      int base = 0;
+      if (lane == __ffs(fm) - 1) base = atomicAdd(&P.fcount[b], __popc(fm));
+      base = __shfl_sync(0xffffffffu, base, __ffs(fm) - 1);
+      if (fol) {
+        int at = base + __popc(fm & ((1u << lane) - 1));
+        if (at < P.Fcap) P.fol[(size_t)b * P.Fcap + at] = make_ulonglong2(v.o, v.k);
+      }
+    }
+    if (__any_sync(0xffffffffu, isnan_) && (threadIdx.x & 31) == 0) atomicOr(&P.nanflag[b], 1);
+    unsigned vm = __ballot_sync(0xffffffffu, valid);
+    if ((threadIdx.x & 31) == 0) scount[threadIdx.x >> 5] = __popc(vm);
+    OK r = block_min(v, red);
+    if (threadIdx.x == 0) {
+      P.partial[c] = make_ulonglong2(r.o, r.k);
+      int s = 0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); w++) s += scount[w];
+      if (s) atomicAdd(&P.cands[(size_t)b * 6 + op], (unsigned long long)s);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// select + apply + rebuild + adapt
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void put_range(int *dst, int &k, const int *src, int from, int to) {
+  for (int i = from; i < to; i++) dst[1 + k++] = src[1 + i];
+}
+
+// one move (route-disjoint from the others of the round); reads old rows
+// from scratch, writes the live rows (moves.move_plan, moves.py:88-148)
+__device__ bool apply_one(const DevInst &I, const DevPop &P, int b, int op, const Cand &c, int new_r) {
+  const int *S1 = P.scratch_seq + row_base(P, b, c.r1);
+  const int4 M1 = P.scratch_meta[(size_t)b * P.J + c.r1];
+  int *D1 = P.seq + row_base(P, b, c.r1);
+  int4 *RM = P.rmeta + (size_t)b * P.J;
+  const int K = P.K;
+  int k1 = M1.x;
+  int seg[2];
+  auto finish = [&](int *row, int r, int dep, int arr, int k) -> bool {
+    if (k > K) return false;
+    row[0] = dep;
+    if (!I.open) row[k + 1] = arr;
+    RM[r] = make_int4(k, dep, arr, 0);
+    return true;
+  };
+  switch (op) {
+    case 0: {
+      for (int i = 0; i < c.l1; i++) seg[i] = S1[1 + c.p1 + i];
+      if (c.rev1 && c.l1 == 2) { int t = seg[0]; seg[0] = seg[1]; seg[1] = t; }
+      if (c.r1 == c.r2) {
+        int at = c.p2 > c.p1 ? c.p2 - c.l1 : c.p2;
+        int k = 0, ri = 0;  // ri indexes "rest" = customers without the segment
+        for (int i = 0; i < k1 && k <= K; i++) {
+          if (i >= c.p1 && i < c.p1 + c.l1) continue;
+          if (ri == at) for (int s = 0; s < c.l1; s++) D1[1 + k++] = seg[s];
+          D1[1 + k++] = S1[1 + i];
+          ri++;
+        }
+        if (ri == at) for (int s = 0; s < c.l1; s++) D1[1 + k++] = seg[s];
+        return finish(D1, c.r1, M1.y, M1.z, k);
+      }
+      const int *S2 = P.scratch_seq + row_base(P, b, c.r2);
+      const int4 M2 = P.scratch_meta[(size_t)b * P.J + c.r2];
+      int *D2 = P.seq + row_base(P, b, c.r2);
+      int ka = 0;
+      put_range(D1, ka, S1, 0, c.p1);
+      put_range(D1, ka, S1, c.p1 + c.l1, k1);
+      if (!finish(D1, c.r1, M1.y, M1.z, ka)) return false;
+      if (M2.x + c.l1 > K) return false;
+      int kb = 0;
+      put_range(D2, kb, S2, 0, c.p2);
+      for (int s = 0; s < c.l1; s++) D2[1 + kb++] = seg[s];
+      put_range(D2, kb, S2, c.p2, M2.x);
+      return finish(D2, c.r2, M2.y, M2.z, kb);
+    }
+    case 1: {
+      int s1[2], s2[2];
+      const int *S2 = c.r1 == c.r2 ? S1 : P.scratch_seq + row_base(P, b, c.r2);
+      const int4 M2 = c.r1 == c.r2 ? M1 : P.scratch_meta[(size_t)b * P.J + c.r2];
+      for (int i = 0; i < c.l1; i++) s1[i] = S1[1 + c.p1 + i];
+      if (c.rev1 && c.l1 == 2) { int t = s1[0]; s1[0] = s1[1]; s1[1] = t; }
+      for (int i = 0; i < c.l2; i++) s2[i] = S2[1 + c.p2 + i];
+      if (c.rev2 && c.l2 == 2) { int t = s2[0]; s2[0] = s2[1]; s2[1] = t; }
+      if (c.r1 == c.r2) {
+        int k = 0;
+        put_range(D1, k, S1, 0, c.p1);
+        for (int s = 0; s < c.l2; s++) D1[1 + k++] = s2[s];
+        put_range(D1, k, S1, c.p1 + c.l1, c.p2);
+        for (int s = 0; s < c.l1; s++) D1[1 + k++] = s1[s];
+        put_range(D1, k, S1, c.p2 + c.l2, k1);
+        return finish(D1, c.r1, M1.y, M1.z, k);
+      }
+      if (k1 - c.l1 + c.l2 > K || M2.x - c.l2 + c.l1 > K) return false;
+      int *D2 = P.seq + row_base(P, b, c.r2);
+      int ka = 0, kb = 0;
+      put_range(D1, ka, S1, 0, c.p1);
+      for (int s = 0; s < c.l2; s++) D1[1 + ka++] = s2[s];
+      put_range(D1, ka, S1, c.p1 + c.l1, k1);
+      put_range(D2, kb, S2, 0, c.p2);
+      for (int s = 0; s < c.l1; s++) D2[1 + kb++] = s1[s];
+      put_range(D2, kb, S2, c.p2 + c.l2, M2.x);
+      return finish(D1, c.r1, M1.y, M1.z, ka) && finish(D2, c.r2, M2.y, M2.z, kb);
+    }
+    case 3: {
+      int k = 0;
+      put_range(D1, k, S1, 0, c.p1);
+      for (int i = c.p2; i >= c.p1; i--) D1[1 + k++] = S1[1 + i];
+      put_range(D1, k, S1, c.p2 + 1, k1);
+      return finish(D1, c.r1, M1.y, M1.z, k);
+    }
+    case 2: {
+      const int *S2 = P.scratch_seq + row_base(P, b, c.r2);
+      const int4 M2 = P.scratch_meta[(size_t)b * P.J + c.r2];
+      int *D2 = P.seq + row_base(P, b, c.r2);
+      int ka = c.p1 + (M2.x - c.p2), kb = c.p2 + (k1 - c.p1);
+      if (ka > K || kb > K) return false;
+      ka = 0; kb = 0;
+      put_range(D1, ka, S1, 0, c.p1);
+      put_range(D1, ka, S2, c.p2, M2.x);
+      put_range(D2, kb, S2, 0, c.p2);
+      put_range(D2, kb, S1, c.p1, k1);
+      return finish(D1, c.r1, M1.y, M2.z, ka) && finish(D2, c.r2, M2.y, M1.z, kb);
+    }
+    case 4: {
+      if (new_r >= P.J) return false;
+      int *DN = P.seq + row_base(P, b, new_r);
+      int ka = 0, kn = 0;
+      put_range(DN, kn, S1, c.p1, k1);
+      put_range(D1, ka, S1, 0, c.p1);
+      return finish(D1, c.r1, M1.y, M1.z, ka) && finish(DN, new_r, c.depot, c.depot, kn);
+    }
+    default: {
+      int dep = (c.mode == 0 || c.mode == 2) ? c.depot : M1.y;
+      int arr = (c.mode == 1 || c.mode == 2) ? c.depot : M1.z;
+      int k = 0;
+      put_range(D1, k, S1, 0, k1);
+      return finish(D1, c.r1, dep, arr, k);
+    }
+  }
+}
+
+template <bool WIN>
+__global__ void __launch_bounds__(256) k_select(DevInst I, DevPop P, LsParams L) {
+  extern __shared__ unsigned long long smx[];
+  __shared__ OK red[8];
+  __shared__ int s_flag, s_nm, s_mnew, s_snap;
+  __shared__ unsigned long long s_leader;
+  const int b = blockIdx.x;
+  if (b >= L.B) return;
+  if (P.st[b].done) return;
+  const int J = P.J;
+  unsigned long long *sel = smx;                            // [J] selected keys
+  unsigned *used = reinterpret_cast<unsigned *>(sel + J);   // [J/32+1] route bitmask
+  int *newidx = reinterpret_cast<int *>(used + (J / 32 + 1));  // [J+J]
+  int *sm_cnt = newidx + 2 * J;                             // [ND]
+  const int op = P.op_cur[b];
+
+  // ---- leader (batch.py:587-597): min (dF, key) over the chunk partials
+  OK best{~0ull, ~0ull};
+  for (int c = P.chunk_off[b] + threadIdx.x; c < P.chunk_off[b + 1]; c += blockDim.x) {
+    ulonglong2 p = P.partial[c];
+    OK x{p.x, p.y};
+    if (ok_less(x, best)) best = x;
+  }
+  best = block_min(best, red);
+  const bool has = !P.nanflag[b] && best.o != ~0ull && unord(best.o) < -MDR_EPS;
+  const int nf = P.fcount[b];
+  if (threadIdx.x == 0) {
+    P.st[b].op_evals++;
+    s_flag = 0;
+    if (has && L.multi_move && nf > P.Fcap) s_flag = 1;  // follower buffer overflow
+  }
+  __syncthreads();
+  if (s_flag) {
+    if (threadIdx.x == 0) { P.st[b].done = 1; P.st[b].status = 3; }
+    return;
+  }
+  if (has) {
+    // ---- select_moves (localsearch.py:45-55): greedy in (dF, key) order ==
+    // repeated argmin over followers not touching used routes
+    for (int i = threadIdx.x; i < J / 32 + 1; i += blockDim.x) used[i] = 0u;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      s_leader = best.k;
+      sel[0] = best.k;
+      Cand c = unpack_key(best.k);
+      used[c.r1 >> 5] |= 1u << (c.r1 & 31);
+      if (c.r2 >= 0) used[c.r2 >> 5] |= 1u << (c.r2 & 31);
+      s_nm = 1;
+    }
+    __syncthreads();
+    if (L.multi_move) {
+      const ulonglong2 *F = P.fol + (size_t)b * P.Fcap;
+      for (;;) {
+        OK x{~0ull, ~0ull};
+        for (int i = threadIdx.x; i < nf; i += blockDim.x) {
+          ulonglong2 e = F[i];
+          if (e.y == s_leader) continue;
+          Cand c = unpack_key(e.y);
+          bool conflict = (used[c.r1 >> 5] >> (c.r1 & 31)) & 1u;
+          if (c.r2 >= 0) conflict = conflict || ((used[c.r2 >> 5] >> (c.r2 & 31)) & 1u);
+          OK y{e.x, e.y};
+          if (!conflict && ok_less(y, x)) x = y;
+        }
+        x = block_min(x, red);
+        if (x.o == ~0ull) break;
+        if (threadIdx.x == 0) {
+          sel[s_nm++] = x.k;
+          Cand c = unpack_key(x.k);
+          used[c.r1 >> 5] |= 1u << (c.r1 & 31);
+          if (c.r2 >= 0) used[c.r2 >> 5] |= 1u << (c.r2 & 31);
+        }
+        __syncthreads();
+      }
+    }
+    // ---- apply_moves (localsearch.py:58-82)
+    const int m = P.m[b];
+    const int nm = s_nm;
+    for (int i = threadIdx.x; i < m * P.Kp; i += blockDim.x) {
+      int r = i / P.Kp, q = i - r * P.Kp;
+      P.scratch_seq[row_base(P, b, r) + q] = P.seq[row_base(P, b, r) + q];
+    }
+    for (int r = threadIdx.x; r < m; r += blockDim.x)
+      P.scratch_meta[(size_t)b * J + r] = P.rmeta[(size_t)b * J + r];
+    if (threadIdx.x == 0) s_flag = 0;
+    __syncthreads();
+    for (int t = threadIdx.x; t < nm; t += blockDim.x) {
+      Cand c = unpack_key(sel[t]);
+      if (!apply_one(I, P, b, op, c, m + t)) s_flag = 1;
+    }
+    __syncthreads();
+    if (s_flag) {
+      if (threadIdx.x == 0) { P.st[b].done = 1; P.st[b].status = 3; }
+      return;
+    }
+    // drop_empty_routes (model.py:198-199), stable; DI tails were appended at m+t
+    const int m2 = m + (op == 4 ? nm : 0);
+    if (threadIdx.x < 32) {
+      int carry = 0;
+      for (int base = 0; base < m2; base += 32) {
+        int r = base + threadIdx.x;
+        bool keep = r < m2 && P.rmeta[(size_t)b * J + r].x > 0;
+        unsigned bal = __ballot_sync(0xffffffffu, keep);
+        if (r < m2) newidx[r] = keep ? carry + __popc(bal & ((1u << threadIdx.x) - 1)) : -1;
+        carry += __popc(bal);
+      }
+      if (threadIdx.x == 0) s_mnew = carry;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < m2 * P.Kp; i += blockDim.x) {
+      int r = i / P.Kp, q = i - r * P.Kp;
+      if (newidx[r] >= 0) P.scratch_seq[row_base(P, b, newidx[r]) + q] = P.seq[row_base(P, b, r) + q];
+    }
+    for (int r = threadIdx.x; r < m2; r += blockDim.x)
+      if (newidx[r] >= 0) P.scratch_meta[(size_t)b * J + newidx[r]] = P.rmeta[(size_t)b * J + r];
+    __syncthreads();
+    const int mn = s_mnew;
+    for (int i = threadIdx.x; i < mn * P.Kp; i += blockDim.x) {
+      int r = i / P.Kp, q = i - r * P.Kp;
+      P.seq[row_base(P, b, r) + q] = P.scratch_seq[row_base(P, b, r) + q];
+    }
+    for (int r = threadIdx.x; r < mn; r += blockDim.x)
+      P.rmeta[(size_t)b * J + r] = P.scratch_meta[(size_t)b * J + r];
+    if (threadIdx.x == 0) P.m[b] = mn;
+    __syncthreads();
+    rebuild_block<WIN>(I, P, b, sm_cnt);
+    // ---- totals, adapt_penalties, bookkeeping (localsearch.py:128-138)
+    if (threadIdx.x == 0) {
+      const double4 *RC = P.rcon + (size_t)b * J;
+      double tot[5];
+      tot[0] = pw_sum(RC, 0, mn);
+      tot[1] = pw_sum(RC, 1, mn);
+      tot[2] = pw_sum(RC, 2, mn);
+      tot[3] = pw_sum(RC, 3, mn);
+      double clo = 0.0;  // sum of 0/1 values: exact in any order
+      for (int r = 0; r < mn; r++) clo += (double)P.rmeta[(size_t)b * J + r].w;
+      tot[4] = I.theta * (clo + P.fexcess[b]);
+      LsState st = P.st[b];
+      bool feas = true;
+      for (int i = 0; i < 4; i++) {
+        double lm = P.lam[b * 4 + i];
+        bool viol = tot[i + 1] > 1e-9;
+        if (viol) { lm = lm / L.kappa; feas = false; }
+        else lm = lm * L.kappa;
+        double x = L.lam_min > lm ? L.lam_min : lm;
+        P.lam[b * 4 + i] = L.lam_max < x ? L.lam_max : x;
+      }
+      s_snap = 0;
+      if (feas) {
+        st.n_feasible++;
+        if (tot[0] < st.bestD) { st.bestD = tot[0]; st.n_improving++; s_snap = 1; }
+      }
+      st.accepted++;
+      st.any = 1;
+      st.moves_applied += nm;
+      if (st.accepted >= L.depth) st.done = 1;
+      P.st[b] = st;
+    }
+    __syncthreads();
+    if (s_snap) {
+      for (int i = threadIdx.x; i < mn * P.Kp; i += blockDim.x) {
+        int r = i / P.Kp, q = i - r * P.Kp;
+        P.best_seq[row_base(P, b, r) + q] = P.seq[row_base(P, b, r) + q];
+      }
+      for (int r = threadIdx.x; r < mn; r += blockDim.x)
+        P.best_meta[(size_t)b * J + r] = P.rmeta[(size_t)b * J + r];
+      if (threadIdx.x == 0) P.best_m[b] = mn;
+    }
+  }
+  // ---- advance the pass/operator cursor
+  if (threadIdx.x == 0) {
+    LsState st = P.st[b];
+    if (!st.done) {
+      st.pos++;
+      if (st.pos >= P.nops) {
+        if (!st.any) st.done = 1;
+        else { st.pass++; st.pos = 0; st.any = 0; }
+      }
+      P.st[b] = st;
+    }
+    if (!st.done) atomicAdd(P.active, 1);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// operator-level (parity) kernels
+// ---------------------------------------------------------------------------
+template <bool WIN>
+__global__ void k_eval_mat(DevInst I, DevPop P, int b, int op, MatCands C, const double *lamp, MatDeltas O) {
+  long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= C.n) return;
+  Cand c;
+  c.r1 = (int)C.r1[i]; c.p1 = (int)C.p1[i]; c.r2 = (int)C.r2[i]; c.p2 = (int)C.p2[i];
+  c.l1 = (int)C.len1[i]; c.l2 = (int)C.len2[i]; c.rev1 = C.rev1[i]; c.rev2 = C.rev2[i];
+  c.depot = (int)C.depot[i]; c.mode = (int)C.mode[i];
+  double lam[4] = {lamp[0], lamp[1], lamp[2], lamp[3]};
+  Delta D = eval_cand<WIN>(I, P, b, op, c, lam);
+  O.dD[i] = D.dD; O.dV1[i] = D.dV1; O.dV2[i] = D.dV2; O.dV3[i] = D.dV3; O.dV4[i] = D.dV4; O.dF[i] = D.dF;
+  O.fn[i] = (unsigned char)D.fn;
+}
+
+__global__ void k_emit(DevInst I, DevPop P, int b, int op, long long items, unsigned long long *keys) {
+  const int M = P.m[b];
+  for (long long it = (long long)blockIdx.x * blockDim.x + threadIdx.x; it < items;
+       it += (long long)gridDim.x * blockDim.x) {
+    Cand c;
+    keys[it] = decode_item(I, P, b, op, it, M, c) ? pack_key(c) : 0ull;
+  }
+}
+
+__global__ void k_totals(DevInst I, DevPop P, int b, double *out) {
+  const int m = P.m[b];
+  const double4 *RC = P.rcon + (size_t)b * P.J;
+  out[0] = pw_sum(RC, 0, m);
+  out[1] = pw_sum(RC, 1, m);
+  out[2] = pw_sum(RC, 2, m);
+  out[3] = pw_sum(RC, 3, m);
+  double clo = 0.0;
+  for (int r = 0; r < m; r++) clo += (double)P.rmeta[(size_t)b * P.J + r].w;
+  out[4] = I.theta * (clo + P.fexcess[b]);
+}
+
+__global__ void k_lf_prep(MatCands C, MatDeltas D, unsigned long long *ord, unsigned long long *key,
+                          unsigned char *flag, int *nan) {
+  long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= C.n) return;
+  Cand c;
+  c.r1 = (int)C.r1[i]; c.p1 = (int)C.p1[i]; c.r2 = (int)C.r2[i]; c.p2 = (int)C.p2[i];
+  c.l1 = (int)C.len1[i]; c.l2 = (int)C.len2[i]; c.rev1 = C.rev1[i]; c.rev2 = C.rev2[i];
+  c.depot = (int)C.depot[i]; c.mode = (int)C.mode[i];
+  double f = D.dF[i];
+  if (f != f) atomicOr(nan, 1);
+  ord[i] = f != f ? ~0ull : ord_of(f);
+  key[i] = pack_key(c);
+  Delta d;
+  d.dD = D.dD[i]; d.dV1 = D.dV1[i]; d.dV2 = D.dV2[i]; d.dV3 = D.dV3[i]; d.dV4 = D.dV4[i]; d.fn = D.fn[i];
+  flag[i] = follower_ok(d) ? 1 : 0;
+}
+
+// ---------------------------------------------------------------------------
+// host <-> device solution transfer (flat layout of mdr_pop_upload)
+// ---------------------------------------------------------------------------
+__global__ void k_unpack(DevInst I, DevPop P, int B, const int *rbase, const int *coff, const int *cust,
+                         const int *dep, const int *arr) {
+  int b = blockIdx.x;
+  if (b >= B) return;
+  int r0 = rbase[b], m = rbase[b + 1] - r0;
+  if (threadIdx.x == 0) P.m[b] = m;
+  for (int r = threadIdx.x >> 5; r < m; r += blockDim.x >> 5) {
+    int c0 = coff[r0 + r], k = coff[r0 + r + 1] - c0;
+    int *row = P.seq + row_base(P, b, r);
+    for (int p = threadIdx.x & 31; p < k; p += 32) row[p + 1] = cust[c0 + p];
+    if ((threadIdx.x & 31) == 0) {
+      row[0] = dep[r0 + r];
+      if (!I.open) row[k + 1] = arr[r0 + r];
+      P.rmeta[(size_t)b * P.J + r] = make_int4(k, dep[r0 + r], arr[r0 + r], 0);
+    }
+  }
+}
+
+// one CTA: flat arrays of all B individuals; hdr = {routes, customers}
+__global__ void __launch_bounds__(1024) k_pack(DevPop P, int B, int best, int *rbase, int *coff, int *cust,
+                                               int *dep, int *arr, int *hdr, int cap_r, int cap_c) {
+  __shared__ int s_r, s_c;
+  const int *M = best ? P.best_m : P.m;
+  const int4 *RM = best ? P.best_meta : P.rmeta;
+  const int *SQ = best ? P.best_seq : P.seq;
+  if (threadIdx.x == 0) {
+    int r = 0, c = 0;
+    for (int b = 0; b < B; b++) {
+      rbase[b] = r;
+      for (int q = 0; q < M[b]; q++) c += RM[(size_t)b * P.J + q].x;
+      r += M[b];
+    }
+    rbase[B] = r;
+    s_r = r; s_c = c;
+    hdr[0] = r; hdr[1] = c;
+  }
+  __syncthreads();
+  if (s_r > cap_r || s_c > cap_c) return;
+  // route-level offsets: one warp per individual
+  for (int b = threadIdx.x >> 5; b < B; b += blockDim.x >> 5) {
+    int lane = threadIdx.x & 31;
+    int r0 = rbase[b];
+    int cbase = 0;
+    if (lane == 0) {
+      // customer offset of individual b: routes before r0
+      int c = 0;
+      for (int bb = 0; bb < b; bb++)
+        for (int q = 0; q < M[bb]; q++) c += RM[(size_t)bb * P.J + q].x;
+      cbase = c;
+    }
+    cbase = __shfl_sync(0xffffffffu, cbase, 0);
+    int c = cbase;
+    for (int q = 0; q < M[b]; q++) {
+      int4 mt = RM[(size_t)b * P.J + q];
+      const int *row = SQ + ((size_t)b * P.J + q) * P.Kp;
+      for (int p = lane; p < mt.x; p += 32) cust[c + p] = row[p + 1];
+      if (lane == 0) {
+        coff[r0 + q] = c;
+        dep[r0 + q] = mt.y;
+        arr[r0 + q] = mt.z;
+      }
+      c += mt.x;
+    }
+    if (b == B - 1 && lane == 0) coff[r0 + M[b]] = c;
+  }
+  if (threadIdx.x == 0 && B > 0 && s_r == 0) coff[0] = 0;
+}
+
+// ---------------------------------------------------------------------------
+// launchers
+// ---------------------------------------------------------------------------
+static size_t select_smem(const DevPop &P) {
+  return sizeof(unsigned long long) * P.J + sizeof(unsigned) * (P.J / 32 + 1) + sizeof(int) * (2 * P.J + P.ND + 4);
+}
+
+void launch_rebuild(const DevInst &I, const DevPop &P, int B, bool win, cudaStream_t s) {
+  size_t sm = sizeof(int) * (P.ND + 1);
+  if (win) k_rebuild<true><<<B, 256, sm, s>>>(I, P, B);
+  else k_rebuild<false><<<B, 256, sm, s>>>(I, P, B);
+}
+
+void launch_plan(const DevInst &I, const DevPop &P, const LsParams &L, cudaStream_t s) {
+  k_plan<<<1, 1024, 0, s>>>(I, P, L);
+}
+
+int eval_grid_size(bool win) {
+  int dev = 0, sms = 148, per = 1;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (win) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_eval<true>, 256, 0);
+  else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_eval<false>, 256, 0);
+  if (per < 1) per = 1;
+  return sms * per;
+}
+
+void launch_eval(const DevInst &I, const DevPop &P, const LsParams &L, int grid, bool win, cudaStream_t s) {
+  if (win) k_eval<true><<<grid, 256, 0, s>>>(I, P, L);
+  else k_eval<false><<<grid, 256, 0, s>>>(I, P, L);
+}
+
+void launch_select(const DevInst &I, const DevPop &P, const LsParams &L, bool win, cudaStream_t s) {
+  size_t sm = select_smem(P);
+  if (win) {
+    if (sm > 48 * 1024) cudaFuncSetAttribute(k_select<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    k_select<true><<<L.B, 256, sm, s>>>(I, P, L);
+  } else {
+    if (sm > 48 * 1024) cudaFuncSetAttribute(k_select<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    k_select<false><<<L.B, 256, sm, s>>>(I, P, L);
+  }
+}
+
+void launch_eval_mat(const DevInst &I, const DevPop &P, int b, int op, const MatCands &c, const double *lam,
+                     MatDeltas out, bool win, cudaStream_t s) {
+  if (c.n == 0) return;
+  int blocks = (int)((c.n + 255) / 256);
+  if (win) k_eval_mat<true><<<blocks, 256, 0, s>>>(I, P, b, op, c, lam, out);
+  else k_eval_mat<false><<<blocks, 256, 0, s>>>(I, P, b, op, c, lam, out);
+}
+
+void launch_emit(const DevInst &I, const DevPop &P, int b, int op, long long items, unsigned long long *keys,
+                 cudaStream_t s) {
+  if (items == 0) return;
+  long long blocks = (items + 255) / 256;
+  if (blocks > 65535) blocks = 65535;
+  k_emit<<<(int)blocks, 256, 0, s>>>(I, P, b, op, items, keys);
+}
+
+void launch_totals(const DevInst &I, const DevPop &P, int b, double *out, cudaStream_t s) {
+  k_totals<<<1, 1, 0, s>>>(I, P, b, out);
+}
+
+void launch_unpack(const DevInst &I, const DevPop &P, int B, const int *rbase, const int *coff, const int *cust,
+                   const int *dep, const int *arr, cudaStream_t s) {
+  k_unpack<<<B, 256, 0, s>>>(I, P, B, rbase, coff, cust, dep, arr);
+}
+
+void launch_pack(const DevPop &P, int B, int best, int *rbase, int *coff, int *cust, int *dep, int *arr, int *hdr,
+                 int cap_r, int cap_c, cudaStream_t s) {
+  k_pack<<<1, 1024, 0, s>>>(P, B, best, rbase, coff, cust, dep, arr, hdr, cap_r, cap_c);
+}
+
+void launch_lf_prep(const MatCands &c, const MatDeltas &d, unsigned long long *ord, unsigned long long *key,
+                    unsigned char *flag, int *nan, cudaStream_t s) {
+  if (c.n == 0) return;
+  k_lf_prep<<<(int)((c.n + 255) / 256), 256, 0, s>>>(c, d, ord, key, flag, nan);
+}
+
+}  // namespace mdr

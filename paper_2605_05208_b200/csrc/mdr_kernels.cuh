@@ -1,0 +1,35 @@
+// mdr_kernels.cuh -- kernel launchers shared by mdr_api.cu
+#pragma once
+#include "mdr_device.cuh"
+
+namespace mdr {
+
+struct MatCands {  // device SoA of a materialised CandidateSet
+  const long long *r1, *p1, *r2, *p2, *len1, *len2, *depot, *mode;
+  const unsigned char *rev1, *rev2;
+  long long n;
+};
+
+struct MatDeltas {
+  double *dD, *dV1, *dV2, *dV3, *dV4, *dF;
+  unsigned char *fn;
+};
+
+void launch_rebuild(const DevInst &I, const DevPop &P, int B, bool win, cudaStream_t s);
+void launch_plan(const DevInst &I, const DevPop &P, const LsParams &L, cudaStream_t s);
+void launch_eval(const DevInst &I, const DevPop &P, const LsParams &L, int grid, bool win, cudaStream_t s);
+void launch_select(const DevInst &I, const DevPop &P, const LsParams &L, bool win, cudaStream_t s);
+void launch_eval_mat(const DevInst &I, const DevPop &P, int b, int op, const MatCands &c, const double *lam,
+                     MatDeltas out, bool win, cudaStream_t s);
+void launch_emit(const DevInst &I, const DevPop &P, int b, int op, long long items, unsigned long long *keys,
+                 cudaStream_t s);
+void launch_totals(const DevInst &I, const DevPop &P, int b, double *out, cudaStream_t s);
+void launch_lf_prep(const MatCands &c, const MatDeltas &d, unsigned long long *ord, unsigned long long *key,
+                    unsigned char *flag, int *nan, cudaStream_t s);
+int eval_grid_size(bool win);
+void launch_unpack(const DevInst &I, const DevPop &P, int B, const int *rbase, const int *coff, const int *cust,
+                   const int *dep, const int *arr, cudaStream_t s);
+void launch_pack(const DevPop &P, int B, int best, int *rbase, int *coff, int *cust, int *dep, int *arr, int *hdr,
+                 int cap_r, int cap_c, cudaStream_t s);
+
+}  // namespace mdr

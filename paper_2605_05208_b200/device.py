@@ -1,0 +1,277 @@
+"""Device-resident instance and population handles (libmdr_sm100 C-ABI).
+
+`DeviceInstance` uploads an instance once per GPU: distance/time matrix,
+node attributes, fleet/capacity/duration scalars, Gamma/Theta and the
+granular neighbour lists (mdr_instance_create).  `Population` owns B
+individuals' route storage and subsequence tables on that GPU
+(mdr_pop_create / upload / download) and runs the batched local search.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+import weakref
+
+import numpy as np
+
+from . import _lib
+from ._lib import (Cands, CapacityError, Deltas, InstanceDesc, LsCfg, LsStats, Timing, check, f64p, i32p,
+                   i64p, ptr, u8p)
+
+
+def _cur_stream(device: int):
+    """Handle of torch's current stream on `device` (0 = legacy default)."""
+    try:
+        import torch
+        if torch.cuda.is_available():
+            return C.c_void_p(torch.cuda.current_stream(device).cuda_stream)
+    except Exception:  # torch optional for plain C-ABI users
+        pass
+    return C.c_void_p(0)
+
+
+class DeviceInstance:
+    def __init__(self, inst, consts, nbr=None, device: int = 0):
+        L = _lib.lib()
+        self.device = device
+        self.n_nodes = int(inst.n_nodes)
+        self.n_depots = int(inst.n_depots)
+        self.has_windows = bool(inst.has_windows)
+        self.open_routes = bool(inst.open_routes)
+        self._dist = np.ascontiguousarray(inst.dist, dtype=np.float64)
+        same = inst.time is inst.dist
+        self._time = self._dist if same else np.ascontiguousarray(inst.time, dtype=np.float64)
+        self._demand = np.ascontiguousarray(inst.demand, np.float64)
+        self._service = np.ascontiguousarray(inst.service, np.float64)
+        self._e = np.ascontiguousarray(inst.tw_early, np.float64)
+        self._l = np.ascontiguousarray(inst.tw_late, np.float64)
+        if nbr is not None:
+            self._lists = np.ascontiguousarray(nbr.lists, np.int32)
+        else:
+            self._lists = np.full((self.n_nodes, 1), -1, np.int32)
+        self.width = int(self._lists.shape[1])
+        d = InstanceDesc()
+        d.n_nodes, d.n_depots = self.n_nodes, self.n_depots
+        d.dist, d.time = ptr(self._dist, f64p), ptr(self._time, f64p)
+        d.demand, d.service = ptr(self._demand, f64p), ptr(self._service, f64p)
+        d.tw_early, d.tw_late = ptr(self._e, f64p), ptr(self._l, f64p)
+        d.capacity = float(inst.capacity)
+        d.max_duration = float(inst.max_duration)
+        d.fleet_per_depot = float(inst.fleet_per_depot)
+        d.open_routes, d.has_windows = int(self.open_routes), int(self.has_windows)
+        d.gamma, d.theta = float(consts.gamma), float(consts.theta)
+        d.lists, d.width = ptr(self._lists, i32p), self.width
+        h = C.c_void_p()
+        check(L.mdr_instance_create(C.byref(d), device, C.byref(h)), "mdr_instance_create")
+        self.handle = h
+        self._fin = weakref.finalize(self, L.mdr_instance_destroy, h)
+
+
+def flatten_population(sols):
+    """B solutions -> (rbase, coff, cust, dep, arr) int32 arrays."""
+    rb = [0]
+    coff = [0]
+    cust, dep, arr = [], [], []
+    for s in sols:
+        for r in s.routes:
+            cust.extend(r.customers)
+            coff.append(len(cust))
+            dep.append(r.depart)
+            arr.append(r.arrive)
+        rb.append(len(dep))
+    f = lambda x: np.ascontiguousarray(np.asarray(x, dtype=np.int32).reshape(-1)) if len(x) else np.zeros(1, np.int32)
+    return (np.asarray(rb, np.int32), np.asarray(coff, np.int32), f(cust), f(dep), f(arr))
+
+
+class Population:
+    """B individuals resident on one GPU."""
+
+    def __init__(self, dinst: DeviceInstance, B_cap: int, J_cap: int, K_cap: int, F_cap: int = 1 << 15):
+        L = _lib.lib()
+        self.dinst = dinst
+        self.B_cap, self.J_cap, self.K_cap, self.F_cap = B_cap, J_cap, K_cap, F_cap
+        h = C.c_void_p()
+        check(L.mdr_pop_create(dinst.handle, B_cap, J_cap, K_cap, F_cap, C.byref(h)), "mdr_pop_create")
+        self.handle = h
+        self._fin = weakref.finalize(self, L.mdr_pop_destroy, h)
+        self.B = 0
+        self.n_cust = 0
+
+    @staticmethod
+    def caps_for(sols, inst):
+        m = max((len(s.routes) for s in sols), default=1)
+        k = max((len(r.customers) for s in sols for r in s.routes), default=1)
+        J = min(2046, max(2 * m, m + 64))
+        K = min(500, max(2 * k, k + 16, 32))
+        return J, K
+
+    def upload(self, sols, lams, stream=None):
+        rbase, coff, cust, dep, arr = flatten_population(sols)
+        lam = np.ascontiguousarray(np.asarray(lams, np.float64).reshape(-1, 4))
+        B = len(sols)
+        s = stream if stream is not None else _cur_stream(self.dinst.device)
+        check(_lib.lib().mdr_pop_upload(self.handle, B, ptr(rbase, i32p), ptr(coff, i32p), ptr(cust, i32p),
+                                        ptr(dep, i32p), ptr(arr, i32p), ptr(lam, f64p), s), "mdr_pop_upload")
+        self.B = B
+        self.n_cust = int(coff[-1])
+        self.h2d_bytes = sum(a.nbytes for a in (rbase, coff, cust, dep, arr, lam))
+
+    def _download(self, best: bool, stream=None):
+        B = self.B
+        cap_r = B * self.J_cap
+        cap_c = max(self.n_cust, 1) + 16
+        rbase = np.zeros(B + 1, np.int32)
+        coff = np.zeros(cap_r + 1, np.int32)
+        cust = np.zeros(cap_c, np.int32)
+        dep = np.zeros(max(cap_r, 1), np.int32)
+        arr = np.zeros(max(cap_r, 1), np.int32)
+        nr, nc = C.c_int32(cap_r), C.c_int32(cap_c)
+        s = stream if stream is not None else _cur_stream(self.dinst.device)
+        L = _lib.lib()
+        if best:
+            extra = np.zeros(max(B, 1), np.float64)
+            rc = L.mdr_pop_download_best(self.handle, ptr(rbase, i32p), ptr(coff, i32p), ptr(cust, i32p),
+                                         ptr(dep, i32p), ptr(arr, i32p), ptr(extra, f64p), C.byref(nr),
+                                         C.byref(nc), s)
+        else:
+            extra = np.zeros(max(B, 1) * 4, np.float64)
+            rc = L.mdr_pop_download(self.handle, ptr(rbase, i32p), ptr(coff, i32p), ptr(cust, i32p),
+                                    ptr(dep, i32p), ptr(arr, i32p), ptr(extra, f64p), C.byref(nr), C.byref(nc), s)
+        check(rc, "mdr_pop_download")
+        self.d2h_bytes = int(rbase.nbytes + 4 * (nr.value + 1) + 4 * nc.value + 8 * nr.value + extra.nbytes)
+        out = []
+        for b in range(B):
+            routes = []
+            for r in range(rbase[b], rbase[b + 1]):
+                routes.append((int(dep[r]), int(arr[r]), cust[coff[r]:coff[r + 1]].tolist()))
+            out.append(routes)
+        return out, extra
+
+    def download(self, stream=None):
+        """[(depart, arrive, customers)] per individual, lam [B,4]."""
+        routes, lam = self._download(False, stream)
+        return routes, lam.reshape(-1, 4)[:self.B]
+
+    def download_best(self, stream=None):
+        routes, bestD = self._download(True, stream)
+        return routes, bestD[:self.B]
+
+    def local_search(self, perms: np.ndarray, depth: int, multi_move: bool, kappa: float, lam_min: float,
+                     lam_max: float, deadline_s: float = -1.0, rounds_per_sync: int = 8, stream=None):
+        """perms: uint8 [B, max_passes, n_ops]. Returns a list of per-individual stats dicts."""
+        B = self.B
+        perms = np.ascontiguousarray(perms, dtype=np.uint8)
+        assert perms.shape[0] == B
+        cfg = LsCfg()
+        cfg.depth, cfg.multi_move = int(depth), int(bool(multi_move))
+        cfg.kappa, cfg.lam_min, cfg.lam_max = float(kappa), float(lam_min), float(lam_max)
+        cfg.max_passes, cfg.n_ops = perms.shape[1], perms.shape[2]
+        cfg.perms = ptr(perms, u8p)
+        cfg.deadline_s = float(deadline_s)
+        cfg.rounds_per_sync = int(rounds_per_sync)
+        cfg.use_graph = 0
+        st = (LsStats * max(B, 1))()
+        s = stream if stream is not None else _cur_stream(self.dinst.device)
+        rc = _lib.lib().mdr_local_search(self.handle, C.byref(cfg), st, s)
+        stats = [dict(passes=x.passes, accepted=x.accepted, op_evals=x.op_evals, status=x.status,
+                      cands=list(x.cands), moves_applied=x.moves_applied, n_feasible=x.n_feasible,
+                      n_improving=x.n_improving, best_feasible_D=x.best_feasible_D) for x in st[:B]]
+        check(rc, "mdr_local_search")
+        return stats
+
+    def set_profiling(self, on: bool):
+        check(_lib.lib().mdr_set_profiling(self.handle, int(on)))
+
+    def timing(self) -> dict:
+        t = Timing()
+        check(_lib.lib().mdr_get_timing(self.handle, C.byref(t)))
+        return {f: getattr(t, f) for f, _ in Timing._fields_}
+
+    # ---- operator-level -----------------------------------------------------
+    def count(self, b: int, op: int) -> int:
+        n = _lib.lib().mdr_count(self.handle, b, op)
+        if n < 0:
+            check(_lib.MDR_ERR_ARG, "mdr_count")
+        return int(n)
+
+    def enumerate(self, b: int, op: int) -> dict:
+        n = self.count(b, op)
+        arrs = {f: np.zeros(max(n, 1), np.int64) for f in ("r1", "p1", "r2", "p2", "len1", "len2", "depot", "mode")}
+        arrs["rev1"] = np.zeros(max(n, 1), np.uint8)
+        arrs["rev2"] = np.zeros(max(n, 1), np.uint8)
+        cs = cands_struct(arrs, n)
+        check(_lib.lib().mdr_enumerate(self.handle, b, op, C.byref(cs)), "mdr_enumerate")
+        out = {f: a[:cs.n] for f, a in arrs.items()}
+        out["rev1"] = out["rev1"].astype(bool)
+        out["rev2"] = out["rev2"].astype(bool)
+        return out
+
+    def evaluate(self, b: int, op: int, cands: dict, lam) -> dict:
+        arrs = as_cand_arrays(cands)
+        n = len(arrs["r1"])
+        cs = cands_struct(arrs, n)
+        out = {f: np.zeros(max(n, 1)) for f in ("dD", "dV1", "dV2", "dV3", "dV4", "dF")}
+        out["fleet_neutral"] = np.zeros(max(n, 1), np.uint8)
+        d = deltas_struct(out)
+        lam_a = np.ascontiguousarray(lam, np.float64)
+        check(_lib.lib().mdr_evaluate(self.handle, b, op, C.byref(cs), ptr(lam_a, f64p), C.byref(d)),
+              "mdr_evaluate")
+        res = {f: a[:n] for f, a in out.items()}
+        res["fleet_neutral"] = res["fleet_neutral"].astype(bool)
+        return res
+
+    def leader_followers(self, cands: dict, deltas: dict, multi_move: bool):
+        arrs = as_cand_arrays(cands)
+        n = len(arrs["r1"])
+        cs = cands_struct(arrs, n)
+        dd = {f: np.ascontiguousarray(deltas[f], np.float64) for f in ("dD", "dV1", "dV2", "dV3", "dV4", "dF")}
+        dd["fleet_neutral"] = np.ascontiguousarray(deltas["fleet_neutral"], np.uint8)
+        d = deltas_struct(dd)
+        lead = C.c_int64(-1)
+        fol = np.zeros(max(n, 1), np.int64)
+        nf = C.c_int64(0)
+        check(_lib.lib().mdr_leader_followers(self.handle, C.byref(cs), C.byref(d), int(bool(multi_move)),
+                                              C.byref(lead), ptr(fol, i64p), C.byref(nf)), "mdr_leader_followers")
+        return int(lead.value), fol[:nf.value]
+
+    def totals(self, b: int):
+        out = np.zeros(5)
+        check(_lib.lib().mdr_totals(self.handle, b, ptr(out, f64p)), "mdr_totals")
+        return tuple(float(x) for x in out)
+
+
+CAND_FIELDS = ("r1", "p1", "r2", "p2", "len1", "len2", "rev1", "rev2", "depot", "mode")
+
+
+def as_cand_arrays(cands) -> dict:
+    get = (lambda f: cands[f]) if isinstance(cands, dict) else (lambda f: getattr(cands, f))
+    out = {}
+    for f in CAND_FIELDS:
+        a = np.asarray(get(f))
+        out[f] = np.ascontiguousarray(a, dtype=np.uint8 if f.startswith("rev") else np.int64)
+        if out[f].size == 0:
+            out[f] = np.zeros(1, out[f].dtype)[:0]
+    return out
+
+
+def cands_struct(arrs: dict, n: int) -> Cands:
+    keep = {}
+    for f, a in arrs.items():
+        if a.size == 0:
+            a = np.zeros(1, a.dtype)
+        keep[f] = a
+    cs = Cands()
+    cs.n = n
+    for f in ("r1", "p1", "r2", "p2", "len1", "len2", "depot", "mode"):
+        setattr(cs, f, ptr(keep[f], i64p))
+    cs.rev1, cs.rev2 = ptr(keep["rev1"], u8p), ptr(keep["rev2"], u8p)
+    cs._keep = keep
+    return cs
+
+
+def deltas_struct(out: dict) -> Deltas:
+    d = Deltas()
+    for f in ("dD", "dV1", "dV2", "dV3", "dV4", "dF"):
+        setattr(d, f, ptr(out[f], f64p))
+    d.fleet_neutral = ptr(out["fleet_neutral"], u8p)
+    return d

@@ -1,0 +1,212 @@
+"""Best-improvement multi-move local search on the GPU (mirrors `mdroute.localsearch`).
+
+`local_search` keeps the reference signature (localsearch.py:97-140) and runs
+the whole descent on the device: per round every active individual evaluates
+one operator of its pre-drawn permutation stream (the exact `rng.shuffle`
+results, drawn from a clone of the caller's rng), the leader and its
+route-disjoint followers are selected and applied on the device, the tables
+are rebuilt and the penalty coefficients adapted -- with no host round trip.
+
+`local_search_population` is the B200 addition: B independent descents
+(e.g. a GA generation's offspring) advance together in the same kernels.
+Each individual's trajectory is bit-identical to a separate reference call.
+"""
+from __future__ import annotations
+
+import random
+import time
+from dataclasses import dataclass
+from typing import Optional
+
+import numpy as np
+
+from ._lib import CapacityError
+from .batch import SolutionCache, evaluate_candidates, leader_and_followers
+from .device import Population
+from .moves import ALL_OPS, Op, move_plan
+from .session import session_for
+
+VIOLATION_TOL = 1e-9
+
+
+@dataclass
+class SearchConfig:
+    depth: int = 500
+    multi_move: bool = False
+
+    def __post_init__(self):
+        if self.depth < 1:
+            raise ValueError("depth must be >= 1")
+
+
+def enabled_operators(inst) -> list:
+    ops = list(ALL_OPS)
+    if inst.has_windows:
+        ops.remove(Op.TWO_OPT)
+    return ops
+
+
+def evaluate_batch(sol, cands, penalties, consts, inst, cache=None, multi_move: bool = True):
+    if cache is None:
+        cache = SolutionCache(sol, inst, consts)
+    deltas = evaluate_candidates(cache, cands, penalties)
+    return leader_and_followers(cache, cands, deltas, multi_move)
+
+
+def select_moves(leader, followers) -> list:
+    """Greedy route-disjoint selection (localsearch.py:45-55)."""
+    chosen = [leader]
+    used = leader.routes_touched()
+    for mv in followers:
+        t = mv.routes_touched()
+        if used & t:
+            continue
+        chosen.append(mv)
+        used |= t
+    return chosen
+
+
+def apply_moves(sol, moves, inst) -> None:
+    """Host twin of the device apply (localsearch.py:58-82)."""
+    used: set = set()
+    for mv in moves:
+        t = mv.routes_touched()
+        if used & t:
+            raise ValueError("conflicting moves: route sets intersect")
+        used |= t
+    plans = [move_plan(sol, mv, inst) for mv in moves]
+    route_cls = type(sol.routes[0]) if sol.routes else None
+    new_routes = []
+    for ps in plans:
+        for p in ps:
+            if p.route_index is None:
+                new_routes.append(route_cls(p.depart, p.arrive, p.customers))
+            else:
+                r = sol.routes[p.route_index]
+                r.depart, r.arrive, r.customers = p.depart, p.arrive, p.customers
+                if hasattr(r, "attr"):
+                    r.attr = None
+    sol.routes.extend(nr for nr in new_routes if nr.customers)
+    sol.drop_empty_routes()
+
+
+def draw_permutations(rng, ops, n_passes: int) -> np.ndarray:
+    """The first n_passes `rng.shuffle(list(ops))` results, drawn on a clone."""
+    if not hasattr(rng, "getstate"):
+        raise TypeError("rng must be a random.Random (getstate/setstate) so the operator stream can be pre-drawn")
+    clone = random.Random()
+    clone.setstate(rng.getstate())
+    out = np.empty((n_passes, len(ops)), np.uint8)
+    for p in range(n_passes):
+        order = list(ops)
+        clone.shuffle(order)
+        out[p] = [int(o) for o in order]
+    return out
+
+
+def _advance(rng, ops, passes: int) -> None:
+    for _ in range(passes):
+        order = list(ops)
+        rng.shuffle(order)
+
+
+class DeviceSearch:
+    """Reusable device population for repeated batched descents."""
+
+    def __init__(self, inst, consts, nbr, device: int = 0):
+        self.session = session_for(inst, consts, nbr, device)
+        self.inst = inst
+        self.pop: Optional[Population] = None
+        self.last_stats = None
+
+    def _ensure(self, sols, scale: int = 1):
+        J, K = Population.caps_for(sols, self.inst)
+        J = min(2046, J * scale)
+        K = min(500, K * scale)
+        F = (1 << 15) * scale
+        p = self.pop
+        if p is None or p.B_cap < len(sols) or p.J_cap < J or p.K_cap < K or p.F_cap < F:
+            self.pop = None
+            p = self.pop = Population(self.session.dinst, max(len(sols), p.B_cap if p else 0), J, K, F)
+        return p
+
+    def run(self, sols, lams, perms, cfg: SearchConfig, kappa=0.5, lam_min=0.01, lam_max=1e4,
+            deadline_s: float = -1.0):
+        """Descents of all `sols` (not modified). Returns (routes, lams, stats)."""
+        scale = 1
+        while True:
+            pop = self._ensure(sols, scale)
+            pop.upload(sols, lams)
+            try:
+                stats = pop.local_search(perms, cfg.depth, cfg.multi_move, kappa, lam_min, lam_max, deadline_s)
+                break
+            except CapacityError:
+                if scale >= 16:
+                    raise
+                scale *= 2
+        routes, lam_out = pop.download()
+        self.last_stats = stats
+        return routes, lam_out, stats
+
+
+def _apply_result(sol, routes):
+    route_cls = type(sol.routes[0]) if sol.routes else None
+    if route_cls is None:
+        from .model import Route as route_cls
+    sol.routes = [route_cls(d, a, c) for d, a, c in routes]
+
+
+def local_search(sol, penalties, cfg: SearchConfig, nbr, consts, inst, rng, deadline: Optional[float] = None,
+                 on_feasible=None):
+    """Reference-compatible descent of one solution (in place), run on the GPU.
+
+    on_feasible(D, sol) is invoked once, after the descent, with the feasible
+    state of lowest D passed through (first reached on ties) -- the only state
+    a best-tracking callback such as engine.snapshot_feasible keeps.
+    """
+    search = _searcher(inst, consts, nbr)
+    ops = enabled_operators(inst)
+    perms = draw_permutations(rng, ops, cfg.depth + 1)[None]
+    dl = -1.0 if deadline is None else max(0.0, deadline - time.monotonic())
+    routes, lam, stats = search.run([sol], [penalties.lam], perms, cfg, penalties.kappa, penalties.lam_min,
+                                    penalties.lam_max, dl)
+    st = stats[0]
+    _advance(rng, ops, st["passes"])
+    _apply_result(sol, routes[0])
+    penalties.lam[:] = [float(x) for x in lam[0]]
+    if on_feasible is not None and st["n_feasible"] > 0:
+        best_routes, bestD = search.pop.download_best()
+        snap = sol.clone() if hasattr(sol, "clone") else None
+        if snap is not None:
+            _apply_result(snap, best_routes[0])
+            on_feasible(float(bestD[0]), snap)
+    return sol
+
+
+_SEARCHERS: dict = {}
+
+
+def _searcher(inst, consts, nbr, device: int = 0) -> DeviceSearch:
+    key = (id(inst), id(nbr), device)
+    s = _SEARCHERS.get(key)
+    if s is None or s.inst is not inst or s.session.nbr is not nbr:
+        s = _SEARCHERS[key] = DeviceSearch(inst, consts, nbr, device)
+    return s
+
+
+def local_search_population(sols, penalties, cfg: SearchConfig, nbr, consts, inst, rngs,
+                            deadline: Optional[float] = None, device: int = 0):
+    """B independent descents in one device run; solutions and penalty states
+    are updated in place.  Returns the per-individual stats."""
+    search = _searcher(inst, consts, nbr, device)
+    ops = enabled_operators(inst)
+    perms = np.stack([draw_permutations(r, ops, cfg.depth + 1) for r in rngs])
+    lams = [p.lam for p in penalties]
+    dl = -1.0 if deadline is None else max(0.0, deadline - time.monotonic())
+    p0 = penalties[0]
+    routes, lam, stats = search.run(sols, lams, perms, cfg, p0.kappa, p0.lam_min, p0.lam_max, dl)
+    for b, (sol, pen, rng) in enumerate(zip(sols, penalties, rngs)):
+        _advance(rng, ops, stats[b]["passes"])
+        _apply_result(sol, routes[b])
+        pen.lam[:] = [float(x) for x in lam[b]]
+    return stats
