@@ -610,7 +610,7 @@ int mdr_leader_followers(mdr_pop *p, const mdr_cands *cs, const mdr_deltas *d, i
       // stable LSD: sort by key, then by ord(dF)
       k_gather_u64<<<gb, 256, 0, s>>>(key, fidx, k1, nf);
       size_t t3 = 0;
-      CK(cub::DeviceRadixSort::SortPairs(nullptr, t3, k1, k2, fidx, fidx2, nf, 0, 56, s));
+      CK(cub::DeviceRadixSort::SortPairs(nullptr, t3, k1, k2, fidx, fidx2, nf, 0, 64, s));
       void *ts3 = nullptr;
       TA(ts3, t3 + 1);
       CK(cub::DeviceRadixSort::SortPairs(ts3, t3, k1, k2, fidx, fidx2, nf, 0, 56, s));
