@@ -1,0 +1,356 @@
+"""Benchmark: population-batched multi-move local search on B200 (sm_100a).
+
+Workload (BASELINE.json configs[3]): synthetic MDVRPTW,
+1000 customers x 10 depots, theta = 50, population 256 per GPU.  Individual i
+starts from initial_solution(..., random.Random(100 + i)) and descends with
+local_search(depth=500, multi_move=True, lambda=1, kappa=0.5, rng=Random(i)).
+
+One step = one complete population descent (every individual to its local
+optimum or depth 500).  Metric: move-evaluations per second (candidates
+scored, duplicates included, exactly as enumerate_candidates counts them),
+whole job; descents/s is reported beside it.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...   (population sharded: weak scaling)
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import random
+import statistics
+import subprocess
+import sys
+import time
+from concurrent.futures import ProcessPoolExecutor
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_2605_05208_b200 import workload as W  # noqa: E402
+from paper_2605_05208_b200.evaluation import PenaltyState, ScalingConstants  # noqa: E402
+from paper_2605_05208_b200.neighborhood import NeighborConfig, build  # noqa: E402
+
+# algorithmic bytes per candidate (fp64 table pieces,
+# node pieces, distance links, old-route terms, descriptor), inter-route
+# figures for relocate/swap.  Windows (C2, C4) / no windows (C1, C3, C5).
+ALG_BYTES_WIN = {0: 436, 1: 500, 2: 372, 3: 0, 4: 304, 5: 204}
+ALG_BYTES_NOWIN = {0: 316, 1: 356, 2: 276, 3: 204, 4: 208, 5: 148}
+
+
+def _init_one(args):
+    name, i = args
+    spec = W.CONFIGS[name]
+    inst, _ = W.appendix_a_instance(spec)
+    consts = ScalingConstants.from_instance(inst)
+    s = W.initial_solution(inst, consts, PenaltyState(), random.Random(100 + i))
+    return [(r.depart, r.arrive, list(r.customers)) for r in s.routes]
+
+
+def make_workload(name, ids):
+    spec = W.CONFIGS[name]
+    inst, _ = W.appendix_a_instance(spec)
+    consts = ScalingConstants.from_instance(inst)
+    nbr = build(inst, NeighborConfig(spec.theta), consts)
+    workers = max(1, min(len(ids), (os.cpu_count() or 2) - 1, 64))
+    if workers > 1:
+        with ProcessPoolExecutor(workers) as ex:
+            raw = list(ex.map(_init_one, [(name, i) for i in ids], chunksize=4))
+    else:
+        raw = [_init_one((name, i)) for i in ids]
+    from paper_2605_05208_b200.model import Route, Solution
+    sols = [Solution([Route(d, a, c) for d, a, c in rs]) for rs in raw]
+    return spec, inst, consts, nbr, sols
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region."""
+
+    def __init__(self, gpu: int):
+        self.path = f"/tmp/mdr_clocks_{os.getpid()}.csv"
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={gpu}", f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                                       "-lms", "200"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return None
+        self.p.terminate()
+        self.p.wait()
+        sms, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sms.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sms:
+            return None
+        return {"sm_mhz": statistics.median(sms), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sms)}
+
+
+def flush_l2(torch, dev):
+    buf = torch.empty(64 << 22, dtype=torch.float32, device=dev)  # 1 GiB > 126 MB L2
+    buf.fill_(1.0)
+    del buf
+
+
+def cpu_baseline(name, inst, consts, nbr, sols, depth, seconds=20.0):
+    """Oracle (C port of the reference) descents on all host threads, bounded sample."""
+    from oracle import oracle as O
+    from paper_2605_05208_b200.localsearch import draw_permutations, enabled_operators
+    oi = O.OracleInstance(inst, consts, nbr)
+    ops = enabled_operators(inst)
+    threads = os.cpu_count() or 1
+    k = min(len(sols), threads)
+    perms = [draw_permutations(random.Random(i), ops, depth + 1) for i in range(k)]
+    t0 = time.perf_counter()
+    st = O.local_search_many(oi, sols[:k], [[1.0] * 4] * k, depth, True, 0.5, 0.01, 1e4, perms, threads)
+    dt = time.perf_counter() - t0
+    cands = sum(sum(s["cands"]) for s in st)
+    return {"value": cands / dt, "unit": "move-evals/s", "cores": threads, "kind": "port",
+            "sample": f"{k} complete {name} descents (individuals 0..{k-1}, depth {depth}, multi-move) "
+                      f"on {threads} host threads, {dt:.1f} s, {cands} candidates",
+            "descents_per_s": k / dt}
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the oracle port of the reference CPU path on the host cores."""
+    if rank != 0:
+        return
+    name = args.config
+    threads = os.cpu_count() or 1
+    spec, inst, consts, nbr, sols = make_workload(name, list(range(threads)))
+    from oracle import oracle as O
+    from paper_2605_05208_b200.localsearch import draw_permutations, enabled_operators
+    oi = O.OracleInstance(inst, consts, nbr)
+    ops = enabled_operators(inst)
+    perms = [draw_permutations(random.Random(i), ops, args.depth + 1) for i in range(len(sols))]
+
+    def step():
+        t0 = time.perf_counter()
+        st = O.local_search_many(oi, sols, [[1.0] * 4] * len(sols), args.depth, True, 0.5, 0.01, 1e4, perms,
+                                 threads)
+        return time.perf_counter() - t0, sum(sum(s["cands"]) for s in st)
+
+    for _ in range(args.warmup):
+        step()
+    tt, cc = 0.0, 0
+    for _ in range(args.steps):
+        dt, c = step()
+        tt += dt
+        cc += c
+    v = cc / tt
+    line = {"impl": "reference", "metric": "move_evals_per_s", "value": v, "unit": "move-evals/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1000 * tt / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{name}: {spec.variant.value} {spec.n_customers}x{spec.n_depots}, "
+                                   f"theta {spec.theta}; per step {len(sols)} complete descents on {threads} threads",
+                       "individuals_per_step": len(sols), "depth": args.depth, "multi_move": True},
+            "cpu_baseline": {"value": v, "unit": "move-evals/s", "cores": threads, "kind": "port",
+                             "sample": f"{len(sols)} descents per step (one per host thread)"},
+            "e2e": {"value": v, "unit": "move-evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "descents_per_s": len(sols) * args.steps / tt}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C4")
+    ap.add_argument("--pop", type=int, default=None, help="individuals per GPU (default: the config's)")
+    ap.add_argument("--depth", type=int, default=500)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    import paper_2605_05208_b200 as P
+    from paper_2605_05208_b200.device import DeviceInstance, Population
+    from paper_2605_05208_b200.localsearch import draw_permutations, enabled_operators
+
+    name = args.config
+    spec = W.CONFIGS[name]
+    per = args.pop or spec.population
+    ids = list(range(rank * per, (rank + 1) * per))
+    spec, inst, consts, nbr, sols = make_workload(name, ids)
+    ops = enabled_operators(inst)
+    perms = np.stack([draw_permutations(random.Random(i), ops, args.depth + 1) for i in ids])
+    lams = [[1.0] * 4] * per
+    dinst = DeviceInstance(inst, consts, nbr, local)
+    J, K = Population.caps_for(sols, inst)
+    pop = Population(dinst, per, J, K, 1 << 15)
+    stream = torch.cuda.current_stream(dev)
+    import ctypes
+    sh = ctypes.c_void_p(stream.cuda_stream)
+    cfg = P.SearchConfig(depth=args.depth, multi_move=True)
+
+    def device_step(profile=False):
+        pop.upload(sols, lams, sh)
+        pop.set_profiling(profile)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        st = pop.local_search(perms, cfg.depth, True, 0.5, 0.01, 1e4, stream=sh)
+        e1.record(stream)
+        e1.synchronize()
+        return e0.elapsed_time(e1), st
+
+    def elite_exchange(st):
+        """NCCL all_gather of each rank's best individual (fixed-size int32 encoding)."""
+        if world == 1:
+            return
+        best = int(np.argmin([s["best_feasible_D"] for s in st]))
+        enc = torch.full((inst.n_customers + 3 * J + 2,), -1, dtype=torch.int32, device=dev)
+        enc[0] = best
+        out = [torch.empty_like(enc) for _ in range(world)]
+        dist.all_gather(out, enc)
+
+    for _ in range(args.warmup):
+        device_step()
+    # timed region: K complete population descents, device-timed
+    flush_l2(torch, dev)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clk = Clocks(local)
+    tot_ms, cands, descents, rounds0 = 0.0, 0, 0, pop.timing()["rounds"]
+    stats_last = None
+    for k in range(args.steps):
+        ms, st = device_step()
+        elite_exchange(st)
+        tot_ms += ms
+        cands += sum(sum(s["cands"]) for s in st)
+        descents += len(st)
+        stats_last = st
+        if k + 1 < args.steps:
+            flush_l2(torch, dev)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = clk.stop()
+    rounds = pop.timing()["rounds"] - rounds0
+    launches = rounds * 3 + 2 * args.steps  # plan/eval/select per round + unpack/rebuild per step
+
+    # profiled pass (untimed): eval-kernel share, avg launch duration, per-op candidates
+    tm0 = pop.timing()
+    ms_p, st_p = device_step(profile=True)
+    tm1 = pop.timing()
+    tm = {k: tm1[k] - tm0[k] for k in tm1}
+    pop.set_profiling(False)
+    op_c = np.sum([s["cands"] for s in st_p], axis=0)
+    ab = ALG_BYTES_WIN if inst.has_windows else ALG_BYTES_NOWIN
+    alg_bytes = float(sum(op_c[o] * ab[o] for o in range(6)))
+    eval_avg_ms = tm["eval_ms"] / max(tm["eval_launches"], 1)
+    achieved = alg_bytes / max(tm["eval_launches"], 1) / (eval_avg_ms * 1e-3) / 1e9
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    hbm = float(peaks.get("hbm_gbs", 6650.0))
+
+    # e2e: through the public API with host Solution objects, H2D + D2H inside
+    e2e = None
+    if not args.no_e2e:
+        work_ms, e_cands, h2d, d2h = 0.0, 0, 0, 0
+        P.local_search_population([s.clone() for s in sols], [P.PenaltyState() for _ in sols], cfg, nbr, consts,
+                                  inst, [random.Random(i) for i in ids], device=local)  # warm-up (allocation)
+        for k in range(max(1, args.steps)):
+            work = [s.clone() for s in sols]
+            pens = [P.PenaltyState() for _ in sols]
+            rngs = [random.Random(i) for i in ids]
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            st = P.local_search_population(work, pens, cfg, nbr, consts, inst, rngs, device=local)
+            torch.cuda.synchronize()
+            work_ms += 1000 * (time.perf_counter() - t0)
+            e_cands += sum(sum(s["cands"]) for s in st)
+            srch = P.localsearch._searcher(inst, consts, nbr, local)
+            h2d = srch.pop.h2d_bytes + perms.nbytes
+            d2h = srch.pop.d2h_bytes
+        e2e = {"value": e_cands / (work_ms / 1000.0), "unit": "move-evals/s", "h2d_bytes_per_step": int(h2d),
+               "d2h_bytes_per_step": int(d2h), "ms_per_step": work_ms / max(1, args.steps)}
+
+    # max over ranks (time), sum over ranks (work)
+    t = torch.tensor([tot_ms, float(cands), float(descents)], dtype=torch.float64, device=dev)
+    if world > 1:
+        tmax = t.clone()
+        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        tot_ms = float(tmax[0])
+        if e2e is not None:
+            ev = torch.tensor([e2e["value"]], dtype=torch.float64, device=dev)
+            dist.all_reduce(ev, op=dist.ReduceOp.SUM)
+            e2e["value"] = float(ev[0])
+    cands_all, desc_all = float(t[1]), float(t[2])
+    if rank == 0:
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            cpu = cpu_baseline(name, inst, consts, nbr, sols, args.depth)
+        value = cands_all / (tot_ms / 1000.0)
+        line = {
+            "metric": "move_evals_per_s", "value": value, "unit": "move-evals/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": tot_ms / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": f"{name}: synthetic {spec.variant.value} {spec.n_customers} customers x "
+                                   f"{spec.n_depots} depots, theta {spec.theta}, population {per} per GPU, "
+                                   f"one step = all {per} descents (depth {args.depth}, multi-move)",
+                       "population_per_gpu": per, "depth": args.depth, "multi_move": True,
+                       "l2": "flushed (1 GiB write) between timed steps"},
+            "descents_per_s": desc_all / (tot_ms / 1000.0),
+            "candidates_per_step": cands_all / args.steps,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                         "frac": achieved / hbm, "traffic": None,
+                         "kernel": "k_eval (fused enumerate+evaluate+reduce)",
+                         "eval_share_of_step": tm["eval_ms"] / max(tm["total_ms"], 1e-9),
+                         "eval_avg_launch_ms": eval_avg_ms,
+                         "alg_bytes_per_launch": alg_bytes / max(tm["eval_launches"], 1),
+                         "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback"},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": int(launches),
+            "clocks": clocks,
+            "profile": {"rounds_per_step": rounds / args.steps, "plan_ms": tm["plan_ms"], "eval_ms": tm["eval_ms"],
+                        "select_ms": tm["select_ms"], "total_ms": tm["total_ms"]},
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

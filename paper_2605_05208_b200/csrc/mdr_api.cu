@@ -56,6 +56,7 @@ struct mdr_pop {
   int profiling;
   mdr_timing tm;
   cudaEvent_t ev[8];
+  std::vector<cudaEvent_t> rev;  // per-round events when profiling (4 per round)
 };
 
 template <typename T>
@@ -226,6 +227,7 @@ void mdr_pop_destroy(mdr_pop *p) {
   if (p->d_xfer) cudaFree(p->d_xfer);
   if (p->h_hdr) cudaFreeHost(p->h_hdr);
   for (int i = 0; i < 8; i++) cudaEventDestroy(p->ev[i]);
+  for (cudaEvent_t e : p->rev) cudaEventDestroy(e);
   delete p;
 }
 
@@ -644,7 +646,6 @@ int mdr_totals(mdr_pop *p, int32_t b, double out[5]) {
 int mdr_set_profiling(mdr_pop *p, int32_t on) {
   if (!p) return fail(MDR_ERR_ARG, "null pop");
   p->profiling = on;
-  memset(&p->tm, 0, sizeof(p->tm));
   return MDR_OK;
 }
 
@@ -700,25 +701,26 @@ int mdr_local_search(mdr_pop *p, const mdr_ls_cfg *cfg, mdr_ls_stats *stats, voi
   int prof = p->profiling;
   if (prof) CK(cudaEventRecord(p->ev[6], s));
   long long rounds = 0;
+  long long ev_used = 0;
+  auto ev_at = [&](long long i) -> cudaEvent_t {
+    while ((long long)p->rev.size() <= i) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      p->rev.push_back(e);
+    }
+    return p->rev[i];
+  };
   while (B > 0) {
     for (int r = 0; r < rps; r++) {
-      if (prof) cudaEventRecord(p->ev[0], s);
+      if (prof) cudaEventRecord(ev_at(ev_used), s);
       launch_plan(I, P, L, s);
-      if (prof) cudaEventRecord(p->ev[1], s);
+      if (prof) cudaEventRecord(ev_at(ev_used + 1), s);
       launch_eval(I, P, L, p->grid, I.win, s);
-      if (prof) cudaEventRecord(p->ev[2], s);
+      if (prof) cudaEventRecord(ev_at(ev_used + 2), s);
       launch_select(I, P, L, I.win, s);
       if (prof) {
-        cudaEventRecord(p->ev[3], s);
-        cudaEventSynchronize(p->ev[3]);
-        float a = 0, b2 = 0, c = 0;
-        cudaEventElapsedTime(&a, p->ev[0], p->ev[1]);
-        cudaEventElapsedTime(&b2, p->ev[1], p->ev[2]);
-        cudaEventElapsedTime(&c, p->ev[2], p->ev[3]);
-        p->tm.plan_ms += a;
-        p->tm.eval_ms += b2;
-        p->tm.select_ms += c;
-        p->tm.eval_launches++;
+        cudaEventRecord(ev_at(ev_used + 3), s);
+        ev_used += 4;
       }
       rounds++;
     }
@@ -738,7 +740,18 @@ int mdr_local_search(mdr_pop *p, const mdr_ls_cfg *cfg, mdr_ls_stats *stats, voi
     cudaEventElapsedTime(&tot, p->ev[6], p->ev[7]);
     p->tm.total_ms += tot;
     p->tm.rounds += rounds;
+    for (long long e = 0; e + 3 < ev_used; e += 4) {
+      float a = 0, b2 = 0, c = 0;
+      cudaEventElapsedTime(&a, p->rev[e], p->rev[e + 1]);
+      cudaEventElapsedTime(&b2, p->rev[e + 1], p->rev[e + 2]);
+      cudaEventElapsedTime(&c, p->rev[e + 2], p->rev[e + 3]);
+      p->tm.plan_ms += a;
+      p->tm.eval_ms += b2;
+      p->tm.select_ms += c;
+      p->tm.eval_launches++;
+    }
   }
+  if (!prof) p->tm.rounds += rounds;
   std::vector<LsState> st(B > 0 ? B : 1);
   std::vector<unsigned long long> cands((size_t)(B > 0 ? B : 1) * 6);
   if (B) {
