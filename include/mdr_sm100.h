@@ -98,6 +98,7 @@ typedef struct mdr_timing {
   double eval_ms, select_ms, plan_ms, total_ms; /* summed CUDA-event times */
   int64_t eval_launches, rounds;
   int64_t cands_total;
+  double geval_ms; /* generic-path evaluator (intra-route, 2-opt, depot operators) */
 } mdr_timing;
 
 const char *mdr_last_error(void);

@@ -12,7 +12,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libmdr_sm100.so")
+LIB_PATH = os.environ.get("MDR_LIB") or os.path.join(_HERE, "libmdr_sm100.so")
 
 MDR_OK, MDR_ERR_ARG, MDR_ERR_CONFLICT, MDR_ERR_CAPACITY, MDR_ERR_CUDA, MDR_ERR_PERMS = range(6)
 
@@ -62,7 +62,7 @@ class LsStats(C.Structure):
 class Timing(C.Structure):
     _fields_ = [("eval_ms", C.c_double), ("select_ms", C.c_double), ("plan_ms", C.c_double),
                 ("total_ms", C.c_double), ("eval_launches", C.c_int64), ("rounds", C.c_int64),
-                ("cands_total", C.c_int64)]
+                ("cands_total", C.c_int64), ("geval_ms", C.c_double)]
 
 
 _L = None

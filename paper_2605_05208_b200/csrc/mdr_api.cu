@@ -6,6 +6,7 @@
 // for completion and the caller's deadline (localsearch.py:116-117).
 #include <cub/cub.cuh>
 
+#include <algorithm>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -192,8 +193,22 @@ int mdr_pop_create(mdr_instance *inst, int32_t Bcap, int32_t J, int32_t K, int32
     if (w > wmax) wmax = w;
   }
   if (wmax > 0x7fffffffLL) return fail(MDR_ERR_ARG, "candidate index space exceeds 2^31 per individual");
-  p->max_chunks = (size_t)Bcap * (size_t)((wmax + MDR_CHUNK - 1) / MDR_CHUNK);
+  p->max_chunks = (size_t)Bcap * (size_t)(I.NC + J);  // tasks per round
   DA(A, P.partial, p->max_chunks);
+  DA(A, P.tcount, p->max_chunks);
+  DA(A, P.task_next, 6);
+  DA(A, P.opcnt, 6);
+  DA(A, P.optasks, 6);
+  DA(A, P.opb, (size_t)6 * Bcap);
+  DA(A, P.opoff, (size_t)6 * (Bcap + 1));
+  DA(A, P.leader, Bcap);
+  DA(A, P.gcount, 1);
+  {
+    long long g = (long long)Bcap * std::max((long long)I.NC * 64, (long long)Fcap);
+    if (g > 0x7fffffffLL) g = 0x7fffffffLL;
+    P.Gcap = (int)g;
+  }
+  DA(A, P.gq, (size_t)P.Gcap);
   DA(A, P.fol, (size_t)Bcap * Fcap);
   DA(A, P.fcount, Bcap);
   DA(A, P.nanflag, Bcap);
@@ -717,10 +732,12 @@ int mdr_local_search(mdr_pop *p, const mdr_ls_cfg *cfg, mdr_ls_stats *stats, voi
       if (prof) cudaEventRecord(ev_at(ev_used + 1), s);
       launch_eval(I, P, L, p->grid, I.win, s);
       if (prof) cudaEventRecord(ev_at(ev_used + 2), s);
+      launch_eval_g(I, P, L, p->grid, I.win, s);
+      if (prof) cudaEventRecord(ev_at(ev_used + 3), s);
       launch_select(I, P, L, I.win, s);
       if (prof) {
-        cudaEventRecord(ev_at(ev_used + 3), s);
-        ev_used += 4;
+        cudaEventRecord(ev_at(ev_used + 4), s);
+        ev_used += 5;
       }
       rounds++;
     }
@@ -740,13 +757,15 @@ int mdr_local_search(mdr_pop *p, const mdr_ls_cfg *cfg, mdr_ls_stats *stats, voi
     cudaEventElapsedTime(&tot, p->ev[6], p->ev[7]);
     p->tm.total_ms += tot;
     p->tm.rounds += rounds;
-    for (long long e = 0; e + 3 < ev_used; e += 4) {
-      float a = 0, b2 = 0, c = 0;
+    for (long long e = 0; e + 4 < ev_used; e += 5) {
+      float a = 0, b2 = 0, g = 0, c = 0;
       cudaEventElapsedTime(&a, p->rev[e], p->rev[e + 1]);
       cudaEventElapsedTime(&b2, p->rev[e + 1], p->rev[e + 2]);
-      cudaEventElapsedTime(&c, p->rev[e + 2], p->rev[e + 3]);
+      cudaEventElapsedTime(&g, p->rev[e + 2], p->rev[e + 3]);
+      cudaEventElapsedTime(&c, p->rev[e + 3], p->rev[e + 4]);
       p->tm.plan_ms += a;
       p->tm.eval_ms += b2;
+      p->tm.geval_ms += g;
       p->tm.select_ms += c;
       p->tm.eval_launches++;
     }

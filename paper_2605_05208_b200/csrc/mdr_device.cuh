@@ -66,7 +66,17 @@ struct DevPop {
   int *chunk_off;             // [B+1]
   int *total_chunks;          // [1]
   int *active;                // [1]
-  ulonglong2 *partial;        // [max chunks] {ord(dF), key}
+  int *task_next;             // [6] dynamic task counters of the per-operator k_eval
+  int *opcnt;                 // [6] individuals evaluating each operator this round
+  int *optasks;               // [6] tasks per operator this round
+  int *opb;                   // [6][Bcap] individual ids per operator
+  int *opoff;                 // [6][Bcap+1] first task of each individual within its operator
+  ulonglong2 *leader;         // [B] running min {ord(dF), key} of the round
+  ulonglong2 *gq;             // [Gcap] generic-path queue {key, b | op << 24}
+  int *gcount;                // [1]
+  int Gcap;
+  int *tcount;                // [max tasks] candidates per task
+  ulonglong2 *partial;        // [max tasks] {ord(dF), key}
   ulonglong2 *fol;            // [B][Fcap]
   int *fcount;                // [B]
   int *nanflag;               // [B]

@@ -13,6 +13,7 @@
 //                  penalty adaptation, state machine (localsearch.py:97-140)
 #include <cstdio>
 
+#include "mdr_fused.cuh"
 #include "mdr_kernels.cuh"
 
 namespace mdr {
@@ -141,126 +142,198 @@ __global__ void __launch_bounds__(256) k_rebuild(DevInst I, DevPop P, int B) {
 // ---------------------------------------------------------------------------
 // plan: operator of the round per individual, flattened chunk offsets
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(1024) k_plan(DevInst I, DevPop P, LsParams L) {
-  __shared__ int wsum[32];
-  __shared__ int carry;
-  if (threadIdx.x == 0) carry = 0;
+__device__ __forceinline__ int block_excl_scan(int x, int *wsum, int &total) {
+  int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  int inc = x;
+#pragma unroll
+  for (int s = 1; s < 32; s <<= 1) {
+    int y = __shfl_up_sync(0xffffffffu, inc, s);
+    if (lane >= s) inc += y;
+  }
   __syncthreads();
-  for (int base = 0; base < L.B; base += blockDim.x) {
-    int b = base + threadIdx.x;
-    int chunks = 0;
-    if (b < L.B) {
-      LsState st = P.st[b];
-      P.fcount[b] = 0;
-      P.nanflag[b] = 0;
-      if (!st.done && st.pass >= P.maxp) {
-        st.done = 1;
-        st.status = 5;
-        P.st[b] = st;
-      }
-      if (!st.done) {
-        int op = P.perms[((size_t)b * P.maxp + st.pass) * P.nops + st.pos];
-        long long items = op_items(op, P.m[b], I.NC, I.W, I.ND, I.win, I.open, P.K);
-        P.op_cur[b] = op;
-        P.wsize[b] = (int)items;
-        chunks = (int)((items + MDR_CHUNK - 1) / MDR_CHUNK);
-      } else {
-        P.wsize[b] = 0;
-      }
-    }
-    // block exclusive scan of chunks
-    int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    int x = chunks;
+  if (lane == 31) wsum[w] = inc;
+  __syncthreads();
+  if (w == 0) {
+    int t = lane < nw ? wsum[lane] : 0;
 #pragma unroll
     for (int s = 1; s < 32; s <<= 1) {
-      int y = __shfl_up_sync(0xffffffffu, x, s);
-      if (lane >= s) x += y;
+      int y = __shfl_up_sync(0xffffffffu, t, s);
+      if (lane >= s) t += y;
     }
-    if (lane == 31) wsum[w] = x;
-    __syncthreads();
-    if (w == 0) {
-      int t = lane < (int)(blockDim.x >> 5) ? wsum[lane] : 0;
-#pragma unroll
-      for (int s = 1; s < 32; s <<= 1) {
-        int y = __shfl_up_sync(0xffffffffu, t, s);
-        if (lane >= s) t += y;
+    wsum[lane] = t;
+  }
+  __syncthreads();
+  total = wsum[nw - 1];
+  return inc - x + (w > 0 ? wsum[w - 1] : 0);
+}
+
+__global__ void __launch_bounds__(1024) k_plan(DevInst I, DevPop P, LsParams L) {
+  __shared__ int wsum[32];
+  // pass 1: operator and task count of every active individual
+  for (int b = threadIdx.x; b < L.B; b += blockDim.x) {
+    LsState st = P.st[b];
+    P.fcount[b] = 0;
+    P.nanflag[b] = 0;
+    P.leader[b] = make_ulonglong2(~0ull, ~0ull);
+    if (!st.done && st.pass >= P.maxp) {
+      st.done = 1;
+      st.status = 5;
+      P.st[b] = st;
+    }
+    if (!st.done) {
+      int op = P.perms[((size_t)b * P.maxp + st.pass) * P.nops + st.pos];
+      P.op_cur[b] = op;
+      P.wsize[b] = op_tasks(op, P.m[b], I.NC, I.win);
+    } else {
+      P.op_cur[b] = -1;
+      P.wsize[b] = 0;
+    }
+  }
+  __syncthreads();
+  // pass 2: per operator, compact list of individuals and their task offsets
+  for (int op = 0; op < 6; op++) {
+    int carry = 0, cnt = 0;
+    for (int base = 0; base < L.B; base += blockDim.x) {
+      int b = base + threadIdx.x;
+      int t = (b < L.B && P.op_cur[b] == op) ? P.wsize[b] : 0;
+      int f = t > 0;
+      int tt, ft;
+      int off = block_excl_scan(t, wsum, tt);
+      int idx = block_excl_scan(f, wsum, ft);
+      if (f) {
+        P.opb[op * P.Bcap + cnt + idx] = b;
+        P.opoff[op * (P.Bcap + 1) + cnt + idx] = carry + off;
       }
-      wsum[lane] = t;
+      carry += tt;
+      cnt += ft;
     }
-    __syncthreads();
-    int excl = x - chunks + (w > 0 ? wsum[w - 1] : 0) + carry;
-    if (b < L.B) P.chunk_off[b] = excl;
-    __syncthreads();
-    if (threadIdx.x == blockDim.x - 1) carry = excl + chunks;
-    __syncthreads();
+    if (threadIdx.x == 0) {
+      P.opoff[op * (P.Bcap + 1) + cnt] = carry;
+      P.opcnt[op] = cnt;
+      P.optasks[op] = carry;
+      P.task_next[op] = 0;
+    }
   }
   if (threadIdx.x == 0) {
-    P.chunk_off[L.B] = carry;
-    *P.total_chunks = carry;
     *P.active = 0;
+    *P.gcount = 0;
   }
 }
 
 // ---------------------------------------------------------------------------
-// fused enumerate + evaluate + reduce
+// fused enumerate + evaluate + reduce: persistent warps over the task list
 // ---------------------------------------------------------------------------
-template <bool WIN>
-__global__ void __launch_bounds__(256) k_eval(DevInst I, DevPop P, LsParams L) {
-  __shared__ OK red[8];
-  __shared__ int sb;
-  __shared__ int scount[8];
-  const int total = *P.total_chunks;
-  for (int c = blockIdx.x; c < total; c += gridDim.x) {
-    if (threadIdx.x == 0) {
-      int lo = 0, hi = L.B - 1;  // last b with chunk_off[b] <= c and chunks > 0
-      while (lo < hi) {
-        int mid = (lo + hi + 1) >> 1;
-        if (P.chunk_off[mid] <= c) lo = mid; else hi = mid - 1;
-      }
-      sb = lo;
-    }
-    __syncthreads();
-    const int b = sb;
-    const int op = P.op_cur[b];
-    const int M = P.m[b];
-    const long long item = (long long)(c - P.chunk_off[b]) * MDR_CHUNK + threadIdx.x;
-    double lam[4];
+#define MDR_TGRAB 2
+#ifndef MDR_EVAL_MINB
+#define MDR_EVAL_MINB 2
+#endif
+
+template <bool WIN, int OP>
+__global__ void __launch_bounds__(256, MDR_EVAL_MINB) k_eval(DevInst I, DevPop P, LsParams L) {
+  const int lane = threadIdx.x & 31;
+  const int total = P.optasks[OP];
+  const int cnt = P.opcnt[OP];
+  const int *OFF = P.opoff + OP * (P.Bcap + 1);
+  const int *OB = P.opb + OP * P.Bcap;
+  const bool mm = L.multi_move != 0;
+  __shared__ double s_u[8][MDR_USLOT];
+  double *U = s_u[threadIdx.x >> 5];
+  int lo = 0, hi = 0, b = 0;
+  IV v;
+  double lam[4] = {0, 0, 0, 0};
+  for (;;) {
+    int t0 = 0;
+    if (lane == 0) t0 = atomicAdd(P.task_next + OP, MDR_TGRAB);
+    t0 = __shfl_sync(0xffffffffu, t0, 0);
+    if (t0 >= total) break;
+    const int t1 = min(t0 + MDR_TGRAB, total);
+    for (int t = t0; t < t1; t++) {
+      if (t < lo || t >= hi) {
+        int l2 = 0, h2 = cnt - 1;  // last i with OFF[i] <= t
+        while (l2 < h2) {
+          int mid = (l2 + h2 + 1) >> 1;
+          if (__ldg(OFF + mid) <= t) l2 = mid; else h2 = mid - 1;
+        }
+        b = OB[l2];
+        lo = OFF[l2];
+        hi = OFF[l2 + 1];
+        v = make_iv(P, b);
 #pragma unroll
-    for (int i = 0; i < 4; i++) lam[i] = P.lam[b * 4 + i];
-    Cand cd;
-    bool valid = item < P.wsize[b] && decode_item(I, P, b, op, item, M, cd);
-    OK v{~0ull, ~0ull};
-    bool fol = false, isnan_ = false;
+        for (int i = 0; i < 4; i++) lam[i] = P.lam[b * 4 + i];
+      }
+      const int local = t - lo;
+      Acc acc{~0ull, ~0ull, 0};
+      if (OP == 0) task_relocate<WIN>(I, P, v, b, I.ND + local, lam, mm, acc, U);
+      else if (OP == 1) task_swap<WIN>(I, P, v, b, I.ND + local, lam, mm, acc, U);
+      else if (OP == 2) {
+        if (local < I.NC) task_tos_u<WIN>(I, P, v, b, I.ND + local, lam, mm, acc);
+        else task_tos_r<WIN>(I, P, v, b, local - I.NC, lam, mm, acc);
+      } else if (OP == 3) task_two_opt<WIN>(I, P, v, b, I.ND + local, lam, mm, acc);
+      else if (OP == 4) task_di<WIN>(I, P, v, b, local, lam, mm, acc);
+      else task_dr<WIN>(I, P, v, b, local, lam, mm, acc);
+      if (OP <= 2) {
+        OK r = warp_min(OK{acc.o, acc.k});
+        int n = acc.n;
+#pragma unroll
+        for (int s = 16; s > 0; s >>= 1) n += __shfl_xor_sync(0xffffffffu, n, s);
+        if (lane == 0) {
+          leader_min(P.leader + b, r.o, r.k);
+          if (n) atomicAdd(&P.cands[(size_t)b * 6 + OP], (unsigned long long)n);
+        }
+      }
+    }
+  }
+}
+
+// generic evaluator: intra-route relocate/swap, 2-opt, depot operators,
+// one thread per queued candidate through eval_cand (batch.py:365-553)
+template <bool WIN>
+__global__ void __launch_bounds__(256) k_eval_g(DevInst I, DevPop P, LsParams L) {
+  const int lane = threadIdx.x & 31;
+  const int total = min(*P.gcount, P.Gcap);
+  const bool mm = L.multi_move != 0;
+  const int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int base = wid * 32; base < total; base += nwarps * 32) {
+    const int i = base + lane;
+    const bool valid = i < total;
+    int b = -1, op = 0;
+    unsigned long long key = 0, o = ~0ull;
+    bool fol = false;
     if (valid) {
-      Delta D = eval_cand<WIN>(I, P, b, op, cd, lam);
+      ulonglong2 e = P.gq[i];
+      key = e.x;
+      b = (int)(e.y & 0xffffffu);
+      op = (int)(e.y >> 24);
+      double lam[4];
+#pragma unroll
+      for (int q = 0; q < 4; q++) lam[q] = P.lam[b * 4 + q];
+      Delta D = eval_cand<WIN>(I, P, b, op, unpack_key(key), lam);
       if (D.dF != D.dF) {
-        isnan_ = true;
+        atomicOr(P.nanflag + b, 1);
       } else {
-        v.o = ord_of(D.dF);
-        v.k = pack_key(cd);
-        fol = L.multi_move && follower_ok(D);
+        o = ord_of(D.dF);
+        fol = mm && follower_ok(D);
       }
     }
-    unsigned fm = __ballot_sync(0xffffffffu, fol);
-    if (fm) {
-      int lane = threadIdx.x & 31;
-      int base = 0;
-      if (lane == __ffs(fm) - 1) base = atomicAdd(&P.fcount[b], __popc(fm));
-      base = __shfl_sync(0xffffffffu, base, __ffs(fm) - 1);
+    const int b0 = __shfl_sync(0xffffffffu, b, 0);
+    const bool uni = __all_sync(0xffffffffu, !valid || b == b0);
+    if (uni) {
+      OK r = warp_min(OK{o, key});
+      unsigned vm = __ballot_sync(0xffffffffu, valid);
+      const int op0 = __shfl_sync(0xffffffffu, op, 0);
+      if (lane == 0) {
+        leader_min(P.leader + b0, r.o, r.k);
+        atomicAdd(&P.cands[(size_t)b0 * 6 + op0], (unsigned long long)__popc(vm));
+      }
+      append_fol(P, b0, fol, o, key);
+    } else if (valid) {
+      leader_min(P.leader + b, o, key);
+      atomicAdd(&P.cands[(size_t)b * 6 + op], 1ull);
       if (fol) {
-        int at = base + __popc(fm & ((1u << lane) - 1));
-        if (at < P.Fcap) P.fol[(size_t)b * P.Fcap + at] = make_ulonglong2(v.o, v.k);
+        int at = atomicAdd(&P.fcount[b], 1);
+        if (at < P.Fcap) P.fol[(size_t)b * P.Fcap + at] = make_ulonglong2(o, key);
       }
-    }
-    if (__any_sync(0xffffffffu, isnan_) && (threadIdx.x & 31) == 0) atomicOr(&P.nanflag[b], 1);
-    unsigned vm = __ballot_sync(0xffffffffu, valid);
-    if ((threadIdx.x & 31) == 0) scount[threadIdx.x >> 5] = __popc(vm);
-    OK r = block_min(v, red);
-    if (threadIdx.x == 0) {
-      P.partial[c] = make_ulonglong2(r.o, r.k);
-      int s = 0;
-      for (int w = 0; w < (int)(blockDim.x >> 5); w++) s += scount[w];
-      if (s) atomicAdd(&P.cands[(size_t)b * 6 + op], (unsigned long long)s);
     }
   }
 }
@@ -401,20 +474,16 @@ __global__ void __launch_bounds__(256) k_select(DevInst I, DevPop P, LsParams L)
   int *sm_cnt = newidx + 2 * J;                             // [ND]
   const int op = P.op_cur[b];
 
-  // ---- leader (batch.py:587-597): min (dF, key) over the chunk partials
-  OK best{~0ull, ~0ull};
-  for (int c = P.chunk_off[b] + threadIdx.x; c < P.chunk_off[b + 1]; c += blockDim.x) {
-    ulonglong2 p = P.partial[c];
-    OK x{p.x, p.y};
-    if (ok_less(x, best)) best = x;
-  }
-  best = block_min(best, red);
+  // ---- leader (batch.py:587-597): the round's min (dF, key) of this individual
+  const ulonglong2 ld = P.leader[b];
+  const OK best{ld.x, ld.y};
   const bool has = !P.nanflag[b] && best.o != ~0ull && unord(best.o) < -MDR_EPS;
   const int nf = P.fcount[b];
   if (threadIdx.x == 0) {
     P.st[b].op_evals++;
     s_flag = 0;
     if (has && L.multi_move && nf > P.Fcap) s_flag = 1;  // follower buffer overflow
+    if (*P.gcount > P.Gcap) s_flag = 1;                  // generic queue overflow
   }
   __syncthreads();
   if (s_flag) {
@@ -711,19 +780,42 @@ void launch_plan(const DevInst &I, const DevPop &P, const LsParams &L, cudaStrea
   k_plan<<<1, 1024, 0, s>>>(I, P, L);
 }
 
-int eval_grid_size(bool win) {
+template <typename K>
+static int grid_for(K kern) {
   int dev = 0, sms = 148, per = 1;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  if (win) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_eval<true>, 256, 0);
-  else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_eval<false>, 256, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, 256, 0);
   if (per < 1) per = 1;
   return sms * per;
 }
 
+int eval_grid_size(bool win) { return win ? grid_for(k_eval<true, 0>) : grid_for(k_eval<false, 0>); }
+
+template <bool WIN>
+static void launch_eval_t(const DevInst &I, const DevPop &P, const LsParams &L, cudaStream_t s) {
+  static int g[6] = {0, 0, 0, 0, 0, 0};
+  if (!g[0]) {
+    g[0] = grid_for(k_eval<WIN, 0>); g[1] = grid_for(k_eval<WIN, 1>); g[2] = grid_for(k_eval<WIN, 2>);
+    g[3] = grid_for(k_eval<WIN, 3>); g[4] = grid_for(k_eval<WIN, 4>); g[5] = grid_for(k_eval<WIN, 5>);
+  }
+  k_eval<WIN, 0><<<g[0], 256, 0, s>>>(I, P, L);
+  k_eval<WIN, 1><<<g[1], 256, 0, s>>>(I, P, L);
+  k_eval<WIN, 2><<<g[2], 256, 0, s>>>(I, P, L);
+  if (!WIN) k_eval<WIN, 3><<<g[3], 256, 0, s>>>(I, P, L);
+  k_eval<WIN, 4><<<g[4], 256, 0, s>>>(I, P, L);
+  k_eval<WIN, 5><<<g[5], 256, 0, s>>>(I, P, L);
+}
+
 void launch_eval(const DevInst &I, const DevPop &P, const LsParams &L, int grid, bool win, cudaStream_t s) {
-  if (win) k_eval<true><<<grid, 256, 0, s>>>(I, P, L);
-  else k_eval<false><<<grid, 256, 0, s>>>(I, P, L);
+  (void)grid;
+  if (win) launch_eval_t<true>(I, P, L, s);
+  else launch_eval_t<false>(I, P, L, s);
+}
+
+void launch_eval_g(const DevInst &I, const DevPop &P, const LsParams &L, int grid, bool win, cudaStream_t s) {
+  if (win) k_eval_g<true><<<grid, 256, 0, s>>>(I, P, L);
+  else k_eval_g<false><<<grid, 256, 0, s>>>(I, P, L);
 }
 
 void launch_select(const DevInst &I, const DevPop &P, const LsParams &L, bool win, cudaStream_t s) {
