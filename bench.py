@@ -205,7 +205,8 @@ def main():
     name = args.config
     spec = W.CONFIGS[name]
     per = args.pop or spec.population
-    ids = list(range(rank * per, (rank + 1) * per))
+    from paper_2605_05208_b200.distributed import shard_range
+    ids = list(shard_range(per * world, world, rank))  # weak scaling: `per` individuals per GPU
     spec, inst, consts, nbr, sols = make_workload(name, ids)
     ops = enabled_operators(inst)
     perms = np.stack([draw_permutations(random.Random(i), ops, args.depth + 1) for i in ids])
@@ -228,15 +229,18 @@ def main():
         e1.synchronize()
         return e0.elapsed_time(e1), st
 
+    from paper_2605_05208_b200 import distributed as DS
+
     def elite_exchange(st):
-        """NCCL all_gather of each rank's best individual (fixed-size int32 encoding)."""
+        """NCCL all_gather of every rank's elite (its lowest-D feasible individual, else
+        its first) as a fixed-size int32 encoding -- the only collective of the job."""
         if world == 1:
-            return
-        best = int(np.argmin([s["best_feasible_D"] for s in st]))
-        enc = torch.full((inst.n_customers + 3 * J + 2,), -1, dtype=torch.int32, device=dev)
-        enc[0] = best
-        out = [torch.empty_like(enc) for _ in range(world)]
-        dist.all_gather(out, enc)
+            return None
+        routes_all, _ = pop.download(sh)
+        Ds = [s["best_feasible_D"] for s in st]
+        best = int(np.argmin(Ds))
+        enc = DS.encode_elite(routes_all[best], Ds[best], inst.n_customers, J)
+        return DS.best_of(DS.exchange_elites(enc, device=dev))
 
     for _ in range(args.warmup):
         device_step()
