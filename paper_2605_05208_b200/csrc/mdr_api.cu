@@ -137,6 +137,8 @@ int mdr_instance_create(const mdr_instance_desc *d, int32_t device, mdr_instance
   D.open = d->open_routes ? 1 : 0;
   D.win = d->has_windows ? 1 : 0;
   D.gamma = d->gamma; D.theta = d->theta;
+  D.rQ = 1.0 / d->capacity;
+  D.rD = 1.0 / d->max_duration;
   cudaError_t e = cudaDeviceSynchronize();
   if (e != cudaSuccess) {
     for (void *p : I->allocs) cudaFree(p);

@@ -32,6 +32,7 @@ struct DevInst {
   double Q, Dmax, NV;
   int d_on, nv_on, open, win;
   double gamma, theta;
+  double rQ, rD;  // RN(1/Q), RN(1/Dmax) for div_q (host IEEE division)
 };
 
 // per-individual search state (localsearch.py:107-140 loop variables)
@@ -131,11 +132,9 @@ __device__ __forceinline__ At<WIN> a_node(const DevInst &I, int v) {
   return a;
 }
 
-// vconcat (batch.py:223-262): empty operands are exact identities
+// vconcat (batch.py:223-262) of two non-empty subsequences
 template <bool WIN>
-__device__ __forceinline__ At<WIN> a_cat(const DevInst &I, const At<WIN> &a, const At<WIN> &b) {
-  if (b.first < 0) return a;
-  if (a.first < 0) return b;
+__device__ __forceinline__ At<WIN> a_cat_ne(const DevInst &I, const At<WIN> &a, const At<WIN> &b) {
   size_t lk = (size_t)a.last * (size_t)I.N + (size_t)b.first;
   double c = __ldg(I.dist + lk);
   double t = I.talias ? c : __ldg(I.time + lk);
@@ -157,6 +156,36 @@ __device__ __forceinline__ At<WIN> a_cat(const DevInst &I, const At<WIN> &a, con
   o.first = a.first;
   o.last = b.last;
   return o;
+}
+
+// vconcat with possibly empty operands: an empty side is the exact identity
+template <bool WIN>
+__device__ __forceinline__ At<WIN> a_cat(const DevInst &I, const At<WIN> &a, const At<WIN> &b) {
+  if (b.first < 0) return a;
+  if (a.first < 0) return b;
+  return a_cat_ne<WIN>(I, a, b);
+}
+
+// Correctly rounded a / b for a divisor known in advance (rb = RN(1/b)):
+// Markstein's correction q' = RN(q + r*rb), r = a - q*b exact (FMA), then an
+// exact acceptance test: the remainder of q' is recomputed exactly and q' is
+// accepted only if |a/b - q'| is strictly below half the smaller neighbour
+// gap of q'; anything else (ties, specials, extreme exponents) falls back to
+// the IEEE division.  The result is therefore always RN(a / b).
+__device__ __forceinline__ double div_q(double a, double b, double rb) {
+  double q = __dmul_rn(a, rb);
+  double r = __fma_rn(-q, b, a);
+  q = __fma_rn(r, rb, q);
+  long long bits = __double_as_longlong(q);
+  int e = (int)((bits >> 52) & 0x7ff);
+  if (e > 60 && e < 2000) {
+    double r2 = fabs(__fma_rn(-q, b, a));  // exact remainder of q
+    // smaller neighbour gap: ulp(q), or ulp(q)/2 when |q| is a power of two
+    long long ge = (bits & 0x000fffffffffffffll) ? (long long)(e - 52) : (long long)(e - 53);
+    double gap = __longlong_as_double(ge << 52);
+    if (__dmul_rn(2.0, r2) < __dmul_rn(gap, fabs(b))) return q;
+  }
+  return a / b;
 }
 
 // ---------------------------------------------------------------------------
@@ -228,8 +257,14 @@ __device__ __forceinline__ void contrib(const DevInst &I, const At<WIN> &a, int 
   if (kc <= 0) { o[0] = o[1] = o[2] = o[3] = o[4] = 0.0; return; }
   o[0] = a.dist;
   o[1] = WIN ? I.gamma * a.TW : 0.0;
-  o[2] = (I.theta * npmax(a.load - I.Q, 0.0)) / I.Q;
-  o[3] = I.d_on ? (I.theta * npmax(a.T - I.Dmax, 0.0)) / I.Dmax : 0.0;
+  double x = I.theta * npmax(a.load - I.Q, 0.0);
+  o[2] = x == 0.0 ? 0.0 : div_q(x, I.Q, I.rQ);
+  if (I.d_on) {
+    double y = I.theta * npmax(a.T - I.Dmax, 0.0);
+    o[3] = y == 0.0 ? 0.0 : div_q(y, I.Dmax, I.rD);
+  } else {
+    o[3] = 0.0;
+  }
   o[4] = I.open ? 0.0 : (dep != arr ? 1.0 : 0.0);
 }
 

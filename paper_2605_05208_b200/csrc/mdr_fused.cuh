@@ -97,10 +97,10 @@ __device__ __forceinline__ void contrib_fast(const DevInst &I, const At<WIN> &a,
   o[0] = a.dist;
   o[1] = WIN ? I.gamma * a.TW : 0.0;
   double x = I.theta * npmax(a.load - I.Q, 0.0);
-  o[2] = x == 0.0 ? 0.0 : x / I.Q;
+  o[2] = x == 0.0 ? 0.0 : div_q(x, I.Q, I.rQ);
   if (I.d_on) {
     double y = I.theta * npmax(a.T - I.Dmax, 0.0);
-    o[3] = y == 0.0 ? 0.0 : y / I.Dmax;
+    o[3] = y == 0.0 ? 0.0 : div_q(y, I.Dmax, I.rD);
   } else {
     o[3] = 0.0;
   }
@@ -230,7 +230,7 @@ __device__ void task_relocate(const DevInst &I, const DevPop &P, const IV &v, in
     }
     At<WIN> s1 = a_node<WIN>(I, u);
     st_at<WIN>(U + 10, s1);
-    if (pu + 2 <= k1) st_at<WIN>(U + 16, a_cat<WIN>(I, s1, a_node<WIN>(I, nxt)));
+    if (pu + 2 <= k1) st_at<WIN>(U + 16, a_cat_ne<WIN>(I, s1, a_node<WIN>(I, nxt)));
     double4 rc1 = ldg4(v.rc + ru);
     U[22] = rc1.x; U[23] = rc1.y; U[24] = rc1.z; U[25] = rc1.w;
     U[26] = I.nv_on ? __ldg(v.fl + m1.y).y : 0.0;
@@ -281,7 +281,8 @@ __device__ void task_relocate(const DevInst &I, const DevPop &P, const IV &v, in
           }
           At<WIN> seg = len == 1 ? ld_at<WIN>(U + 10, u, u) : ld_at<WIN>(U + 16, u, nxt);
           if (rev) swap_ends(seg);
-          At<WIN> B = a_cat<WIN>(I, a_cat<WIN>(I, P2, seg), S2);
+          At<WIN> B = a_cat_ne<WIN>(I, P2, seg);
+          if (S2.first >= 0) B = a_cat_ne<WIN>(I, B, S2);
           double cB[5], nw[5];
           contrib_fast<WIN>(I, B, m2.y, m2.z, m2.x + len, cB);
           const double *ca = U + 5 * (len - 1);
@@ -324,7 +325,7 @@ __device__ void task_swap(const DevInst &I, const DevPop &P, const IV &v, int b,
   if (lane == 0) {
     At<WIN> s1 = a_node<WIN>(I, u);
     st_at<WIN>(U, s1);
-    if (pu + 2 <= k1) st_at<WIN>(U + 6, a_cat<WIN>(I, s1, a_node<WIN>(I, nxtu)));
+    if (pu + 2 <= k1) st_at<WIN>(U + 6, a_cat_ne<WIN>(I, s1, a_node<WIN>(I, nxtu)));
     st_at<WIN>(U + 12, pre<WIN>(v, ru, pu));
     double4 rc1 = ldg4(v.rc + ru);
     U[18] = rc1.x; U[19] = rc1.y; U[20] = rc1.z; U[21] = rc1.w;
@@ -355,7 +356,7 @@ __device__ void task_swap(const DevInst &I, const DevPop &P, const IV &v, int b,
       At<WIN> segB;
       if (rv >= 0 && !same && pv + lv_ <= m2.x) {
         segB = a_node<WIN>(I, vv);
-        if (lv_ == 2) segB = a_cat<WIN>(I, segB, a_node<WIN>(I, nxtv));
+        if (lv_ == 2) segB = a_cat_ne<WIN>(I, segB, a_node<WIN>(I, nxtv));
       }
       const int ncomb = I.win ? 2 : (lv_ == 1 ? 3 : 6);
       for (int ci = 0; ci < ncomb; ci++) {
@@ -383,11 +384,12 @@ __device__ void task_swap(const DevInst &I, const DevPop &P, const IV &v, int b,
             if (au) swap_ends(sA);
             At<WIN> sB = segB;
             if (av) swap_ends(sB);
-            At<WIN> A = a_cat<WIN>(I, a_cat<WIN>(I, ld_at<WIN>(U + 12, dep1, lastP1), sB),
-                                   suf<WIN>(v, ru, pu + lu_ + 1, n1));
+            At<WIN> A = a_cat_ne<WIN>(I, ld_at<WIN>(U + 12, dep1, lastP1), sB);
+            if (pu + lu_ + 1 <= n1 - 1) A = a_cat_ne<WIN>(I, A, suf<WIN>(v, ru, pu + lu_ + 1, n1));
             double cA[5], cB[5], nw[5];
             contrib_fast<WIN>(I, A, m1.y, m1.z, k1 - lu_ + lv_, cA);
-            At<WIN> B = a_cat<WIN>(I, a_cat<WIN>(I, P2, sA), suf<WIN>(v, rv, pv + lv_ + 1, n2));
+            At<WIN> B = a_cat_ne<WIN>(I, P2, sA);
+            if (pv + lv_ + 1 <= n2 - 1) B = a_cat_ne<WIN>(I, B, suf<WIN>(v, rv, pv + lv_ + 1, n2));
             contrib_fast<WIN>(I, B, m2.y, m2.z, k2 - lv_ + lu_, cB);
 #pragma unroll
             for (int f = 0; f < 5; f++) nw[f] = (0.0 + cA[f]) + cB[f];
@@ -447,8 +449,10 @@ __device__ __forceinline__ bool eval_tos(const DevInst &I, const DevPop &P, cons
   const int4 m1 = __ldg(v.rm + r1), m2 = __ldg(v.rm + r2);
   const int k1 = m1.x, k2 = m2.x;
   const int n1 = k1 + (I.open ? 1 : 2), n2 = k2 + (I.open ? 1 : 2);
-  At<WIN> A = a_cat<WIN>(I, pre<WIN>(v, r1, p1), suf<WIN>(v, r2, p2 + 1, n2));
-  At<WIN> B = a_cat<WIN>(I, pre<WIN>(v, r2, p2), suf<WIN>(v, r1, p1 + 1, n1));
+  At<WIN> A = pre<WIN>(v, r1, p1);
+  if (p2 + 1 <= n2 - 1) A = a_cat_ne<WIN>(I, A, suf<WIN>(v, r2, p2 + 1, n2));
+  At<WIN> B = pre<WIN>(v, r2, p2);
+  if (p1 + 1 <= n1 - 1) B = a_cat_ne<WIN>(I, B, suf<WIN>(v, r1, p1 + 1, n1));
   const int kA = p1 + (k2 - p2), kB = p2 + (k1 - p1);
   double cA[5], cB[5], nw[5];
   contrib_fast<WIN>(I, A, m1.y, m2.z, kA, cA);

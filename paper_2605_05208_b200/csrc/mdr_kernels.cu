@@ -79,27 +79,26 @@ __device__ double pw_sum(const double4 *a, int f, int n) {
 // ---------------------------------------------------------------------------
 // rebuild one individual (whole block): loc, tables, route terms, fleet
 // ---------------------------------------------------------------------------
+// per-route part (warp per route): SolutionIndex entries of its customers,
+// prefix/suffix tables (lane i folds positions i..n-1 -- the left fold from i
+// of batch.py:99-124), route terms and closure flag.  list == nullptr: all m.
 template <bool WIN>
-__device__ void rebuild_block(const DevInst &I, const DevPop &P, int b, int *sm_cnt) {
-  const int m = P.m[b];
+__device__ void rebuild_routes(const DevInst &I, const DevPop &P, int b, const int *list, int cnt) {
   int *LOC = P.loc + (size_t)b * P.N;
   int4 *RM = P.rmeta + (size_t)b * P.J;
   double4 *RC = P.rcon + (size_t)b * P.J;
-  for (int v = threadIdx.x; v < P.N; v += blockDim.x) LOC[v] = -1;
-  for (int d = threadIdx.x; d < P.ND; d += blockDim.x) sm_cnt[d] = 0;
-  __syncthreads();
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  for (int r = wid; r < m; r += nw) {
+  for (int q = wid; q < cnt; q += nw) {
+    const int r = list ? list[q] : q;
     int4 mt = RM[r];
     int k = mt.x, n = k + (I.open ? 1 : 2);
     const int *sq = P.seq + row_base(P, b, r);
     for (int p = lane; p < k; p += 32) LOC[sq[p + 1]] = (r << 9) | p;
-    // lane i folds positions i..n-1 (left fold from i, batch.py:99-124)
     for (int i = lane; i < n; i += 32) {
       At<WIN> acc = a_node<WIN>(I, sq[i]);
       if (i == 0) tab_store<WIN>(P, P.tabP, b, r, 0, acc);
       for (int j = i + 1; j < n; j++) {
-        acc = a_cat<WIN>(I, acc, a_node<WIN>(I, sq[j]));
+        acc = a_cat_ne<WIN>(I, acc, a_node<WIN>(I, sq[j]));
         if (i == 0) tab_store<WIN>(P, P.tabP, b, r, j, acc);
       }
       tab_store<WIN>(P, P.tabS, b, r, i, acc);
@@ -110,7 +109,18 @@ __device__ void rebuild_block(const DevInst &I, const DevPop &P, int b, int *sm_
         RM[r].w = (int)o[4];
       }
     }
-    if (lane == 0 && k > 0) atomicAdd(&sm_cnt[mt.y], 1);
+  }
+}
+
+// depot counts of non-empty routes -> fleet_inc/dec, excess (batch.py:144-158)
+__device__ void rebuild_fleet(const DevInst &I, const DevPop &P, int b, int *sm_cnt) {
+  const int m = P.m[b];
+  const int4 *RM = P.rmeta + (size_t)b * P.J;
+  for (int d = threadIdx.x; d < P.ND; d += blockDim.x) sm_cnt[d] = 0;
+  __syncthreads();
+  for (int r = threadIdx.x; r < m; r += blockDim.x) {
+    int4 mt = RM[r];
+    if (mt.x > 0) atomicAdd(&sm_cnt[mt.y], 1);
   }
   __syncthreads();
   if (I.nv_on) {
@@ -129,6 +139,17 @@ __device__ void rebuild_block(const DevInst &I, const DevPop &P, int b, int *sm_
     P.fexcess[b] = 0.0;
   }
   __syncthreads();
+}
+
+// rebuild one individual (whole block): loc, tables, route terms, fleet
+template <bool WIN>
+__device__ void rebuild_block(const DevInst &I, const DevPop &P, int b, int *sm_cnt) {
+  int *LOC = P.loc + (size_t)b * P.N;
+  for (int v = threadIdx.x; v < P.N; v += blockDim.x) LOC[v] = -1;
+  __syncthreads();
+  rebuild_routes<WIN>(I, P, b, nullptr, P.m[b]);
+  __syncthreads();
+  rebuild_fleet(I, P, b, sm_cnt);
 }
 
 template <bool WIN>
@@ -462,7 +483,7 @@ template <bool WIN>
 __global__ void __launch_bounds__(256) k_select(DevInst I, DevPop P, LsParams L) {
   extern __shared__ unsigned long long smx[];
   __shared__ OK red[8];
-  __shared__ int s_flag, s_nm, s_mnew, s_snap;
+  __shared__ int s_flag, s_nm, s_mnew, s_snap, s_nt, s_empty;
   __shared__ unsigned long long s_leader;
   const int b = blockIdx.x;
   if (b >= L.B) return;
@@ -472,6 +493,7 @@ __global__ void __launch_bounds__(256) k_select(DevInst I, DevPop P, LsParams L)
   unsigned *used = reinterpret_cast<unsigned *>(sel + J);   // [J/32+1] route bitmask
   int *newidx = reinterpret_cast<int *>(used + (J / 32 + 1));  // [J+J]
   int *sm_cnt = newidx + 2 * J;                             // [ND]
+  int *tl = sm_cnt + P.ND + 4;                              // [3J] touched routes
   const int op = P.op_cur[b];
 
   // ---- leader (batch.py:587-597): the round's min (dF, key) of this individual
@@ -528,16 +550,26 @@ __global__ void __launch_bounds__(256) k_select(DevInst I, DevPop P, LsParams L)
         __syncthreads();
       }
     }
-    // ---- apply_moves (localsearch.py:58-82)
+    // ---- apply_moves (localsearch.py:58-82); touched routes staged in scratch
     const int m = P.m[b];
     const int nm = s_nm;
-    for (int i = threadIdx.x; i < m * P.Kp; i += blockDim.x) {
-      int r = i / P.Kp, q = i - r * P.Kp;
+    if (threadIdx.x == 0) {
+      int nt = 0;
+      for (int t = 0; t < nm; t++) {
+        Cand c = unpack_key(sel[t]);
+        tl[nt++] = c.r1;
+        if (c.r2 >= 0 && c.r2 != c.r1) tl[nt++] = c.r2;
+      }
+      s_nt = nt;
+      s_flag = 0;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < s_nt * P.Kp; i += blockDim.x) {
+      int r = tl[i / P.Kp], q = i % P.Kp;
       P.scratch_seq[row_base(P, b, r) + q] = P.seq[row_base(P, b, r) + q];
     }
-    for (int r = threadIdx.x; r < m; r += blockDim.x)
-      P.scratch_meta[(size_t)b * J + r] = P.rmeta[(size_t)b * J + r];
-    if (threadIdx.x == 0) s_flag = 0;
+    for (int i = threadIdx.x; i < s_nt; i += blockDim.x)
+      P.scratch_meta[(size_t)b * J + tl[i]] = P.rmeta[(size_t)b * J + tl[i]];
     __syncthreads();
     for (int t = threadIdx.x; t < nm; t += blockDim.x) {
       Cand c = unpack_key(sel[t]);
@@ -550,6 +582,27 @@ __global__ void __launch_bounds__(256) k_select(DevInst I, DevPop P, LsParams L)
     }
     // drop_empty_routes (model.py:198-199), stable; DI tails were appended at m+t
     const int m2 = m + (op == 4 ? nm : 0);
+    if (threadIdx.x == 0) {
+      int e = 0;
+      for (int i = 0; i < s_nt; i++) e |= P.rmeta[(size_t)b * J + tl[i]].x == 0;
+      s_empty = e;
+    }
+    __syncthreads();
+    if (!s_empty) {
+      // no index shifts: only the touched routes and the appended depot-insert
+      // tails change; their tables, terms and SolutionIndex entries are rebuilt
+      if (threadIdx.x == 0) {
+        int nt = s_nt;
+        for (int r = m; r < m2; r++) tl[nt++] = r;
+        s_nt = nt;
+        P.m[b] = m2;
+        s_mnew = m2;
+      }
+      __syncthreads();
+      rebuild_routes<WIN>(I, P, b, tl, s_nt);
+      __syncthreads();
+      rebuild_fleet(I, P, b, sm_cnt);
+    } else {
     if (threadIdx.x < 32) {
       int carry = 0;
       for (int base = 0; base < m2; base += 32) {
@@ -569,16 +622,18 @@ __global__ void __launch_bounds__(256) k_select(DevInst I, DevPop P, LsParams L)
     for (int r = threadIdx.x; r < m2; r += blockDim.x)
       if (newidx[r] >= 0) P.scratch_meta[(size_t)b * J + newidx[r]] = P.rmeta[(size_t)b * J + r];
     __syncthreads();
-    const int mn = s_mnew;
-    for (int i = threadIdx.x; i < mn * P.Kp; i += blockDim.x) {
+    const int mn_ = s_mnew;
+    for (int i = threadIdx.x; i < mn_ * P.Kp; i += blockDim.x) {
       int r = i / P.Kp, q = i - r * P.Kp;
       P.seq[row_base(P, b, r) + q] = P.scratch_seq[row_base(P, b, r) + q];
     }
-    for (int r = threadIdx.x; r < mn; r += blockDim.x)
+    for (int r = threadIdx.x; r < mn_; r += blockDim.x)
       P.rmeta[(size_t)b * J + r] = P.scratch_meta[(size_t)b * J + r];
-    if (threadIdx.x == 0) P.m[b] = mn;
+    if (threadIdx.x == 0) P.m[b] = mn_;
     __syncthreads();
     rebuild_block<WIN>(I, P, b, sm_cnt);
+    }
+    const int mn = s_mnew;
     // ---- totals, adapt_penalties, bookkeeping (localsearch.py:128-138)
     if (threadIdx.x == 0) {
       const double4 *RC = P.rcon + (size_t)b * J;
@@ -767,7 +822,7 @@ __global__ void __launch_bounds__(1024) k_pack(DevPop P, int B, int best, int *r
 // launchers
 // ---------------------------------------------------------------------------
 static size_t select_smem(const DevPop &P) {
-  return sizeof(unsigned long long) * P.J + sizeof(unsigned) * (P.J / 32 + 1) + sizeof(int) * (2 * P.J + P.ND + 4);
+  return sizeof(unsigned long long) * P.J + sizeof(unsigned) * (P.J / 32 + 1) + sizeof(int) * (5 * P.J + P.ND + 8);
 }
 
 void launch_rebuild(const DevInst &I, const DevPop &P, int B, bool win, cudaStream_t s) {
