@@ -10,6 +10,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -138,6 +139,19 @@ int mdr_instance_create(const mdr_instance_desc *d, int32_t device, mdr_instance
   D.win = d->has_windows ? 1 : 0;
   D.gamma = d->gamma; D.theta = d->theta;
   D.rQ = 1.0 / d->capacity;
+  {
+    // exact (bitwise) symmetry of dist and time enables row-oriented link reads
+    int sym = 1;
+    for (int x = 0; x < N && sym; x++)
+      for (int y = x + 1; y < N; y++) {
+        size_t a = (size_t)x * N + y, b = (size_t)y * N + x;
+        if (memcmp(&d->dist[a], &d->dist[b], 8) || (!D.talias && memcmp(&d->time[a], &d->time[b], 8))) {
+          sym = 0;
+          break;
+        }
+      }
+    D.sym = getenv("MDR_NO_SYM") ? 0 : sym;
+  }
   D.rD = 1.0 / d->max_duration;
   cudaError_t e = cudaDeviceSynchronize();
   if (e != cudaSuccess) {
@@ -170,6 +184,8 @@ int mdr_pop_create(mdr_instance *inst, int32_t Bcap, int32_t J, int32_t K, int32
   const DevInst &I = inst->I;
   P.Bcap = Bcap; P.J = J; P.K = K; P.Kp = K + 2; P.Fcap = Fcap; P.FE = I.win ? 6 : 4;
   P.N = I.N; P.ND = I.ND;
+  P.staged = (J * 160 <= 96 * 1024) ? 1 : 0;  // RB staging fits shared memory
+  if (getenv("MDR_NO_STAGED")) P.staged = 0;
   auto &A = p->allocs;
   size_t rows = (size_t)Bcap * J, slots = rows * P.Kp;
   DA(A, P.m, Bcap);

@@ -33,6 +33,7 @@ struct DevInst {
   int d_on, nv_on, open, win;
   double gamma, theta;
   double rQ, rD;  // RN(1/Q), RN(1/Dmax) for div_q (host IEEE division)
+  int sym;        // dist (and time) exactly symmetric: m[x][y] == m[y][x] bit for bit
 };
 
 // per-individual search state (localsearch.py:107-140 loop variables)
@@ -46,6 +47,7 @@ struct LsState {
 
 struct DevPop {
   int Bcap, J, K, Kp, Fcap, FE;
+  int staged;  // relocate/swap/2-opt* use the CTA-staged evaluators (mdr_staged.cuh)
   int N, ND;
   int *m;
   int4 *rmeta;
@@ -132,12 +134,28 @@ __device__ __forceinline__ At<WIN> a_node(const DevInst &I, int v) {
   return a;
 }
 
-// vconcat (batch.py:223-262) of two non-empty subsequences
+// distance/time link a.last -> b.first.  When the matrices are exactly
+// symmetric the caller may name the warp-uniform end so the read comes from
+// that node's (L1-resident) row; the value is identical by symmetry.
+struct Link {
+  double c, t;
+};
+__device__ __forceinline__ Link link_of(const DevInst &I, int x, int y) {
+  size_t lk = (size_t)x * (size_t)I.N + (size_t)y;
+  Link L;
+  L.c = __ldg(I.dist + lk);
+  L.t = I.talias ? L.c : __ldg(I.time + lk);
+  return L;
+}
+// link x -> y where y is warp-uniform
+__device__ __forceinline__ Link link_to_u(const DevInst &I, int x, int y) {
+  return I.sym ? link_of(I, y, x) : link_of(I, x, y);
+}
+
+// vconcat (batch.py:223-262) of two non-empty subsequences with a given link
 template <bool WIN>
-__device__ __forceinline__ At<WIN> a_cat_ne(const DevInst &I, const At<WIN> &a, const At<WIN> &b) {
-  size_t lk = (size_t)a.last * (size_t)I.N + (size_t)b.first;
-  double c = __ldg(I.dist + lk);
-  double t = I.talias ? c : __ldg(I.time + lk);
+__device__ __forceinline__ At<WIN> a_cat_l(const At<WIN> &a, const At<WIN> &b, Link L) {
+  const double c = L.c, t = L.t;
   At<WIN> o;
   o.dist = (a.dist + c) + b.dist;
   o.load = a.load + b.load;
@@ -156,6 +174,11 @@ __device__ __forceinline__ At<WIN> a_cat_ne(const DevInst &I, const At<WIN> &a, 
   o.first = a.first;
   o.last = b.last;
   return o;
+}
+
+template <bool WIN>
+__device__ __forceinline__ At<WIN> a_cat_ne(const DevInst &I, const At<WIN> &a, const At<WIN> &b) {
+  return a_cat_l<WIN>(a, b, link_of(I, a.last, b.first));
 }
 
 // vconcat with possibly empty operands: an empty side is the exact identity

@@ -279,8 +279,8 @@ __device__ void task_relocate(const DevInst &I, const DevPop &P, const IV &v, in
             S2 = suf<WIN>(v, rv, tgt + 1, m2.x + (I.open ? 1 : 2));
             loaded = true;
           }
-          At<WIN> seg = len == 1 ? ld_at<WIN>(U + 10, u, u) : ld_at<WIN>(U + 16, u, nxt);
-          if (rev) swap_ends(seg);
+          At<WIN> seg = ld_at<WIN>(U + (len == 1 ? 10 : 16), rev ? (len == 1 ? u : nxt) : u,
+                                   rev ? u : (len == 1 ? u : nxt));
           At<WIN> B = a_cat_ne<WIN>(I, P2, seg);
           if (S2.first >= 0) B = a_cat_ne<WIN>(I, B, S2);
           double cB[5], nw[5];
@@ -380,8 +380,8 @@ __device__ void task_swap(const DevInst &I, const DevPop &P, const IV &v, int b,
             key = pack_key(c);
           } else if (pu + lu_ <= k1 && pv + lv_ <= m2.x) {
             const int k2 = m2.x, n2 = k2 + (I.open ? 1 : 2);
-            At<WIN> sA = lu_ == 1 ? ld_at<WIN>(U, u, u) : ld_at<WIN>(U + 6, u, nxtu);
-            if (au) swap_ends(sA);
+            const int ua = lu_ == 1 ? u : nxtu;
+            At<WIN> sA = ld_at<WIN>(U + (lu_ == 1 ? 0 : 6), au ? ua : u, au ? u : ua);
             At<WIN> sB = segB;
             if (av) swap_ends(sB);
             At<WIN> A = a_cat_ne<WIN>(I, ld_at<WIN>(U + 12, dep1, lastP1), sB);

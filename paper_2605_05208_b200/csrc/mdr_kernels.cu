@@ -14,6 +14,7 @@
 #include <cstdio>
 
 #include "mdr_fused.cuh"
+#include "mdr_staged.cuh"
 #include "mdr_kernels.cuh"
 
 namespace mdr {
@@ -204,7 +205,7 @@ __global__ void __launch_bounds__(1024) k_plan(DevInst I, DevPop P, LsParams L) 
     if (!st.done) {
       int op = P.perms[((size_t)b * P.maxp + st.pass) * P.nops + st.pos];
       P.op_cur[b] = op;
-      P.wsize[b] = op_tasks(op, P.m[b], I.NC, I.win);
+      P.wsize[b] = (P.staged && op <= 2) ? op_tasks_c(op, P.m[b], I.NC) : op_tasks(op, P.m[b], I.NC, I.win);
     } else {
       P.op_cur[b] = -1;
       P.wsize[b] = 0;
@@ -303,6 +304,73 @@ __global__ void __launch_bounds__(256, MDR_EVAL_MINB) k_eval(DevInst I, DevPop P
         }
       }
     }
+  }
+}
+
+// CTA-task evaluators (relocate, swap, 2-opt*) with staged route boundaries
+template <bool WIN, int OP>
+__global__ void __launch_bounds__(256, MDR_EVAL_MINB) k_eval_c(DevInst I, DevPop P, LsParams L) {
+  extern __shared__ __align__(16) unsigned char smx_c[];
+  RB *R = reinterpret_cast<RB *>(smx_c);
+  __shared__ double s_u[8][MDR_USLOT];
+  __shared__ int s_t, s_b, s_lo;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  double *U = s_u[wid];
+  const int total = P.optasks[OP];
+  const int cnt = P.opcnt[OP];
+  const int *OFF = P.opoff + OP * (P.Bcap + 1);
+  const int *OB = P.opb + OP * P.Bcap;
+  const bool mm = L.multi_move != 0;
+  const int nch = (I.NC + MDR_CU - 1) / MDR_CU;
+  int staged = -1;
+  for (;;) {
+    if (threadIdx.x == 0) {
+      int t = atomicAdd(P.task_next + OP, 1);
+      s_t = t;
+      if (t < total) {
+        int l2 = 0, h2 = cnt - 1;
+        while (l2 < h2) {
+          int mid = (l2 + h2 + 1) >> 1;
+          if (OFF[mid] <= t) l2 = mid; else h2 = mid - 1;
+        }
+        s_b = OB[l2];
+        s_lo = OFF[l2];
+      }
+    }
+    __syncthreads();
+    const int t = s_t;
+    if (t >= total) break;
+    const int b = s_b, local = t - s_lo;
+    const IV v = make_iv(P, b);
+    if (b != staged) {
+      stage_routes<WIN>(I, v, R);
+      staged = b;
+    }
+    __syncthreads();
+    double lam[4];
+#pragma unroll
+    for (int i = 0; i < 4; i++) lam[i] = P.lam[b * 4 + i];
+    Acc acc{~0ull, ~0ull, 0};
+    if (OP == 2 && local >= nch) {
+      const int ra = (local - nch) * MDR_CU + wid;
+      if (ra < v.M) stos_r<WIN>(I, P, v, R, b, ra, lam, mm, acc);
+    } else {
+      const int u = I.ND + local * MDR_CU + wid;
+      if (u < I.N) {
+        if (OP == 0) srelocate<WIN>(I, P, v, R, b, u, lam, mm, acc, U);
+        else if (OP == 1) sswap<WIN>(I, P, v, R, b, u, lam, mm, acc, U);
+        else stos_u<WIN>(I, P, v, R, b, u, lam, mm, acc, U);
+      }
+    }
+    OK r = warp_min(OK{acc.o, acc.k});
+    int n = acc.n;
+#pragma unroll
+    for (int s = 16; s > 0; s >>= 1) n += __shfl_xor_sync(0xffffffffu, n, s);
+    if (lane == 0) {
+      leader_min(P.leader + b, r.o, r.k);
+      if (n) atomicAdd(&P.cands[(size_t)b * 6 + OP], (unsigned long long)n);
+    }
+    __syncthreads();
   }
 }
 
@@ -854,9 +922,37 @@ static void launch_eval_t(const DevInst &I, const DevPop &P, const LsParams &L, 
     g[0] = grid_for(k_eval<WIN, 0>); g[1] = grid_for(k_eval<WIN, 1>); g[2] = grid_for(k_eval<WIN, 2>);
     g[3] = grid_for(k_eval<WIN, 3>); g[4] = grid_for(k_eval<WIN, 4>); g[5] = grid_for(k_eval<WIN, 5>);
   }
-  k_eval<WIN, 0><<<g[0], 256, 0, s>>>(I, P, L);
-  k_eval<WIN, 1><<<g[1], 256, 0, s>>>(I, P, L);
-  k_eval<WIN, 2><<<g[2], 256, 0, s>>>(I, P, L);
+  if (P.staged) {
+    static int gc[3] = {0, 0, 0};
+    const size_t sm = sizeof(RB) * (size_t)P.J;
+    static size_t sm_set = 0;
+    if (sm_set < sm) {
+      cudaFuncSetAttribute(k_eval_c<WIN, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      cudaFuncSetAttribute(k_eval_c<WIN, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      cudaFuncSetAttribute(k_eval_c<WIN, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      sm_set = sm;
+      gc[0] = 0;
+    }
+    if (!gc[0]) {
+      int dev = 0, sms = 148;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      int per = 1;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_eval_c<WIN, 0>, 256, sm);
+      gc[0] = sms * (per < 1 ? 1 : per);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_eval_c<WIN, 1>, 256, sm);
+      gc[1] = sms * (per < 1 ? 1 : per);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_eval_c<WIN, 2>, 256, sm);
+      gc[2] = sms * (per < 1 ? 1 : per);
+    }
+    k_eval_c<WIN, 0><<<gc[0], 256, sm, s>>>(I, P, L);
+    k_eval_c<WIN, 1><<<gc[1], 256, sm, s>>>(I, P, L);
+    k_eval_c<WIN, 2><<<gc[2], 256, sm, s>>>(I, P, L);
+  } else {
+    k_eval<WIN, 0><<<g[0], 256, 0, s>>>(I, P, L);
+    k_eval<WIN, 1><<<g[1], 256, 0, s>>>(I, P, L);
+    k_eval<WIN, 2><<<g[2], 256, 0, s>>>(I, P, L);
+  }
   if (!WIN) k_eval<WIN, 3><<<g[3], 256, 0, s>>>(I, P, L);
   k_eval<WIN, 4><<<g[4], 256, 0, s>>>(I, P, L);
   k_eval<WIN, 5><<<g[5], 256, 0, s>>>(I, P, L);

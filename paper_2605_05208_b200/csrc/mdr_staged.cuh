@@ -1,0 +1,436 @@
+// mdr_staged.cuh -- CTA-task evaluators for relocate, swap and 2-opt* with
+// the individual's per-route boundary data staged in shared memory.
+//
+// A CTA task is (individual b, 8 customers): every warp owns one customer u
+// (or, for the 2-opt* route-pair family, one route ra).  Before its warps
+// start, the CTA stages for every route r of b: meta, old route terms, the
+// suffix after the departure depot S[r][1] and the prefix up to the last
+// customer P[r][k].  These are exactly the pieces of the route-boundary
+// candidate families (moves.py:289-310, 390-404) -- ~75 % of relocate and
+// 2-opt* candidates -- which then need nothing from global memory except
+// their distance links.  Evaluation order inside a task differs from the
+// reference's enumeration order; the result does not (every candidate is
+// scored independently and reduced by (dF, key)).
+#pragma once
+#include "mdr_fused.cuh"
+
+namespace mdr {
+
+struct RB {
+  double sf[6];  // S[r][1] (suffix after the departure depot), empty when n-1 < 1
+  double pb[6];  // P[r][k] (prefix up to the last customer)
+  double rc[4];  // route D, V1, V2, V3
+  int k, dep, arr, clo;
+  int sf_first, sf_last, pb_last, n;
+};
+
+template <bool WIN>
+__device__ __forceinline__ void stage_routes(const DevInst &I, const IV &v, RB *R) {
+  for (int r = threadIdx.x; r < v.M; r += blockDim.x) {
+    const int4 mt = __ldg(v.rm + r);
+    const int n = mt.x + (I.open ? 1 : 2);
+    const int *sq = v.seq + r * v.Kp;
+    RB &x = R[r];
+    x.k = mt.x; x.dep = mt.y; x.arr = mt.z; x.clo = mt.w; x.n = n;
+    const double4 rc = ldg4(v.rc + r);
+    x.rc[0] = rc.x; x.rc[1] = rc.y; x.rc[2] = rc.z; x.rc[3] = rc.w;
+    if (n - 1 >= 1) {
+      st_at<WIN>(x.sf, ld_tab<WIN>(v.tS, r * v.Kp + 1));
+      x.sf_first = __ldg(sq + 1);
+      x.sf_last = __ldg(sq + n - 1);
+    } else {
+      x.sf_first = -1;
+      x.sf_last = -1;
+    }
+    st_at<WIN>(x.pb, ld_tab<WIN>(v.tP, r * v.Kp + mt.x));
+    x.pb_last = __ldg(sq + mt.x);
+  }
+}
+
+template <bool WIN>
+__device__ __forceinline__ At<WIN> rb_sf(const RB &x) { return ld_at<WIN>(x.sf, x.sf_first, x.sf_last); }
+template <bool WIN>
+__device__ __forceinline__ At<WIN> rb_pb(const RB &x) { return ld_at<WIN>(x.pb, x.dep, x.pb_last); }
+
+// (0 + cA) + cB, old terms, fleet delta, combine (batch.py:545-553) and record
+template <bool WIN>
+__device__ __forceinline__ bool two_route_delta(const DevInst &I, const double cA[5], const double cB[5],
+                                                const double *rc1, const double *rc2, int clo1, int clo2,
+                                                double fleet_delta, int fn, const double lam[4], Acc &acc,
+                                                unsigned long long key, bool mm, int *nanflag,
+                                                unsigned long long &o) {
+  double nw[5];
+#pragma unroll
+  for (int f = 0; f < 5; f++) nw[f] = (0.0 + cA[f]) + cB[f];
+  double old[5] = {rc1[0] + rc2[0], rc1[1] + rc2[1], rc1[2] + rc2[2], rc1[3] + rc2[3], (double)clo1 + (double)clo2};
+  Delta D;
+  finish_delta(I, nw, old, fleet_delta, lam, D);
+  D.fn = fn;
+  bool f = record(acc, D, key, mm, nanflag);
+  o = ord_of(D.dF);
+  return f;
+}
+
+// ---------------------------------------------------------------------------
+// RELOCATE (moves.py:280-311, batch.py:391-428), warp task = customer u
+// ---------------------------------------------------------------------------
+template <bool WIN>
+__device__ void srelocate(const DevInst &I, const DevPop &P, const IV &v, const RB *R, int b, int u,
+                          const double lam[4], bool mm, Acc &acc, double *U) {
+  const int lane = threadIdx.x & 31;
+  const int lu = __ldg(v.loc + u);
+  if (lu < 0) return;
+  const int ru = loc_r(lu), pu = loc_p(lu);
+  const RB &X1 = R[ru];
+  const int k1 = X1.k;
+  const int nxt = pu + 2 <= k1 ? __ldg(v.seq + ru * v.Kp + pu + 2) : u;
+  // U[0..4] removal terms l=1, U[5..9] l=2, U[10..15] seg l=1, U[16..21] seg l=2
+  if (lane == 0) {
+    const int n1 = X1.n;
+    At<WIN> P1 = pre<WIN>(v, ru, pu);
+    for (int l = 1; l <= 2; l++) {
+      if (pu + l <= k1) {
+        At<WIN> A = P1;
+        if (pu + l + 1 <= n1 - 1) A = a_cat_ne<WIN>(I, P1, suf<WIN>(v, ru, pu + l + 1, n1));
+        contrib_fast<WIN>(I, A, X1.dep, X1.arr, k1 - l, U + 5 * (l - 1));
+      }
+    }
+    At<WIN> s1 = a_node<WIN>(I, u);
+    st_at<WIN>(U + 10, s1);
+    if (pu + 2 <= k1) st_at<WIN>(U + 16, a_cat_ne<WIN>(I, s1, a_node<WIN>(I, nxt)));
+  }
+  __syncwarp();
+  const int nvar = I.win ? 2 : 3;
+  const double fdec1 = I.nv_on ? __ldg(v.fl + X1.dep).y : 0.0;
+  // one candidate: target (r2, tgt) with prefix P2 and (possibly empty) suffix S2
+  auto eval_inter = [&](int len, int rev, int r2, int tgt, const At<WIN> &P2, const At<WIN> &S2,
+                        const RB &X2, unsigned long long &o, unsigned long long key) -> bool {
+    At<WIN> seg = ld_at<WIN>(U + (len == 1 ? 10 : 16), rev ? (len == 1 ? u : nxt) : u, rev ? u : (len == 1 ? u : nxt));
+    At<WIN> B = a_cat_l<WIN>(P2, seg, link_to_u(I, P2.last, seg.first));
+    if (S2.first >= 0) B = a_cat_l<WIN>(B, S2, link_of(I, seg.last, S2.first));
+    double cB[5];
+    contrib_fast<WIN>(I, B, X2.dep, X2.arr, X2.k + len, cB);
+    double fleet_delta = 0.0;
+    int fn = 1;
+    if (I.nv_on && k1 - len == 0) { fleet_delta = 0.0 + fdec1; fn = 0; }
+    return two_route_delta<WIN>(I, U + 5 * (len - 1), cB, X1.rc, X2.rc, X1.clo, X2.clo, fleet_delta, fn, lam, acc,
+                                key, mm, P.nanflag + b, o);
+  };
+  // granular targets: insert after v (p2 = pv + 1)
+  const int W = I.W;
+  const int *lst = I.lists + (size_t)(u - I.ND) * W;
+  for (int base = 0; base < W; base += 32) {
+    const int t = base + lane;
+    int rv = -1, tgt = -1;
+    if (t < W) {
+      int vv = __ldg(lst + t);
+      if (vv >= 0) {
+        int lv = __ldg(v.loc + vv);
+        if (lv >= 0) { rv = loc_r(lv); tgt = loc_p(lv) + 1; }
+      }
+    }
+    const bool same = rv == ru;
+    At<WIN> P2, S2;
+    if (rv >= 0 && !same) {
+      P2 = pre<WIN>(v, rv, tgt);
+      S2 = suf<WIN>(v, rv, tgt + 1, R[rv].n);
+    }
+    for (int vi = 0; vi < nvar; vi++) {
+      const int len = vi == 0 ? 1 : 2, rev = vi == 2;
+      bool ok = rv >= 0 && pu + len <= k1 && !(same && tgt > pu && tgt <= pu + len);
+      if (!rev) ok = ok && !(same && tgt == pu);
+      bool fol = false, gqf = false;
+      unsigned long long o = 0, key = 0;
+      if (ok) {
+        key = key_of(ru, pu, rv, tgt, len, 0, rev, 0, -1, -1);
+        if (same) gqf = true;
+        else fol = eval_inter(len, rev, rv, tgt, P2, S2, R[rv], o, key);
+      }
+      append_fol(P, b, fol, o, key);
+      enqueue_g(P, b, 0, gqf, key);
+    }
+  }
+  // boundary targets: front (p2 = 0) and back (p2 = k_rb) of every route rb
+  for (int base = 0; base < v.M; base += 32) {
+    const int rb = base + lane;
+    const bool in = rb < v.M;
+    const bool same = rb == ru;
+    for (int side = 0; side < 2; side++) {
+      int tgt = 0;
+      At<WIN> P2, S2;
+      if (in) {
+        const RB &X2 = R[rb];
+        if (side == 0) {
+          tgt = 0;
+          P2 = a_node<WIN>(I, X2.dep);
+          S2 = X2.sf_first >= 0 ? rb_sf<WIN>(X2) : a_empty<WIN>();
+        } else {
+          tgt = X2.k;
+          P2 = rb_pb<WIN>(X2);
+          S2 = I.open ? a_empty<WIN>() : a_node<WIN>(I, X2.arr);
+        }
+      }
+      for (int vi = 0; vi < nvar; vi++) {
+        const int len = vi == 0 ? 1 : 2, rev = vi == 2;
+        bool ok = in && pu + len <= k1 && !(same && tgt == pu + len);
+        if (!rev) ok = ok && !(same && tgt == pu);
+        bool fol = false, gqf = false;
+        unsigned long long o = 0, key = 0;
+        if (ok) {
+          key = key_of(ru, pu, rb, tgt, len, 0, rev, 0, -1, -1);
+          if (same) gqf = true;
+          else fol = eval_inter(len, rev, rb, tgt, P2, S2, R[rb], o, key);
+        }
+        append_fol(P, b, fol, o, key);
+        enqueue_g(P, b, 0, gqf, key);
+      }
+    }
+  }
+  __syncwarp();
+}
+
+// ---------------------------------------------------------------------------
+// SWAP (moves.py:314-358, batch.py:430-463), warp task = customer u
+// ---------------------------------------------------------------------------
+template <bool WIN>
+__device__ void sswap(const DevInst &I, const DevPop &P, const IV &v, const RB *R, int b, int u, const double lam[4],
+                      bool mm, Acc &acc, double *U) {
+  const int lane = threadIdx.x & 31;
+  const int lu = __ldg(v.loc + u);
+  if (lu < 0) return;
+  const int ru = loc_r(lu), pu = loc_p(lu);
+  const RB &X1 = R[ru];
+  const int k1 = X1.k, n1 = X1.n;
+  const int nxtu = pu + 2 <= k1 ? __ldg(v.seq + ru * v.Kp + pu + 2) : u;
+  const int dep1 = X1.dep, lastP1 = __ldg(v.seq + ru * v.Kp + pu);
+  // U[0..5] seg u l=1, U[6..11] seg u l=2, U[12..17] prefix (0..pu)
+  if (lane == 0) {
+    At<WIN> s1 = a_node<WIN>(I, u);
+    st_at<WIN>(U, s1);
+    if (pu + 2 <= k1) st_at<WIN>(U + 6, a_cat_ne<WIN>(I, s1, a_node<WIN>(I, nxtu)));
+    st_at<WIN>(U + 12, pre<WIN>(v, ru, pu));
+  }
+  __syncwarp();
+  const int W = I.W;
+  const int *lst = I.lists + (size_t)(u - I.ND) * W;
+  for (int base = 0; base < W; base += 32) {
+    const int t = base + lane;
+    int vv = t < W ? __ldg(lst + t) : -1;
+    int rv = -1, pv = -1;
+    if (vv >= 0 && vv != u) {
+      int lv = __ldg(v.loc + vv);
+      if (lv >= 0) { rv = loc_r(lv); pv = loc_p(lv); }
+    }
+    const bool same = rv == ru;
+    const bool inter = rv >= 0 && !same;
+    int k2 = 0, n2 = 0, nxtv = vv;
+    At<WIN> P2;
+    if (inter) {
+      k2 = R[rv].k;
+      n2 = R[rv].n;
+      P2 = pre<WIN>(v, rv, pv);
+      if (pv + 2 <= k2) nxtv = __ldg(v.seq + rv * v.Kp + pv + 2);
+    }
+    for (int lv_ = 1; lv_ <= 2; lv_++) {
+      At<WIN> segB;
+      if (inter && pv + lv_ <= k2) {
+        segB = a_node<WIN>(I, vv);
+        if (lv_ == 2) segB = a_cat_ne<WIN>(I, segB, a_node<WIN>(I, nxtv));
+      }
+      const int ncomb = I.win ? 2 : (lv_ == 1 ? 3 : 6);
+      for (int ci = 0; ci < ncomb; ci++) {
+        int lu_, au, av;
+        if (I.win) { lu_ = ci + 1; au = 0; av = 0; }
+        else if (lv_ == 1) { lu_ = ci == 0 ? 1 : 2; au = ci == 2; av = 0; }
+        else { lu_ = ci < 2 ? 1 : 2; av = ci & 1; au = ci >= 4; }
+        bool fol = false, gqf = false;
+        unsigned long long o = 0, key = 0;
+        if (rv >= 0) {
+          if (same) {
+            int flip = pu > pv;
+            Cand c;
+            c.r1 = ru; c.r2 = rv;
+            c.p1 = flip ? pv : pu; c.p2 = flip ? pu : pv;
+            c.l1 = flip ? lv_ : lu_; c.l2 = flip ? lu_ : lv_;
+            c.rev1 = flip ? av : au; c.rev2 = flip ? au : av;
+            c.depot = -1; c.mode = -1;
+            gqf = (c.p1 + c.l1 <= k1) && (c.p2 + c.l2 <= k1) && (c.p2 >= c.p1 + c.l1);
+            key = pack_key(c);
+          } else if (pu + lu_ <= k1 && pv + lv_ <= k2) {
+            const int ua = lu_ == 1 ? u : nxtu;
+            At<WIN> sA = ld_at<WIN>(U + (lu_ == 1 ? 0 : 6), au ? ua : u, au ? u : ua);
+            At<WIN> sB = segB;
+            if (av) swap_ends(sB);
+            At<WIN> A = a_cat_l<WIN>(ld_at<WIN>(U + 12, dep1, lastP1), sB, link_of(I, lastP1, sB.first));
+            if (pu + lu_ + 1 <= n1 - 1) {
+              At<WIN> S1 = suf<WIN>(v, ru, pu + lu_ + 1, n1);
+              A = a_cat_l<WIN>(A, S1, link_to_u(I, sB.last, S1.first));
+            }
+            double cA[5], cB[5];
+            contrib_fast<WIN>(I, A, X1.dep, X1.arr, k1 - lu_ + lv_, cA);
+            At<WIN> B = a_cat_l<WIN>(P2, sA, link_to_u(I, P2.last, sA.first));
+            if (pv + lv_ + 1 <= n2 - 1) {
+              At<WIN> S2 = suf<WIN>(v, rv, pv + lv_ + 1, n2);
+              B = a_cat_l<WIN>(B, S2, link_of(I, sA.last, S2.first));
+            }
+            const RB &X2 = R[rv];
+            contrib_fast<WIN>(I, B, X2.dep, X2.arr, k2 - lv_ + lu_, cB);
+            key = key_of(ru, pu, rv, pv, lu_, lv_, au, av, -1, -1);
+            fol = two_route_delta<WIN>(I, cA, cB, X1.rc, X2.rc, X1.clo, X2.clo, 0.0, 1, lam, acc, key, mm,
+                                       P.nanflag + b, o);
+          }
+        }
+        append_fol(P, b, fol, o, key);
+        enqueue_g(P, b, 1, gqf, key);
+      }
+    }
+  }
+  __syncwarp();
+}
+
+// ---------------------------------------------------------------------------
+// TWO_OPT_STAR (moves.py:375-405, batch.py:475-494)
+// ---------------------------------------------------------------------------
+// A = PA (+) SB, B = PB (+) SA for the cut (r1, p1, r2, p2); SA/SB may be empty
+// uA / uB: which end of the A / B link is warp-uniform (0 = the prefix's last node, 1 = the suffix's first)
+template <bool WIN>
+__device__ __forceinline__ bool tos_eval(const DevInst &I, const DevPop &P, const IV &v, int b, const RB &X1,
+                                         const RB &X2, int r1, int p1, int r2, int p2, const At<WIN> &PA,
+                                         const At<WIN> &SB, const At<WIN> &PB, const At<WIN> &SA, int uA, int uB,
+                                         const double lam[4], Acc &acc, bool mm, unsigned long long &o,
+                                         unsigned long long &key) {
+  At<WIN> A = PA;
+  if (SB.first >= 0)
+    A = a_cat_l<WIN>(A, SB, uA ? link_to_u(I, PA.last, SB.first) : link_of(I, PA.last, SB.first));
+  At<WIN> B = PB;
+  if (SA.first >= 0)
+    B = a_cat_l<WIN>(B, SA, uB ? link_to_u(I, PB.last, SA.first) : link_of(I, PB.last, SA.first));
+  const int kA = p1 + (X2.k - p2), kB = p2 + (X1.k - p1);
+  double cA[5], cB[5];
+  contrib_fast<WIN>(I, A, X1.dep, X2.arr, kA, cA);
+  contrib_fast<WIN>(I, B, X2.dep, X1.arr, kB, cB);
+  double fleet_delta = 0.0;
+  int fn = 1;
+  if (I.nv_on) {
+    fleet_delta = (0.0 + (kA == 0 ? __ldg(v.fl + X1.dep).y : 0.0)) + (kB == 0 ? __ldg(v.fl + X2.dep).y : 0.0);
+    fn = (kA > 0) && (kB > 0);
+  }
+  key = key_of(r1, p1, r2, p2, 0, 0, 0, 0, -1, -1);
+  return two_route_delta<WIN>(I, cA, cB, X1.rc, X2.rc, X1.clo, X2.clo, fleet_delta, fn, lam, acc, key, mm,
+                              P.nanflag + b, o);
+}
+
+// warp task = customer u: granular cut and the two boundary families
+template <bool WIN>
+__device__ void stos_u(const DevInst &I, const DevPop &P, const IV &v, const RB *R, int b, int u, const double lam[4],
+                       bool mm, Acc &acc, double *U) {
+  const int lane = threadIdx.x & 31;
+  const int lu = __ldg(v.loc + u);
+  if (lu < 0) return;
+  const int ru = loc_r(lu), pu = loc_p(lu);
+  const RB &X1 = R[ru];
+  const int n1 = X1.n;
+  const int *sq1 = v.seq + ru * v.Kp;
+  // u-side pieces: U[0..5] P[ru][pu+1], U[6..11] S[ru][pu+2], U[12..17] P[ru][pu], U[18..23] S[ru][pu+1]
+  const int lastP0 = __ldg(sq1 + pu), s2first = pu + 2 <= n1 - 1 ? __ldg(sq1 + pu + 2) : -1;
+  const int lastS = __ldg(sq1 + n1 - 1);
+  if (lane == 0) {
+    st_at<WIN>(U, pre<WIN>(v, ru, pu + 1));
+    if (s2first >= 0) st_at<WIN>(U + 6, suf<WIN>(v, ru, pu + 2, n1));
+    st_at<WIN>(U + 12, pre<WIN>(v, ru, pu));
+    st_at<WIN>(U + 18, suf<WIN>(v, ru, pu + 1, n1));
+  }
+  __syncwarp();
+  const At<WIN> PU1 = ld_at<WIN>(U, X1.dep, u);
+  const At<WIN> SU2 = s2first >= 0 ? ld_at<WIN>(U + 6, s2first, lastS) : a_empty<WIN>();
+  // granular: (ru, pu+1, rv, pv)
+  const int W = I.W;
+  const int *lst = I.lists + (size_t)(u - I.ND) * W;
+  for (int base = 0; base < W; base += 32) {
+    const int t = base + lane;
+    int rv = -1, pv = 0;
+    if (t < W) {
+      int vv = __ldg(lst + t);
+      if (vv >= 0) {
+        int lv = __ldg(v.loc + vv);
+        if (lv >= 0 && loc_r(lv) != ru) { rv = loc_r(lv); pv = loc_p(lv); }
+      }
+    }
+    bool fol = false;
+    unsigned long long o = 0, key = 0;
+    if (rv >= 0) {
+      const RB &X2 = R[rv];
+      fol = tos_eval<WIN>(I, P, v, b, X1, X2, ru, pu + 1, rv, pv, PU1, suf<WIN>(v, rv, pv + 1, X2.n),
+                          pre<WIN>(v, rv, pv), SU2, 0, 1, lam, acc, mm, o, key);
+    }
+    append_fol(P, b, fol, o, key);
+  }
+  // boundary families for every route rb != ru
+  const At<WIN> PU0 = ld_at<WIN>(U + 12, X1.dep, lastP0);
+  const At<WIN> SU1 = ld_at<WIN>(U + 18, u, lastS);
+  for (int base = 0; base < v.M; base += 32) {
+    const int rb = base + lane;
+    const bool in = rb < v.M && rb != ru;
+    // (ru, pu+1, rb, k_rb): u's tail to the end of rb, minus "both tails empty, same arrival"
+    {
+      bool fol = false;
+      unsigned long long o = 0, key = 0;
+      if (in) {
+        const RB &X2 = R[rb];
+        bool drop = (pu + 1 == X1.k);
+        if (!I.open) drop = drop && (X1.arr == X2.arr);
+        if (!drop) {
+          At<WIN> SB = I.open ? a_empty<WIN>() : a_node<WIN>(I, X2.arr);
+          fol = tos_eval<WIN>(I, P, v, b, X1, X2, ru, pu + 1, rb, X2.k, PU1, SB, rb_pb<WIN>(X2), SU2, 0, 1, lam, acc,
+                              mm, o, key);
+        }
+      }
+      append_fol(P, b, fol, o, key);
+    }
+    // (rb, 0, ru, pu): rb's customers follow u's head
+    {
+      bool fol = false;
+      unsigned long long o = 0, key = 0;
+      if (in) {
+        const RB &X2 = R[rb];
+        At<WIN> SB = X2.sf_first >= 0 ? rb_sf<WIN>(X2) : a_empty<WIN>();
+        fol = tos_eval<WIN>(I, P, v, b, X2, X1, rb, 0, ru, pu, a_node<WIN>(I, X2.dep), SU1, PU0, SB, 1, 0, lam, acc,
+                            mm, o, key);
+      }
+      append_fol(P, b, fol, o, key);
+    }
+  }
+  __syncwarp();
+}
+
+// warp task = route ra: route pairs (ra, 0, rb, k_rb) (moves.py:401-404)
+template <bool WIN>
+__device__ void stos_r(const DevInst &I, const DevPop &P, const IV &v, const RB *R, int b, int ra, const double lam[4],
+                       bool mm, Acc &acc) {
+  const int lane = threadIdx.x & 31;
+  const RB &X1 = R[ra];
+  const At<WIN> PA = a_node<WIN>(I, X1.dep);
+  const At<WIN> SA = X1.sf_first >= 0 ? rb_sf<WIN>(X1) : a_empty<WIN>();
+  for (int base = 0; base < v.M; base += 32) {
+    const int rb = base + lane;
+    bool fol = false;
+    unsigned long long o = 0, key = 0;
+    if (rb < v.M && rb != ra) {
+      const RB &X2 = R[rb];
+      At<WIN> SB = I.open ? a_empty<WIN>() : a_node<WIN>(I, X2.arr);
+      fol = tos_eval<WIN>(I, P, v, b, X1, X2, ra, 0, rb, X2.k, PA, SB, rb_pb<WIN>(X2), SA, 0, 1, lam, acc, mm, o,
+                          key);
+    }
+    append_fol(P, b, fol, o, key);
+  }
+}
+
+#define MDR_CU 8  // customers (warps) per CTA task
+
+__host__ __device__ __forceinline__ int op_tasks_c(int op, int M, int NC) {
+  int nch = (NC + MDR_CU - 1) / MDR_CU;
+  if (op == 2) return M < 2 ? 0 : nch + (M + MDR_CU - 1) / MDR_CU;
+  return nch;
+}
+
+}  // namespace mdr
