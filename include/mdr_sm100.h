@@ -141,6 +141,12 @@ int mdr_totals(mdr_pop *pop, int32_t b, double out[5]);
 /* B_active = individuals 0..B-1 of the last upload. stats: [B] */
 int mdr_local_search(mdr_pop *pop, const mdr_ls_cfg *cfg, mdr_ls_stats *stats, void *stream);
 int mdr_get_timing(mdr_pop *pop, mdr_timing *out);
+
+/* n_passes results of CPython random.Random.shuffle(list(items)) continuing the
+ * MT19937 state of rng.getstate()[1] (624 words + index, advanced in place);
+ * out: [n_passes * n_items] or NULL (only advance).  Host-only; no GPU needed.
+ * Replaces the rng.shuffle calls of localsearch.py:112-113. */
+int mdr_shuffle_stream(uint32_t *state, int32_t n_items, const uint8_t *items, int32_t n_passes, uint8_t *out);
 int mdr_set_profiling(mdr_pop *pop, int32_t on);
 
 #ifdef __cplusplus

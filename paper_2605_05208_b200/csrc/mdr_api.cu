@@ -676,6 +676,59 @@ int mdr_totals(mdr_pop *p, int32_t b, double out[5]) {
 // ---------------------------------------------------------------------------
 // population-batched local search
 // ---------------------------------------------------------------------------
+// ---------------------------------------------------------------------------
+// operator permutation stream: CPython's random.Random.shuffle on MT19937
+// (Modules/_randommodule.c genrand_uint32, Lib/random.py shuffle /
+// _randbelow_with_getrandbits), driven by the state rng.getstate() exposes
+// ---------------------------------------------------------------------------
+static uint32_t mt_next(uint32_t *mt, uint32_t *idx) {
+  const int N = 624, M = 397;
+  const uint32_t A = 0x9908b0dfU, UP = 0x80000000U, LO = 0x7fffffffU;
+  uint32_t y;
+  if (*idx >= (uint32_t)N) {
+    int kk;
+    for (kk = 0; kk < N - M; kk++) {
+      y = (mt[kk] & UP) | (mt[kk + 1] & LO);
+      mt[kk] = mt[kk + M] ^ (y >> 1) ^ ((y & 1U) ? A : 0U);
+    }
+    for (; kk < N - 1; kk++) {
+      y = (mt[kk] & UP) | (mt[kk + 1] & LO);
+      mt[kk] = mt[kk + (M - N)] ^ (y >> 1) ^ ((y & 1U) ? A : 0U);
+    }
+    y = (mt[N - 1] & UP) | (mt[0] & LO);
+    mt[N - 1] = mt[M - 1] ^ (y >> 1) ^ ((y & 1U) ? A : 0U);
+    *idx = 0;
+  }
+  y = mt[(*idx)++];
+  y ^= (y >> 11);
+  y ^= (y << 7) & 0x9d2c5680U;
+  y ^= (y << 15) & 0xefc60000U;
+  y ^= (y >> 18);
+  return y;
+}
+
+int mdr_shuffle_stream(uint32_t *state, int32_t n_items, const uint8_t *items, int32_t n_passes, uint8_t *out) {
+  if (!state || !items || n_items < 1 || n_items > 64 || n_passes < 0) return fail(MDR_ERR_ARG, "bad shuffle arguments");
+  uint32_t *mt = state, *idx = state + 624;
+  if (*idx > 624) return fail(MDR_ERR_ARG, "bad MT19937 state index");
+  uint8_t tmp[64];
+  for (int p = 0; p < n_passes; p++) {
+    for (int i = 0; i < n_items; i++) tmp[i] = items[i];
+    for (int i = n_items - 1; i >= 1; i--) {
+      uint32_t n = (uint32_t)i + 1, k = 0;
+      while ((1u << k) <= n && k < 32) k++;  // n.bit_length()
+      uint32_t r;
+      do { r = mt_next(mt, idx) >> (32 - k); } while (r >= n);
+      uint8_t t = tmp[i];
+      tmp[i] = tmp[r];
+      tmp[r] = t;
+    }
+    if (out)
+      for (int i = 0; i < n_items; i++) out[(size_t)p * n_items + i] = tmp[i];
+  }
+  return MDR_OK;
+}
+
 int mdr_set_profiling(mdr_pop *p, int32_t on) {
   if (!p) return fail(MDR_ERR_ARG, "null pop");
   p->profiling = on;

@@ -13,6 +13,7 @@ Each individual's trajectory is bit-identical to a separate reference call.
 """
 from __future__ import annotations
 
+import ctypes as C
 import random
 import time
 from dataclasses import dataclass
@@ -90,24 +91,36 @@ def apply_moves(sol, moves, inst) -> None:
     sol.drop_empty_routes()
 
 
-def draw_permutations(rng, ops, n_passes: int) -> np.ndarray:
-    """The first n_passes `rng.shuffle(list(ops))` results, drawn on a clone."""
-    if not hasattr(rng, "getstate"):
+def _mt_state(rng):
+    if not (hasattr(rng, "getstate") and hasattr(rng, "setstate")):
         raise TypeError("rng must be a random.Random (getstate/setstate) so the operator stream can be pre-drawn")
-    clone = random.Random()
-    clone.setstate(rng.getstate())
+    st = rng.getstate()
+    if not (isinstance(st, tuple) and len(st) == 3 and len(st[1]) == 625):
+        raise TypeError("rng state is not a MT19937 random.Random state")
+    return st, np.ascontiguousarray(np.asarray(st[1], dtype=np.uint32))
+
+
+def draw_permutations(rng, ops, n_passes: int) -> np.ndarray:
+    """The first n_passes `rng.shuffle(list(ops))` results (rng not advanced):
+    CPython's shuffle on the MT19937 state, run natively (mdr_shuffle_stream)."""
+    from . import _lib
+    _, mt = _mt_state(rng)
+    items = np.ascontiguousarray([int(o) for o in ops], dtype=np.uint8)
     out = np.empty((n_passes, len(ops)), np.uint8)
-    for p in range(n_passes):
-        order = list(ops)
-        clone.shuffle(order)
-        out[p] = [int(o) for o in order]
+    _lib.check(_lib.lib().mdr_shuffle_stream(_lib.ptr(mt, C.POINTER(C.c_uint32)), len(items),
+                                             _lib.ptr(items, _lib.u8p), n_passes, _lib.ptr(out, _lib.u8p)),
+               "mdr_shuffle_stream")
     return out
 
 
 def _advance(rng, ops, passes: int) -> None:
-    for _ in range(passes):
-        order = list(ops)
-        rng.shuffle(order)
+    """Advance rng exactly as `passes` calls of rng.shuffle(list(ops)) would."""
+    from . import _lib
+    st, mt = _mt_state(rng)
+    items = np.ascontiguousarray([int(o) for o in ops], dtype=np.uint8)
+    _lib.check(_lib.lib().mdr_shuffle_stream(_lib.ptr(mt, C.POINTER(C.c_uint32)), len(items),
+                                             _lib.ptr(items, _lib.u8p), passes, None), "mdr_shuffle_stream")
+    rng.setstate((st[0], tuple(int(x) for x in mt), st[2]))
 
 
 class DeviceSearch:

@@ -48,3 +48,25 @@ def test_sm100a_code_is_in_the_library():
     out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", _lib.LIB_PATH],
                          capture_output=True, text=True).stdout
     assert "sm_100a" in out
+
+
+def test_native_shuffle_stream_equals_cpython_shuffle():
+    """mdr_shuffle_stream reproduces random.Random.shuffle bit for bit (no GPU needed)."""
+    import random
+    from paper_2605_05208_b200.localsearch import _advance, draw_permutations
+    for seed in (0, 1, 7, 12345, 2 ** 40 + 3):
+        for ops in ([0, 1, 2, 4, 5], [0, 1, 2, 3, 4, 5], [3], list(range(20))):
+            rng = random.Random(seed)
+            rng.random()  # arbitrary prior consumption
+            want_rng = random.Random()
+            want_rng.setstate(rng.getstate())
+            want = []
+            for _ in range(700):  # crosses several MT19937 regenerations
+                o = list(ops)
+                want_rng.shuffle(o)
+                want.append(o)
+            got = draw_permutations(rng, ops, 700)
+            assert got.tolist() == want
+            _advance(rng, ops, 700)
+            assert rng.getstate() == want_rng.getstate()
+            assert rng.random() == want_rng.random()
