@@ -92,6 +92,8 @@ typedef struct mdr_ls_stats {
   int32_t n_feasible;     /* feasible post-step states */
   int32_t n_improving;    /* feasible states that lowered the running minimum D */
   double best_feasible_D; /* +inf if none */
+  /* on MDR_ERR_CAPACITY: the capacities a retry needs (0 = not the cause) */
+  int32_t need_followers, need_queue, need_routes, need_positions;
 } mdr_ls_stats;
 
 typedef struct mdr_timing {

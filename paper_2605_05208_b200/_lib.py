@@ -56,7 +56,9 @@ class LsCfg(C.Structure):
 class LsStats(C.Structure):
     _fields_ = [("passes", C.c_int32), ("accepted", C.c_int32), ("op_evals", C.c_int32),
                 ("status", C.c_int32), ("cands", C.c_int64 * 6), ("moves_applied", C.c_int64),
-                ("n_feasible", C.c_int32), ("n_improving", C.c_int32), ("best_feasible_D", C.c_double)]
+                ("n_feasible", C.c_int32), ("n_improving", C.c_int32), ("best_feasible_D", C.c_double),
+                ("need_followers", C.c_int32), ("need_queue", C.c_int32), ("need_routes", C.c_int32),
+                ("need_positions", C.c_int32)]
 
 
 class Timing(C.Structure):

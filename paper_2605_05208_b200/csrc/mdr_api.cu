@@ -173,7 +173,7 @@ void mdr_instance_destroy(mdr_instance *I) {
 int mdr_pop_create(mdr_instance *inst, int32_t Bcap, int32_t J, int32_t K, int32_t Fcap, mdr_pop **out) {
   if (!inst || !out) return fail(MDR_ERR_ARG, "null argument");
   if (Bcap < 1 || J < 1 || K < 1 || Fcap < 1) return fail(MDR_ERR_ARG, "capacities must be >= 1");
-  if (J > 2046) return fail(MDR_ERR_ARG, "J_cap must be <= 2046 (11-bit route field of the packed key)");
+  if (J > 4094) return fail(MDR_ERR_ARG, "J_cap must be <= 4094 (12-bit route field of the packed key)");
   if (K > 500) return fail(MDR_ERR_ARG, "K_cap must be <= 500 (9-bit position field of the packed key)");
   CK(cudaSetDevice(inst->device));
   mdr_pop *p = new mdr_pop();
@@ -566,7 +566,7 @@ int mdr_leader_followers(mdr_pop *p, const mdr_cands *cs, const mdr_deltas *d, i
   long long n = cs->n;
   if (n == 0) return MDR_OK;
   for (long long i = 0; i < n; i++) {
-    if (cs->r1[i] < -1 || cs->r1[i] > 2045 || cs->r2[i] < -1 || cs->r2[i] > 2045 || cs->p1[i] < -1 ||
+    if (cs->r1[i] < -1 || cs->r1[i] > 4093 || cs->r2[i] < -1 || cs->r2[i] > 4093 || cs->p1[i] < -1 ||
         cs->p1[i] > 510 || cs->p2[i] < -1 || cs->p2[i] > 510 || cs->len1[i] < 0 || cs->len1[i] > 3 ||
         cs->len2[i] < 0 || cs->len2[i] > 3 || cs->depot[i] < -1 || cs->depot[i] > 254 || cs->mode[i] < -1 ||
         cs->mode[i] > 2)
@@ -648,7 +648,7 @@ int mdr_leader_followers(mdr_pop *p, const mdr_cands *cs, const mdr_deltas *d, i
       CK(cub::DeviceRadixSort::SortPairs(nullptr, t3, k1, k2, fidx, fidx2, nf, 0, 64, s));
       void *ts3 = nullptr;
       TA(ts3, t3 + 1);
-      CK(cub::DeviceRadixSort::SortPairs(ts3, t3, k1, k2, fidx, fidx2, nf, 0, 56, s));
+      CK(cub::DeviceRadixSort::SortPairs(ts3, t3, k1, k2, fidx, fidx2, nf, 0, 58, s));
       k_gather_u64<<<gb, 256, 0, s>>>(ord, fidx2, k1, nf);
       CK(cub::DeviceRadixSort::SortPairs(ts3, t3, k1, k2, fidx2, fidx, nf, 0, 64, s));
       CK(cudaMemcpyAsync(followers, fidx, sizeof(long long) * nf, cudaMemcpyDeviceToHost, s));
@@ -788,6 +788,7 @@ int mdr_local_search(mdr_pop *p, const mdr_ls_cfg *cfg, mdr_ls_stats *stats, voi
   if (prof) CK(cudaEventRecord(p->ev[6], s));
   long long rounds = 0;
   long long ev_used = 0;
+  const bool dbg = getenv("MDR_SYNC_DEBUG") != nullptr;  // sync + check after every kernel
   auto ev_at = [&](long long i) -> cudaEvent_t {
     while ((long long)p->rev.size() <= i) {
       cudaEvent_t e;
@@ -800,12 +801,16 @@ int mdr_local_search(mdr_pop *p, const mdr_ls_cfg *cfg, mdr_ls_stats *stats, voi
     for (int r = 0; r < rps; r++) {
       if (prof) cudaEventRecord(ev_at(ev_used), s);
       launch_plan(I, P, L, s);
+      if (dbg && cudaStreamSynchronize(s)) return fail(MDR_ERR_CUDA, "k_plan failed");
       if (prof) cudaEventRecord(ev_at(ev_used + 1), s);
       launch_eval(I, P, L, p->grid, I.win, s);
+      if (dbg && cudaStreamSynchronize(s)) return fail(MDR_ERR_CUDA, "k_eval failed");
       if (prof) cudaEventRecord(ev_at(ev_used + 2), s);
       launch_eval_g(I, P, L, p->grid, I.win, s);
+      if (dbg && cudaStreamSynchronize(s)) return fail(MDR_ERR_CUDA, "k_eval_g failed");
       if (prof) cudaEventRecord(ev_at(ev_used + 3), s);
       launch_select(I, P, L, I.win, s);
+      if (dbg && cudaStreamSynchronize(s)) return fail(MDR_ERR_CUDA, "k_select failed");
       if (prof) {
         cudaEventRecord(ev_at(ev_used + 4), s);
         ev_used += 5;
@@ -828,6 +833,7 @@ int mdr_local_search(mdr_pop *p, const mdr_ls_cfg *cfg, mdr_ls_stats *stats, voi
     cudaEventElapsedTime(&tot, p->ev[6], p->ev[7]);
     p->tm.total_ms += tot;
     p->tm.rounds += rounds;
+    FILE *rlog = getenv("MDR_ROUND_LOG") ? fopen(getenv("MDR_ROUND_LOG"), "w") : nullptr;
     for (long long e = 0; e + 4 < ev_used; e += 5) {
       float a = 0, b2 = 0, g = 0, c = 0;
       cudaEventElapsedTime(&a, p->rev[e], p->rev[e + 1]);
@@ -839,7 +845,9 @@ int mdr_local_search(mdr_pop *p, const mdr_ls_cfg *cfg, mdr_ls_stats *stats, voi
       p->tm.geval_ms += g;
       p->tm.select_ms += c;
       p->tm.eval_launches++;
+      if (rlog) fprintf(rlog, "%lld,%.4f,%.4f,%.4f,%.4f\n", e / 5, a, b2, g, c);
     }
+    if (rlog) fclose(rlog);
   }
   if (!prof) p->tm.rounds += rounds;
   std::vector<LsState> st(B > 0 ? B : 1);
@@ -865,6 +873,10 @@ int mdr_local_search(mdr_pop *p, const mdr_ls_cfg *cfg, mdr_ls_stats *stats, voi
       o.n_feasible = st[b].n_feasible;
       o.n_improving = st[b].n_improving;
       o.best_feasible_D = st[b].bestD;
+      o.need_followers = st[b].need_f;
+      o.need_queue = st[b].need_g;
+      o.need_routes = st[b].need_j;
+      o.need_positions = st[b].need_k;
     }
     if (st[b].status && !worst) worst = st[b].status;
   }

@@ -43,6 +43,7 @@ struct LsState {
   int n_improving, pad0;
   long long moves_applied;
   double bestD;
+  int need_f, need_g, need_j, need_k;  // capacity a retry needs (status 3)
 };
 
 struct DevPop {
@@ -298,9 +299,9 @@ struct Cand {
   int r1, p1, r2, p2, l1, l2, rev1, rev2, depot, mode;
 };
 
-// Move.key() order (moves.py:66-70) packed into 56 bits, -1 fields biased by 1
+// Move.key() order (moves.py:66-70) packed into 58 bits, -1 fields biased by 1
 __host__ __device__ __forceinline__ unsigned long long pack_key(const Cand &c) {
-  return ((unsigned long long)(c.r1 + 1) << 45) | ((unsigned long long)(c.r2 + 1) << 34) |
+  return ((unsigned long long)(c.r1 + 1) << 46) | ((unsigned long long)(c.r2 + 1) << 34) |
          ((unsigned long long)(c.p1 + 1) << 25) | ((unsigned long long)(c.p2 + 1) << 16) |
          ((unsigned long long)c.l1 << 14) | ((unsigned long long)c.l2 << 12) |
          ((unsigned long long)c.rev1 << 11) | ((unsigned long long)c.rev2 << 10) |
@@ -309,8 +310,8 @@ __host__ __device__ __forceinline__ unsigned long long pack_key(const Cand &c) {
 
 __host__ __device__ __forceinline__ Cand unpack_key(unsigned long long k) {
   Cand c;
-  c.r1 = (int)((k >> 45) & 0x7ff) - 1;
-  c.r2 = (int)((k >> 34) & 0x7ff) - 1;
+  c.r1 = (int)((k >> 46) & 0xfff) - 1;
+  c.r2 = (int)((k >> 34) & 0xfff) - 1;
   c.p1 = (int)((k >> 25) & 0x1ff) - 1;
   c.p2 = (int)((k >> 16) & 0x1ff) - 1;
   c.l1 = (int)((k >> 14) & 3);

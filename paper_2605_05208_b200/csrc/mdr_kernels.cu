@@ -56,30 +56,62 @@ __device__ __forceinline__ OK block_min(OK v, OK *sm) {
   return r;
 }
 
-// numpy pairwise summation (numpy/_core/src/umath/loops_utils.h.src), field f of rcon
-__device__ double pw_sum(const double4 *a, int f, int n) {
+// numpy pairwise summation (numpy/_core/src/umath/loops_utils.h.src), field f
+// of rcon.  The recursion (halves rounded down to a multiple of 8, blocks of
+// <= 128 summed with 8 accumulators) is run with an explicit stack: device
+// recursion would overflow the default per-thread stack for long route lists.
+__device__ __forceinline__ double pw_leaf(const double4 *a, int f, int n) {
   if (n < 8) {
     double res = 0.0;
     for (int i = 0; i < n; i++) res += (&a[i].x)[f];
     return res;
-  } else if (n <= 128) {
-    double r[8];
-    for (int j = 0; j < 8; j++) r[j] = (&a[j].x)[f];
-    int i;
-    for (i = 8; i < n - (n % 8); i += 8)
-      for (int j = 0; j < 8; j++) r[j] += (&a[i + j].x)[f];
-    double res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
-    for (; i < n; i++) res += (&a[i].x)[f];
-    return res;
   }
-  int n2 = n / 2;
-  n2 -= n2 % 8;
-  return pw_sum(a, f, n2) + pw_sum(a + n2, f, n - n2);
+  double r[8];
+  for (int j = 0; j < 8; j++) r[j] = (&a[j].x)[f];
+  int i;
+  for (i = 8; i < n - (n % 8); i += 8)
+    for (int j = 0; j < 8; j++) r[j] += (&a[i + j].x)[f];
+  double res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+  for (; i < n; i++) res += (&a[i].x)[f];
+  return res;
 }
 
-// ---------------------------------------------------------------------------
-// rebuild one individual (whole block): loc, tables, route terms, fleet
-// ---------------------------------------------------------------------------
+__device__ double pw_sum(const double4 *a, int f, int n) {
+  if (n <= 128) return pw_leaf(a, f, n);
+  int st_start[32], st_n[32], st_n2[32], st_state[32];
+  double st_left[32];
+  int sp = 0;
+  st_start[0] = 0; st_n[0] = n; st_state[0] = 0;
+  double ret = 0.0;
+  for (;;) {
+    const int S = st_start[sp], Nn = st_n[sp];
+    if (st_state[sp] == 0) {
+      if (Nn <= 128) {
+        ret = pw_leaf(a + S, f, Nn);
+        if (sp == 0) return ret;
+        --sp;
+        continue;
+      }
+      int n2 = Nn / 2;
+      n2 -= n2 % 8;
+      st_n2[sp] = n2;
+      st_state[sp] = 1;
+      ++sp;
+      st_start[sp] = S; st_n[sp] = n2; st_state[sp] = 0;
+    } else if (st_state[sp] == 1) {
+      st_left[sp] = ret;
+      st_state[sp] = 2;
+      const int n2 = st_n2[sp];
+      ++sp;
+      st_start[sp] = S + n2; st_n[sp] = Nn - n2; st_state[sp] = 0;
+    } else {
+      ret = st_left[sp] + ret;
+      if (sp == 0) return ret;
+      --sp;
+    }
+  }
+}
+
 // per-route part (warp per route): SolutionIndex entries of its customers,
 // prefix/suffix tables (lane i folds positions i..n-1 -- the left fold from i
 // of batch.py:99-124), route terms and closure flag.  list == nullptr: all m.
@@ -572,8 +604,8 @@ __global__ void __launch_bounds__(256) k_select(DevInst I, DevPop P, LsParams L)
   if (threadIdx.x == 0) {
     P.st[b].op_evals++;
     s_flag = 0;
-    if (has && L.multi_move && nf > P.Fcap) s_flag = 1;  // follower buffer overflow
-    if (*P.gcount > P.Gcap) s_flag = 1;                  // generic queue overflow
+    if (has && L.multi_move && nf > P.Fcap) { s_flag = 1; P.st[b].need_f = nf; }  // follower buffer overflow
+    if (*P.gcount > P.Gcap) { s_flag = 1; P.st[b].need_g = *P.gcount; }         // generic queue overflow
   }
   __syncthreads();
   if (s_flag) {
@@ -641,7 +673,11 @@ __global__ void __launch_bounds__(256) k_select(DevInst I, DevPop P, LsParams L)
     __syncthreads();
     for (int t = threadIdx.x; t < nm; t += blockDim.x) {
       Cand c = unpack_key(sel[t]);
-      if (!apply_one(I, P, b, op, c, m + t)) s_flag = 1;
+      if (!apply_one(I, P, b, op, c, m + t)) {
+        s_flag = 1;
+        atomicMax(&P.st[b].need_j, m + nm);
+        atomicMax(&P.st[b].need_k, 2 * P.K);
+      }
     }
     __syncthreads();
     if (s_flag) {
@@ -650,11 +686,11 @@ __global__ void __launch_bounds__(256) k_select(DevInst I, DevPop P, LsParams L)
     }
     // drop_empty_routes (model.py:198-199), stable; DI tails were appended at m+t
     const int m2 = m + (op == 4 ? nm : 0);
-    if (threadIdx.x == 0) {
-      int e = 0;
-      for (int i = 0; i < s_nt; i++) e |= P.rmeta[(size_t)b * J + tl[i]].x == 0;
-      s_empty = e;
-    }
+    // drop_empty_routes removes every empty route, including ones the input carried
+    if (threadIdx.x == 0) s_empty = 0;
+    __syncthreads();
+    for (int r = threadIdx.x; r < m; r += blockDim.x)
+      if (P.rmeta[(size_t)b * J + r].x == 0) s_empty = 1;
     __syncthreads();
     if (!s_empty) {
       // no index shifts: only the touched routes and the appended depot-insert

@@ -100,7 +100,7 @@ __device__ void srelocate(const DevInst &I, const DevPop &P, const IV &v, const 
     if (pu + 2 <= k1) st_at<WIN>(U + 16, a_cat_ne<WIN>(I, s1, a_node<WIN>(I, nxt)));
   }
   __syncwarp();
-  const int nvar = I.win ? 2 : 3;
+  constexpr int nvar = WIN ? 2 : 3;
   const double fdec1 = I.nv_on ? __ldg(v.fl + X1.dep).y : 0.0;
   // one candidate: target (r2, tgt) with prefix P2 and (possibly empty) suffix S2
   auto eval_inter = [&](int len, int rev, int r2, int tgt, const At<WIN> &P2, const At<WIN> &S2,
@@ -135,6 +135,7 @@ __device__ void srelocate(const DevInst &I, const DevPop &P, const IV &v, const 
       P2 = pre<WIN>(v, rv, tgt);
       S2 = suf<WIN>(v, rv, tgt + 1, R[rv].n);
     }
+#pragma unroll
     for (int vi = 0; vi < nvar; vi++) {
       const int len = vi == 0 ? 1 : 2, rev = vi == 2;
       bool ok = rv >= 0 && pu + len <= k1 && !(same && tgt > pu && tgt <= pu + len);
@@ -155,6 +156,7 @@ __device__ void srelocate(const DevInst &I, const DevPop &P, const IV &v, const 
     const int rb = base + lane;
     const bool in = rb < v.M;
     const bool same = rb == ru;
+#pragma unroll
     for (int side = 0; side < 2; side++) {
       int tgt = 0;
       At<WIN> P2, S2;
@@ -170,6 +172,7 @@ __device__ void srelocate(const DevInst &I, const DevPop &P, const IV &v, const 
           S2 = I.open ? a_empty<WIN>() : a_node<WIN>(I, X2.arr);
         }
       }
+#pragma unroll
       for (int vi = 0; vi < nvar; vi++) {
         const int len = vi == 0 ? 1 : 2, rev = vi == 2;
         bool ok = in && pu + len <= k1 && !(same && tgt == pu + len);

@@ -101,7 +101,7 @@ class Population:
     def caps_for(sols, inst):
         m = max((len(s.routes) for s in sols), default=1)
         k = max((len(r.customers) for s in sols for r in s.routes), default=1)
-        J = min(2046, max(2 * m, m + 64))
+        J = min(4094, max(2 * m, m + 64))
         K = min(500, max(2 * k, k + 16, 32))
         return J, K
 
@@ -176,6 +176,14 @@ class Population:
         stats = [dict(passes=x.passes, accepted=x.accepted, op_evals=x.op_evals, status=x.status,
                       cands=list(x.cands), moves_applied=x.moves_applied, n_feasible=x.n_feasible,
                       n_improving=x.n_improving, best_feasible_D=x.best_feasible_D) for x in st[:B]]
+        if rc == _lib.MDR_ERR_CAPACITY:
+            need = dict(F=max(x.need_followers for x in st[:B]), G=max(x.need_queue for x in st[:B]),
+                        J=max(x.need_routes for x in st[:B]), K=max(x.need_positions for x in st[:B]))
+            try:
+                check(rc, "mdr_local_search")
+            except CapacityError as e:
+                e.need = need
+                raise
         check(rc, "mdr_local_search")
         return stats
 

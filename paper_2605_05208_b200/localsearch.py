@@ -132,11 +132,16 @@ class DeviceSearch:
         self.pop: Optional[Population] = None
         self.last_stats = None
 
-    def _ensure(self, sols, scale: int = 1):
+    def _ensure(self, sols, need=None):
         J, K = Population.caps_for(sols, self.inst)
-        J = min(2046, J * scale)
-        K = min(500, K * scale)
-        F = (1 << 15) * scale
+        F = 1 << 15
+        if need:  # grow exactly what the failed attempt reported (at least doubling it)
+            p = self.pop
+            J = max(J, 2 * p.J_cap if need["J"] else J, need["J"] + 64)
+            K = max(K, need["K"])
+            F = max(F, p.F_cap * 2 if (need["F"] or need["G"]) else p.F_cap, need["F"] + 1024,
+                    (need["G"] + 1024) // max(len(sols), 1))
+        J, K = min(4094, J), min(500, K)
         p = self.pop
         if p is None or p.B_cap < len(sols) or p.J_cap < J or p.K_cap < K or p.F_cap < F:
             self.pop = None
@@ -146,17 +151,17 @@ class DeviceSearch:
     def run(self, sols, lams, perms, cfg: SearchConfig, kappa=0.5, lam_min=0.01, lam_max=1e4,
             deadline_s: float = -1.0):
         """Descents of all `sols` (not modified). Returns (routes, lams, stats)."""
-        scale = 1
-        while True:
-            pop = self._ensure(sols, scale)
+        need = None
+        for attempt in range(8):
+            pop = self._ensure(sols, need)
             pop.upload(sols, lams)
             try:
                 stats = pop.local_search(perms, cfg.depth, cfg.multi_move, kappa, lam_min, lam_max, deadline_s)
                 break
-            except CapacityError:
-                if scale >= 16:
+            except CapacityError as e:
+                need = getattr(e, "need", None) or dict(F=1, G=0, J=0, K=0)
+                if attempt == 7:
                     raise
-                scale *= 2
         routes, lam_out = pop.download()
         self.last_stats = stats
         return routes, lam_out, stats

@@ -194,3 +194,114 @@ def test_on_feasible_reports_best_feasible_state():
         assert len(seen) == 1 and seen[0][0] == st["best_feasible_D"]
     else:
         assert not seen
+
+
+@pytest.mark.parametrize("name,pop,depth", [("C1", 6, 500), ("C3", 3, 60), ("C5", 1, 8)])
+def test_appendix_a_configs_descents_vs_oracle(name, pop, depth):
+    """BASELINE.json shapes (MDVRP 50x4, MDOVRP 360x9, MDVRP 4000x20 theta 40): short
+    population descents bit-exact against the oracle, counts included."""
+    spec = W.CONFIGS[name]
+    inst, _ = W.appendix_a_instance(spec)
+    consts = P.ScalingConstants.from_instance(inst)
+    nbr = P.build_neighbors(inst, P.NeighborConfig(spec.theta), consts)
+    sols = [W.initial_solution(inst, consts, P.PenaltyState(), random.Random(100 + i)) for i in range(pop)]
+    cfg = P.SearchConfig(depth=depth, multi_move=True)
+    ops = P.enabled_operators(inst)
+    oi = O.OracleInstance(inst, consts, nbr)
+    work = [s.clone() for s in sols]
+    pens = [P.PenaltyState() for _ in sols]
+    stats = P.local_search_population(work, pens, cfg, nbr, consts, inst, [random.Random(i) for i in range(pop)])
+    for i, s in enumerate(sols):
+        perms = draw_permutations(random.Random(i), ops, cfg.depth + 1)
+        routes, lam, st, _ = O.local_search(oi, s, [1.0] * 4, cfg.depth, True, 0.5, 0.01, 1e4, perms)
+        assert G.routes_of(work[i]) == routes, f"{name} individual {i}"
+        assert pens[i].lam == lam
+        assert stats[i]["cands"] == st["cands"]
+
+
+def test_edge_cases_empty_routes_unrouted_and_single_move():
+    """Input with empty routes and an unrouted customer, single-move mode, depth 1 and 3."""
+    rng = random.Random(17)
+    for variant in ("mdvrp", "mdvrptw", "mdovrp"):
+        inst = W.make_instance(rng, variant, n_customers=25, n_depots=3, fleet=2,
+                               max_duration=None if variant == "mdovrp" else 400.0)
+        consts = P.ScalingConstants.from_instance(inst)
+        nbr = P.build_neighbors(inst, P.NeighborConfig(8), consts)
+        oi = O.OracleInstance(inst, consts, nbr)
+        for depth, mm in ((1, False), (3, True), (500, False)):
+            sol = W.random_solution(random.Random(depth), inst)
+            sol.routes.insert(1, P.Route(0, 0, []))
+            sol.routes.append(P.Route(1, 2 if variant != "mdovrp" else 1, []))
+            sol.routes[0].customers.pop()  # one unrouted customer
+            perms = draw_permutations(random.Random(5), P.enabled_operators(inst), depth + 1)
+            routes, lam, st, _ = O.local_search(oi, sol, [1.0] * 4, depth, mm, 0.5, 0.01, 1e4, perms)
+            work = sol.clone()
+            pen = P.PenaltyState()
+            P.local_search(work, pen, P.SearchConfig(depth, mm), nbr, consts, inst, random.Random(5))
+            assert G.routes_of(work) == routes, (variant, depth, mm)
+            assert pen.lam == lam
+
+
+def test_operator_level_api_on_random_states_vs_oracle():
+    """enumerate_candidates / evaluate_candidates / leader_and_followers through the
+    reference-shaped API on larger random states."""
+    rng = random.Random(99)
+    for variant in ("mdvrp", "mdvrptw", "mdovrp"):
+        inst = W.make_instance(rng, variant, n_customers=80, n_depots=4, fleet=5, max_duration=None)
+        consts = P.ScalingConstants.from_instance(inst)
+        nbr = P.build_neighbors(inst, P.NeighborConfig(15), consts)
+        sol = W.random_solution(random.Random(3), inst)
+        pen = P.PenaltyState(lam=[0.3, 2.0, 1.7, 0.9])
+        oi = O.OracleInstance(inst, consts, nbr)
+        cache = P.SolutionCache(sol, inst, consts)
+        for op in P.enabled_operators(inst):
+            cs = P.enumerate_candidates(sol, op, nbr, inst)
+            want = O.enumerate_op(oi, sol, int(op))
+            assert np.array_equal(_cm({f: getattr(cs, f) for f in G.FIELDS}), _cm(want))
+            d = P.evaluate_candidates(cache, cs, pen)
+            od = O.evaluate(oi, sol, int(op), want, pen.lam)
+            for f in G.DFIELDS + ("fleet_neutral",):
+                assert np.array_equal(getattr(d, f), od[f]), (variant, op, f)
+            leader, fol = P.leader_and_followers(cache, cs, d, True)
+            best, ofol = O.leader_followers(want, od, True)
+            assert (leader is None) == (best < 0)
+            if leader is not None:
+                assert leader.key()[1:] == tuple(_key(want, best))
+                assert [m.key()[1:] for m in fol] == [tuple(_key(want, i)) for i in ofol]
+        assert [x.hex() for x in cache.totals()] == [x.hex() for x in O.totals(oi, sol)]
+
+
+def test_many_routes_beyond_2046_capacity_path():
+    """Random C5-shaped start (~1300 short routes): population caps grow to 4094 routes,
+    the CTA-staging is disabled (too many routes for shared memory) and the warp-task
+    path runs; trajectory bit-exact vs the oracle."""
+    spec = W.CONFIGS["C5"]
+    inst, _ = W.appendix_a_instance(spec)
+    consts = P.ScalingConstants.from_instance(inst)
+    nbr = P.build_neighbors(inst, P.NeighborConfig(spec.theta), consts)
+    sol = W.random_solution(random.Random(301), inst)
+    assert len(sol.routes) > 1100
+    work = sol.clone()
+    pen = P.PenaltyState()
+    P.local_search(work, pen, P.SearchConfig(depth=3, multi_move=True), nbr, consts, inst, random.Random(0))
+    oi = O.OracleInstance(inst, consts, nbr)
+    perms = draw_permutations(random.Random(0), P.enabled_operators(inst), 4)
+    routes, lam, st, _ = O.local_search(oi, sol, [1.0] * 4, 3, True, 0.5, 0.01, 1e4, perms)
+    assert G.routes_of(work) == routes
+    assert pen.lam == lam
+
+
+def test_totals_pairwise_sum_many_routes():
+    """SolutionCache.totals() uses numpy's pairwise summation; check the device
+    restatement bit for bit on route lists far beyond one 128-element block."""
+    rng = random.Random(8)
+    for variant in ("mdvrptw", "mdvrp"):
+        inst = W.make_instance(rng, variant, n_customers=1500, n_depots=5, max_duration=300.0, capacity=15)
+        consts = P.ScalingConstants.from_instance(inst)
+        nbr = P.build_neighbors(inst, P.NeighborConfig(5), consts)
+        oi = O.OracleInstance(inst, consts, nbr)
+        for seed in range(3):
+            sol = W.random_solution(random.Random(seed), inst)
+            assert len(sol.routes) > 300
+            cache = P.SolutionCache(sol, inst, consts)
+            assert [x.hex() for x in cache.totals()] == [x.hex() for x in O.totals(oi, sol)]
