@@ -52,12 +52,14 @@ __device__ __forceinline__ At<WIN> rb_sf(const RB &x) { return ld_at<WIN>(x.sf, 
 template <bool WIN>
 __device__ __forceinline__ At<WIN> rb_pb(const RB &x) { return ld_at<WIN>(x.pb, x.dep, x.pb_last); }
 
-// (0 + cA) + cB, old terms, fleet delta, combine (batch.py:545-553) and record
-template <bool WIN>
+// (0 + cA) + cB, old terms, fleet delta, combine (batch.py:545-553) and record.
+// The 58-bit key is packed lazily: only when the candidate can displace the
+// lane's running leader (ord(dF) <= best) or is a follower.
+template <bool WIN, typename KeyF>
 __device__ __forceinline__ bool two_route_delta(const DevInst &I, const double cA[5], const double cB[5],
                                                 const double *rc1, const double *rc2, int clo1, int clo2,
                                                 double fleet_delta, int fn, const double lam[4], Acc &acc,
-                                                unsigned long long key, bool mm, int *nanflag,
+                                                KeyF mk, unsigned long long &key, bool mm, int *nanflag,
                                                 unsigned long long &o) {
   double nw[5];
 #pragma unroll
@@ -66,8 +68,20 @@ __device__ __forceinline__ bool two_route_delta(const DevInst &I, const double c
   Delta D;
   finish_delta(I, nw, old, fleet_delta, lam, D);
   D.fn = fn;
-  bool f = record(acc, D, key, mm, nanflag);
+  acc.n++;
+  if (D.dF != D.dF) {
+    atomicOr(nanflag, 1);
+    return false;
+  }
   o = ord_of(D.dF);
+  bool have = false;
+  if (o <= acc.o) {
+    key = mk();
+    have = true;
+    if (o < acc.o || key < acc.k) { acc.o = o; acc.k = key; }
+  }
+  const bool f = mm && follower_ok(D);
+  if (f && !have) key = mk();
   return f;
 }
 
@@ -104,7 +118,7 @@ __device__ void srelocate(const DevInst &I, const DevPop &P, const IV &v, const 
   const double fdec1 = I.nv_on ? __ldg(v.fl + X1.dep).y : 0.0;
   // one candidate: target (r2, tgt) with prefix P2 and (possibly empty) suffix S2
   auto eval_inter = [&](int len, int rev, int r2, int tgt, const At<WIN> &P2, const At<WIN> &S2,
-                        const RB &X2, unsigned long long &o, unsigned long long key) -> bool {
+                        const RB &X2, unsigned long long &o, unsigned long long &key) -> bool {
     At<WIN> seg = ld_at<WIN>(U + (len == 1 ? 10 : 16), rev ? (len == 1 ? u : nxt) : u, rev ? u : (len == 1 ? u : nxt));
     At<WIN> B = a_cat_l<WIN>(P2, seg, link_to_u(I, P2.last, seg.first));
     if (S2.first >= 0) B = a_cat_l<WIN>(B, S2, link_of(I, seg.last, S2.first));
@@ -114,7 +128,8 @@ __device__ void srelocate(const DevInst &I, const DevPop &P, const IV &v, const 
     int fn = 1;
     if (I.nv_on && k1 - len == 0) { fleet_delta = 0.0 + fdec1; fn = 0; }
     return two_route_delta<WIN>(I, U + 5 * (len - 1), cB, X1.rc, X2.rc, X1.clo, X2.clo, fleet_delta, fn, lam, acc,
-                                key, mm, P.nanflag + b, o);
+                                [&] { return key_of(ru, pu, r2, tgt, len, 0, rev, 0, -1, -1); }, key, mm,
+                                P.nanflag + b, o);
   };
   // granular targets: insert after v (p2 = pv + 1)
   const int W = I.W;
@@ -143,8 +158,7 @@ __device__ void srelocate(const DevInst &I, const DevPop &P, const IV &v, const 
       bool fol = false, gqf = false;
       unsigned long long o = 0, key = 0;
       if (ok) {
-        key = key_of(ru, pu, rv, tgt, len, 0, rev, 0, -1, -1);
-        if (same) gqf = true;
+        if (same) { gqf = true; key = key_of(ru, pu, rv, tgt, len, 0, rev, 0, -1, -1); }
         else fol = eval_inter(len, rev, rv, tgt, P2, S2, R[rv], o, key);
       }
       append_fol(P, b, fol, o, key);
@@ -180,8 +194,7 @@ __device__ void srelocate(const DevInst &I, const DevPop &P, const IV &v, const 
         bool fol = false, gqf = false;
         unsigned long long o = 0, key = 0;
         if (ok) {
-          key = key_of(ru, pu, rb, tgt, len, 0, rev, 0, -1, -1);
-          if (same) gqf = true;
+          if (same) { gqf = true; key = key_of(ru, pu, rb, tgt, len, 0, rev, 0, -1, -1); }
           else fol = eval_inter(len, rev, rb, tgt, P2, S2, R[rb], o, key);
         }
         append_fol(P, b, fol, o, key);
@@ -194,6 +207,9 @@ __device__ void srelocate(const DevInst &I, const DevPop &P, const IV &v, const 
 
 // ---------------------------------------------------------------------------
 // SWAP (moves.py:314-358, batch.py:430-463), warp task = customer u
+// A = (P1 + segB) + S1, B = (P2 + segA) + S2: X = P1 + segB depends only on v's
+// segment (lv, av) and Y = P2 + segA only on u's (lu, au), so each is built
+// once per lane and shared by the combos that use it.
 // ---------------------------------------------------------------------------
 template <bool WIN>
 __device__ void sswap(const DevInst &I, const DevPop &P, const IV &v, const RB *R, int b, int u, const double lam[4],
@@ -204,16 +220,22 @@ __device__ void sswap(const DevInst &I, const DevPop &P, const IV &v, const RB *
   const int ru = loc_r(lu), pu = loc_p(lu);
   const RB &X1 = R[ru];
   const int k1 = X1.k, n1 = X1.n;
-  const int nxtu = pu + 2 <= k1 ? __ldg(v.seq + ru * v.Kp + pu + 2) : u;
-  const int dep1 = X1.dep, lastP1 = __ldg(v.seq + ru * v.Kp + pu);
-  // U[0..5] seg u l=1, U[6..11] seg u l=2, U[12..17] prefix (0..pu)
+  const int *sq1 = v.seq + ru * v.Kp;
+  const int nxtu = pu + 2 <= k1 ? __ldg(sq1 + pu + 2) : u;
+  const int dep1 = X1.dep, lastP1 = __ldg(sq1 + pu), lastS1 = __ldg(sq1 + n1 - 1);
+  const int s1f1 = pu + 2 <= n1 - 1 ? __ldg(sq1 + pu + 2) : -1;  // S[ru][pu+2].first
+  const int s1f2 = pu + 3 <= n1 - 1 ? __ldg(sq1 + pu + 3) : -1;  // S[ru][pu+3].first
+  // U[0..5] seg u l=1, U[6..11] seg u l=2, U[12..17] prefix (0..pu), U[18..23] S[ru][pu+2], U[24..29] S[ru][pu+3]
   if (lane == 0) {
     At<WIN> s1 = a_node<WIN>(I, u);
     st_at<WIN>(U, s1);
     if (pu + 2 <= k1) st_at<WIN>(U + 6, a_cat_ne<WIN>(I, s1, a_node<WIN>(I, nxtu)));
     st_at<WIN>(U + 12, pre<WIN>(v, ru, pu));
+    if (s1f1 >= 0) st_at<WIN>(U + 18, suf<WIN>(v, ru, pu + 2, n1));
+    if (s1f2 >= 0) st_at<WIN>(U + 24, suf<WIN>(v, ru, pu + 3, n1));
   }
   __syncwarp();
+  constexpr int NV = WIN ? 2 : 3;  // segment variants (len, rev): (1,0), (2,0), (2,1)
   const int W = I.W;
   const int *lst = I.lists + (size_t)(u - I.ND) * W;
   for (int base = 0; base < W; base += 32) {
@@ -228,24 +250,37 @@ __device__ void sswap(const DevInst &I, const DevPop &P, const IV &v, const RB *
     const bool inter = rv >= 0 && !same;
     int k2 = 0, n2 = 0, nxtv = vv;
     At<WIN> P2;
+    At<WIN> Y[NV];
     if (inter) {
       k2 = R[rv].k;
       n2 = R[rv].n;
       P2 = pre<WIN>(v, rv, pv);
       if (pv + 2 <= k2) nxtv = __ldg(v.seq + rv * v.Kp + pv + 2);
-    }
-    for (int lv_ = 1; lv_ <= 2; lv_++) {
-      At<WIN> segB;
-      if (inter && pv + lv_ <= k2) {
-        segB = a_node<WIN>(I, vv);
-        if (lv_ == 2) segB = a_cat_ne<WIN>(I, segB, a_node<WIN>(I, nxtv));
+#pragma unroll
+      for (int yi = 0; yi < NV; yi++) {
+        const int lu_ = yi == 0 ? 1 : 2, au = yi == 2;
+        if (pu + lu_ <= k1) {
+          const int ua = lu_ == 1 ? u : nxtu;
+          At<WIN> sA = ld_at<WIN>(U + (lu_ == 1 ? 0 : 6), au ? ua : u, au ? u : ua);
+          Y[yi] = a_cat_l<WIN>(P2, sA, link_to_u(I, P2.last, sA.first));
+        }
       }
-      const int ncomb = I.win ? 2 : (lv_ == 1 ? 3 : 6);
-      for (int ci = 0; ci < ncomb; ci++) {
-        int lu_, au, av;
-        if (I.win) { lu_ = ci + 1; au = 0; av = 0; }
-        else if (lv_ == 1) { lu_ = ci == 0 ? 1 : 2; au = ci == 2; av = 0; }
-        else { lu_ = ci < 2 ? 1 : 2; av = ci & 1; au = ci >= 4; }
+    }
+#pragma unroll
+    for (int xi = 0; xi < NV; xi++) {
+      const int lv_ = xi == 0 ? 1 : 2, av = xi == 2;
+      const bool xok = inter && pv + lv_ <= k2;
+      At<WIN> X, S2;
+      if (xok) {
+        At<WIN> sB = a_node<WIN>(I, vv);
+        if (lv_ == 2) sB = a_cat_ne<WIN>(I, sB, a_node<WIN>(I, nxtv));
+        if (av) swap_ends(sB);
+        X = a_cat_l<WIN>(ld_at<WIN>(U + 12, dep1, lastP1), sB, link_of(I, lastP1, sB.first));
+        S2 = suf<WIN>(v, rv, pv + lv_ + 1, n2);
+      }
+#pragma unroll
+      for (int yi = 0; yi < NV; yi++) {
+        const int lu_ = yi == 0 ? 1 : 2, au = yi == 2;
         bool fol = false, gqf = false;
         unsigned long long o = 0, key = 0;
         if (rv >= 0) {
@@ -259,27 +294,18 @@ __device__ void sswap(const DevInst &I, const DevPop &P, const IV &v, const RB *
             c.depot = -1; c.mode = -1;
             gqf = (c.p1 + c.l1 <= k1) && (c.p2 + c.l2 <= k1) && (c.p2 >= c.p1 + c.l1);
             key = pack_key(c);
-          } else if (pu + lu_ <= k1 && pv + lv_ <= k2) {
-            const int ua = lu_ == 1 ? u : nxtu;
-            At<WIN> sA = ld_at<WIN>(U + (lu_ == 1 ? 0 : 6), au ? ua : u, au ? u : ua);
-            At<WIN> sB = segB;
-            if (av) swap_ends(sB);
-            At<WIN> A = a_cat_l<WIN>(ld_at<WIN>(U + 12, dep1, lastP1), sB, link_of(I, lastP1, sB.first));
-            if (pu + lu_ + 1 <= n1 - 1) {
-              At<WIN> S1 = suf<WIN>(v, ru, pu + lu_ + 1, n1);
-              A = a_cat_l<WIN>(A, S1, link_to_u(I, sB.last, S1.first));
-            }
+          } else if (xok && pu + lu_ <= k1) {
+            const int sf = lu_ == 1 ? s1f1 : s1f2;
+            At<WIN> A = X;
+            if (sf >= 0) A = a_cat_l<WIN>(X, ld_at<WIN>(U + (lu_ == 1 ? 18 : 24), sf, lastS1), link_to_u(I, X.last, sf));
+            At<WIN> B = Y[yi];
+            if (S2.first >= 0) B = a_cat_l<WIN>(B, S2, link_of(I, B.last, S2.first));
             double cA[5], cB[5];
             contrib_fast<WIN>(I, A, X1.dep, X1.arr, k1 - lu_ + lv_, cA);
-            At<WIN> B = a_cat_l<WIN>(P2, sA, link_to_u(I, P2.last, sA.first));
-            if (pv + lv_ + 1 <= n2 - 1) {
-              At<WIN> S2 = suf<WIN>(v, rv, pv + lv_ + 1, n2);
-              B = a_cat_l<WIN>(B, S2, link_of(I, sA.last, S2.first));
-            }
             const RB &X2 = R[rv];
             contrib_fast<WIN>(I, B, X2.dep, X2.arr, k2 - lv_ + lu_, cB);
-            key = key_of(ru, pu, rv, pv, lu_, lv_, au, av, -1, -1);
-            fol = two_route_delta<WIN>(I, cA, cB, X1.rc, X2.rc, X1.clo, X2.clo, 0.0, 1, lam, acc, key, mm,
+            fol = two_route_delta<WIN>(I, cA, cB, X1.rc, X2.rc, X1.clo, X2.clo, 0.0, 1, lam, acc,
+                                       [&] { return key_of(ru, pu, rv, pv, lu_, lv_, au, av, -1, -1); }, key, mm,
                                        P.nanflag + b, o);
           }
         }
@@ -318,9 +344,8 @@ __device__ __forceinline__ bool tos_eval(const DevInst &I, const DevPop &P, cons
     fleet_delta = (0.0 + (kA == 0 ? __ldg(v.fl + X1.dep).y : 0.0)) + (kB == 0 ? __ldg(v.fl + X2.dep).y : 0.0);
     fn = (kA > 0) && (kB > 0);
   }
-  key = key_of(r1, p1, r2, p2, 0, 0, 0, 0, -1, -1);
-  return two_route_delta<WIN>(I, cA, cB, X1.rc, X2.rc, X1.clo, X2.clo, fleet_delta, fn, lam, acc, key, mm,
-                              P.nanflag + b, o);
+  return two_route_delta<WIN>(I, cA, cB, X1.rc, X2.rc, X1.clo, X2.clo, fleet_delta, fn, lam, acc,
+                              [&] { return key_of(r1, p1, r2, p2, 0, 0, 0, 0, -1, -1); }, key, mm, P.nanflag + b, o);
 }
 
 // warp task = customer u: granular cut and the two boundary families

@@ -1,5 +1,5 @@
 # GPU parity suite + one C4 bench step (dev loop); extra args: env assignments for an A/B run
-timeout 900 python -m pytest tests -q -m gpu -x 2>&1 | tail -2
+timeout 900 python -m pytest tests -q -m gpu -x 2>&1 | tail -1 | cut -c1-80
 run() {
 timeout 600 env "$@" python bench.py --config C4 --steps 1 --warmup 1 --no-cpu-baseline --no-e2e 2>&1 | python -c "
 import sys,json
