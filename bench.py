@@ -143,14 +143,14 @@ def run_reference(args, rank, world):
     ops = enabled_operators(inst)
     perms = [draw_permutations(random.Random(i), ops, args.depth + 1) for i in range(len(sols))]
 
-    def step():
+    def step(depth=args.depth):
         t0 = time.perf_counter()
-        st = O.local_search_many(oi, sols, [[1.0] * 4] * len(sols), args.depth, True, 0.5, 0.01, 1e4, perms,
+        st = O.local_search_many(oi, sols, [[1.0] * 4] * len(sols), depth, True, 0.5, 0.01, 1e4, perms,
                                  threads)
         return time.perf_counter() - t0, sum(sum(s["cands"]) for s in st)
 
     for _ in range(args.warmup):
-        step()
+        step(depth=10)  # untimed warm-up (page-in, thread start-up); kept short on the CPU
     tt, cc = 0.0, 0
     for _ in range(args.steps):
         dt, c = step()
