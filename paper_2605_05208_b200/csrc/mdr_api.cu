@@ -195,6 +195,7 @@ int mdr_pop_create(mdr_instance *inst, int32_t Bcap, int32_t J, int32_t K, int32
   DA(A, P.rcon, rows);
   DA(A, P.tabP, slots * P.FE);
   DA(A, P.tabS, slots * P.FE);
+  DA(A, P.tabT, slots * P.Kp * P.FE);
   DA(A, P.fleet, (size_t)Bcap * I.ND);
   DA(A, P.fexcess, Bcap);
   DA(A, P.lam, (size_t)Bcap * 4);

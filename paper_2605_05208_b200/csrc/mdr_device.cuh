@@ -56,6 +56,7 @@ struct DevPop {
   int *loc;
   double4 *rcon;
   double *tabP, *tabS;
+  double *tabT;  // [B][J][Kp][Kp][FE] full subsequence table (i..j), left fold from i
   double2 *fleet;
   double *fexcess;
   double *lam;
@@ -246,10 +247,22 @@ __device__ __forceinline__ void tab_store(const DevPop &P, double *tab, int b, i
   }
 }
 
+template <bool WIN>
+__device__ __forceinline__ void tab_store_at(double *p, const At<WIN> &a) {
+  double2 *e = reinterpret_cast<double2 *>(p);
+  e[0] = make_double2(a.dist, a.load);
+  if (WIN) {
+    e[1] = make_double2(a.T, a.E);
+    e[2] = make_double2(a.L, a.TW);
+  } else {
+    e[1] = make_double2(a.T, 0.0);
+  }
+}
+
 // attributes of sequence positions i..j of route r (SolutionCache.gather,
 // batch.py:184-221); j < i is the empty sequence.  The source is the prefix
-// table (i == 0), the suffix table (j == n-1) or an on-the-fly left fold --
-// all three are the same left fold from i, bit for bit.
+// table (i == 0), the suffix table (j == n-1) or the full table T[r][i][j] --
+// all three hold the same left fold from i, bit for bit.
 template <bool WIN>
 __device__ __forceinline__ At<WIN> gat(const DevInst &I, const DevPop &P, int b, int r, int i, int j, int n) {
   if (j < i) return a_empty<WIN>();
@@ -265,8 +278,18 @@ __device__ __forceinline__ At<WIN> gat(const DevInst &I, const DevPop &P, int b,
     a.first = __ldg(sq + i); a.last = __ldg(sq + j);
     return a;
   }
-  a = a_node<WIN>(I, __ldg(sq + i));
-  for (int t = i + 1; t <= j; t++) a = a_cat<WIN>(I, a, a_node<WIN>(I, __ldg(sq + t)));
+  {
+    const double2 *e = reinterpret_cast<const double2 *>(P.tabT + ((row_base(P, b, r) + i) * P.Kp + j) * P.FE);
+    double2 x = __ldg(e), y = __ldg(e + 1);
+    a.dist = x.x; a.load = x.y; a.T = y.x;
+    if (WIN) {
+      double2 z = __ldg(e + 2);
+      a.E = y.y; a.L = z.x; a.TW = z.y;
+    } else {
+      a.E = 0.0; a.L = 0.0; a.TW = 0.0;
+    }
+  }
+  a.first = __ldg(sq + i); a.last = __ldg(sq + j);
   return a;
 }
 

@@ -129,10 +129,13 @@ __device__ void rebuild_routes(const DevInst &I, const DevPop &P, int b, const i
     for (int p = lane; p < k; p += 32) LOC[sq[p + 1]] = (r << 9) | p;
     for (int i = lane; i < n; i += 32) {
       At<WIN> acc = a_node<WIN>(I, sq[i]);
+      double *trow = P.tabT + (row_base(P, b, r) + i) * P.Kp * P.FE;  // T[r][i][*]
       if (i == 0) tab_store<WIN>(P, P.tabP, b, r, 0, acc);
+      tab_store_at<WIN>(trow + i * P.FE, acc);
       for (int j = i + 1; j < n; j++) {
         acc = a_cat_ne<WIN>(I, acc, a_node<WIN>(I, sq[j]));
         if (i == 0) tab_store<WIN>(P, P.tabP, b, r, j, acc);
+        tab_store_at<WIN>(trow + j * P.FE, acc);
       }
       tab_store<WIN>(P, P.tabS, b, r, i, acc);
       if (i == 0) {
