@@ -344,10 +344,10 @@ __global__ void __launch_bounds__(256, MDR_EVAL_MINB) k_eval(DevInst I, DevPop P
 
 // CTA-task evaluators (relocate, swap, 2-opt*) with staged route boundaries
 template <bool WIN, int OP>
-__global__ void __launch_bounds__(256, MDR_EVAL_MINB) k_eval_c(DevInst I, DevPop P, LsParams L) {
+__global__ void __launch_bounds__(32 * MDR_CU, MDR_CMINB) k_eval_c(DevInst I, DevPop P, LsParams L) {
   extern __shared__ __align__(16) unsigned char smx_c[];
   RB *R = reinterpret_cast<RB *>(smx_c);
-  __shared__ double s_u[8][MDR_USLOT];
+  __shared__ double s_u[MDR_CU][MDR_USLOT];
   __shared__ int s_t, s_b, s_lo;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   double *U = s_u[wid];
@@ -977,16 +977,16 @@ static void launch_eval_t(const DevInst &I, const DevPop &P, const LsParams &L, 
       cudaGetDevice(&dev);
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
       int per = 1;
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_eval_c<WIN, 0>, 256, sm);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_eval_c<WIN, 0>, 32 * MDR_CU, sm);
       gc[0] = sms * (per < 1 ? 1 : per);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_eval_c<WIN, 1>, 256, sm);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_eval_c<WIN, 1>, 32 * MDR_CU, sm);
       gc[1] = sms * (per < 1 ? 1 : per);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_eval_c<WIN, 2>, 256, sm);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_eval_c<WIN, 2>, 32 * MDR_CU, sm);
       gc[2] = sms * (per < 1 ? 1 : per);
     }
-    k_eval_c<WIN, 0><<<gc[0], 256, sm, s>>>(I, P, L);
-    k_eval_c<WIN, 1><<<gc[1], 256, sm, s>>>(I, P, L);
-    k_eval_c<WIN, 2><<<gc[2], 256, sm, s>>>(I, P, L);
+    k_eval_c<WIN, 0><<<gc[0], 32 * MDR_CU, sm, s>>>(I, P, L);
+    k_eval_c<WIN, 1><<<gc[1], 32 * MDR_CU, sm, s>>>(I, P, L);
+    k_eval_c<WIN, 2><<<gc[2], 32 * MDR_CU, sm, s>>>(I, P, L);
   } else {
     k_eval<WIN, 0><<<g[0], 256, 0, s>>>(I, P, L);
     k_eval<WIN, 1><<<g[1], 256, 0, s>>>(I, P, L);

@@ -453,7 +453,12 @@ __device__ void stos_r(const DevInst &I, const DevPop &P, const IV &v, const RB 
   }
 }
 
-#define MDR_CU 8  // customers (warps) per CTA task
+#ifndef MDR_CU
+#define MDR_CU 8  // customers (warps) per CTA task = warps per CTA of k_eval_c
+#endif
+#ifndef MDR_CMINB
+#define MDR_CMINB 2
+#endif
 
 __host__ __device__ __forceinline__ int op_tasks_c(int op, int M, int NC) {
   int nch = (NC + MDR_CU - 1) / MDR_CU;
