@@ -59,6 +59,8 @@ struct mdr_pop {
   mdr_timing tm;
   cudaEvent_t ev[8];
   std::vector<cudaEvent_t> rev;  // per-round events when profiling (4 per round)
+  cudaStream_t ls;               // private stream of the round loop (graph capture)
+  cudaEvent_t join[2];
 };
 
 template <typename T>
@@ -249,6 +251,9 @@ int mdr_pop_create(mdr_instance *inst, int32_t Bcap, int32_t J, int32_t K, int32
   p->grid = eval_grid_size(I.win);
   p->profiling = 0;
   for (int i = 0; i < 8; i++) CK(cudaEventCreate(&p->ev[i]));
+  CK(cudaStreamCreateWithFlags(&p->ls, cudaStreamNonBlocking));
+  CK(cudaEventCreateWithFlags(&p->join[0], cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&p->join[1], cudaEventDisableTiming));
   *out = p;
   return MDR_OK;
 }
@@ -262,6 +267,9 @@ void mdr_pop_destroy(mdr_pop *p) {
   if (p->h_hdr) cudaFreeHost(p->h_hdr);
   for (int i = 0; i < 8; i++) cudaEventDestroy(p->ev[i]);
   for (cudaEvent_t e : p->rev) cudaEventDestroy(e);
+  cudaStreamDestroy(p->ls);
+  cudaEventDestroy(p->join[0]);
+  cudaEventDestroy(p->join[1]);
   delete p;
 }
 
@@ -798,7 +806,33 @@ int mdr_local_search(mdr_pop *p, const mdr_ls_cfg *cfg, mdr_ls_stats *stats, voi
     }
     return p->rev[i];
   };
+  // the round loop runs on a private stream joined to the caller's; after a
+  // first eager batch, each batch of rps rounds is one CUDA graph launch
+  const bool graph = !prof && !dbg && !getenv("MDR_NO_GRAPH");
+  cudaGraphExec_t gexec = nullptr;
+  cudaStream_t cs = s;
+  s = p->ls;
+  CK(cudaEventRecord(p->join[0], cs));
+  CK(cudaStreamWaitEvent(s, p->join[0], 0));
+  long long batches = 0;
   while (B > 0) {
+    if (graph && batches > 0) {
+      if (!gexec) {
+        cudaGraph_t gr;
+        CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+        for (int r = 0; r < rps; r++) {
+          launch_plan(I, P, L, s);
+          launch_eval(I, P, L, p->grid, I.win, s);
+          launch_eval_g(I, P, L, p->grid, I.win, s);
+          launch_select(I, P, L, I.win, s);
+        }
+        CK(cudaStreamEndCapture(s, &gr));
+        CK(cudaGraphInstantiate(&gexec, gr, 0));
+        cudaGraphDestroy(gr);
+      }
+      CK(cudaGraphLaunch(gexec, s));
+      rounds += rps;
+    } else
     for (int r = 0; r < rps; r++) {
       if (prof) cudaEventRecord(ev_at(ev_used), s);
       launch_plan(I, P, L, s);
@@ -818,6 +852,7 @@ int mdr_local_search(mdr_pop *p, const mdr_ls_cfg *cfg, mdr_ls_stats *stats, voi
       }
       rounds++;
     }
+    batches++;
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(p->h_hdr, P.active, sizeof(int), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
@@ -827,6 +862,9 @@ int mdr_local_search(mdr_pop *p, const mdr_ls_cfg *cfg, mdr_ls_stats *stats, voi
       if (el > cfg->deadline_s) break;
     }
   }
+  if (gexec) cudaGraphExecDestroy(gexec);
+  CK(cudaEventRecord(p->join[1], s));
+  CK(cudaStreamWaitEvent(cs, p->join[1], 0));
   if (prof) {
     CK(cudaEventRecord(p->ev[7], s));
     CK(cudaEventSynchronize(p->ev[7]));

@@ -1010,11 +1010,18 @@ void launch_eval_g(const DevInst &I, const DevPop &P, const LsParams &L, int gri
 
 void launch_select(const DevInst &I, const DevPop &P, const LsParams &L, bool win, cudaStream_t s) {
   size_t sm = select_smem(P);
+  static size_t set_t = 0, set_f = 0;  // attribute set once per size (not during graph capture)
   if (win) {
-    if (sm > 48 * 1024) cudaFuncSetAttribute(k_select<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (sm > 48 * 1024 && sm > set_t) {
+      cudaFuncSetAttribute(k_select<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      set_t = sm;
+    }
     k_select<true><<<L.B, 256, sm, s>>>(I, P, L);
   } else {
-    if (sm > 48 * 1024) cudaFuncSetAttribute(k_select<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (sm > 48 * 1024 && sm > set_f) {
+      cudaFuncSetAttribute(k_select<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      set_f = sm;
+    }
     k_select<false><<<L.B, 256, sm, s>>>(I, P, L);
   }
 }
