@@ -61,6 +61,8 @@ struct mdr_pop {
   std::vector<cudaEvent_t> rev;  // per-round events when profiling (4 per round)
   cudaStream_t ls;               // private stream of the round loop (graph capture)
   cudaEvent_t join[2];
+  cudaStream_t side[3];          // fork/join branches of the per-operator evaluators
+  cudaEvent_t fev[4];
 };
 
 template <typename T>
@@ -254,6 +256,8 @@ int mdr_pop_create(mdr_instance *inst, int32_t Bcap, int32_t J, int32_t K, int32
   CK(cudaStreamCreateWithFlags(&p->ls, cudaStreamNonBlocking));
   CK(cudaEventCreateWithFlags(&p->join[0], cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&p->join[1], cudaEventDisableTiming));
+  for (int q = 0; q < 3; q++) CK(cudaStreamCreateWithFlags(&p->side[q], cudaStreamNonBlocking));
+  for (int q = 0; q < 4; q++) CK(cudaEventCreateWithFlags(&p->fev[q], cudaEventDisableTiming));
   *out = p;
   return MDR_OK;
 }
@@ -270,6 +274,8 @@ void mdr_pop_destroy(mdr_pop *p) {
   cudaStreamDestroy(p->ls);
   cudaEventDestroy(p->join[0]);
   cudaEventDestroy(p->join[1]);
+  for (int q = 0; q < 3; q++) cudaStreamDestroy(p->side[q]);
+  for (int q = 0; q < 4; q++) cudaEventDestroy(p->fev[q]);
   delete p;
 }
 
@@ -822,7 +828,7 @@ int mdr_local_search(mdr_pop *p, const mdr_ls_cfg *cfg, mdr_ls_stats *stats, voi
         CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
         for (int r = 0; r < rps; r++) {
           launch_plan(I, P, L, s);
-          launch_eval(I, P, L, p->grid, I.win, s);
+          launch_eval(I, P, L, p->grid, I.win, s, p->side, p->fev);
           launch_eval_g(I, P, L, p->grid, I.win, s);
           launch_select(I, P, L, I.win, s);
         }
@@ -838,7 +844,7 @@ int mdr_local_search(mdr_pop *p, const mdr_ls_cfg *cfg, mdr_ls_stats *stats, voi
       launch_plan(I, P, L, s);
       if (dbg && cudaStreamSynchronize(s)) return fail(MDR_ERR_CUDA, "k_plan failed");
       if (prof) cudaEventRecord(ev_at(ev_used + 1), s);
-      launch_eval(I, P, L, p->grid, I.win, s);
+      launch_eval(I, P, L, p->grid, I.win, s, p->side, p->fev);
       if (dbg && cudaStreamSynchronize(s)) return fail(MDR_ERR_CUDA, "k_eval failed");
       if (prof) cudaEventRecord(ev_at(ev_used + 2), s);
       launch_eval_g(I, P, L, p->grid, I.win, s);

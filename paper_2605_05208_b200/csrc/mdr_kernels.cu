@@ -225,8 +225,13 @@ __device__ __forceinline__ int block_excl_scan(int x, int *wsum, int &total) {
 }
 
 __global__ void __launch_bounds__(1024) k_plan(DevInst I, DevPop P, LsParams L) {
-  __shared__ int wsum[32];
-  // pass 1: operator and task count of every active individual
+  // one pass: operator and task count of every active individual, appended to
+  // its operator's list with one packed 64-bit shared atomic {index:24 | first task:40}
+  // (list order is irrelevant: every result is reduced order-independently)
+  __shared__ unsigned long long acc6[6];
+  if (threadIdx.x < 6) acc6[threadIdx.x] = 0ull;
+  __syncthreads();
+  const unsigned long long MASK = (1ull << 40) - 1;
   for (int b = threadIdx.x; b < L.B; b += blockDim.x) {
     LsState st = P.st[b];
     P.fcount[b] = 0;
@@ -238,38 +243,29 @@ __global__ void __launch_bounds__(1024) k_plan(DevInst I, DevPop P, LsParams L) 
       P.st[b] = st;
     }
     if (!st.done) {
-      int op = P.perms[((size_t)b * P.maxp + st.pass) * P.nops + st.pos];
+      const int op = P.perms[((size_t)b * P.maxp + st.pass) * P.nops + st.pos];
+      const int t = (P.staged && op <= 2) ? op_tasks_c(op, P.m[b], I.NC) : op_tasks(op, P.m[b], I.NC, I.win);
       P.op_cur[b] = op;
-      P.wsize[b] = (P.staged && op <= 2) ? op_tasks_c(op, P.m[b], I.NC) : op_tasks(op, P.m[b], I.NC, I.win);
+      P.wsize[b] = t;
+      if (t > 0) {
+        unsigned long long old = atomicAdd(&acc6[op], (1ull << 40) | (unsigned long long)t);
+        const int idx = (int)(old >> 40);
+        P.opb[op * P.Bcap + idx] = b;
+        P.opoff[op * (P.Bcap + 1) + idx] = (int)(old & MASK);
+      }
     } else {
       P.op_cur[b] = -1;
       P.wsize[b] = 0;
     }
   }
   __syncthreads();
-  // pass 2: per operator, compact list of individuals and their task offsets
-  for (int op = 0; op < 6; op++) {
-    int carry = 0, cnt = 0;
-    for (int base = 0; base < L.B; base += blockDim.x) {
-      int b = base + threadIdx.x;
-      int t = (b < L.B && P.op_cur[b] == op) ? P.wsize[b] : 0;
-      int f = t > 0;
-      int tt, ft;
-      int off = block_excl_scan(t, wsum, tt);
-      int idx = block_excl_scan(f, wsum, ft);
-      if (f) {
-        P.opb[op * P.Bcap + cnt + idx] = b;
-        P.opoff[op * (P.Bcap + 1) + cnt + idx] = carry + off;
-      }
-      carry += tt;
-      cnt += ft;
-    }
-    if (threadIdx.x == 0) {
-      P.opoff[op * (P.Bcap + 1) + cnt] = carry;
-      P.opcnt[op] = cnt;
-      P.optasks[op] = carry;
-      P.task_next[op] = 0;
-    }
+  if (threadIdx.x < 6) {
+    const int op = threadIdx.x;
+    const int cnt = (int)(acc6[op] >> 40), tot = (int)(acc6[op] & MASK);
+    P.opoff[op * (P.Bcap + 1) + cnt] = tot;
+    P.opcnt[op] = cnt;
+    P.optasks[op] = tot;
+    P.task_next[op] = 0;
   }
   if (threadIdx.x == 0) {
     *P.active = 0;
@@ -955,7 +951,8 @@ static int grid_for(K kern) {
 int eval_grid_size(bool win) { return win ? grid_for(k_eval<true, 0>) : grid_for(k_eval<false, 0>); }
 
 template <bool WIN>
-static void launch_eval_t(const DevInst &I, const DevPop &P, const LsParams &L, cudaStream_t s) {
+static void launch_eval_t(const DevInst &I, const DevPop &P, const LsParams &L, cudaStream_t s, const cudaStream_t *side,
+                          cudaEvent_t *ev) {
   static int g[6] = {0, 0, 0, 0, 0, 0};
   if (!g[0]) {
     g[0] = grid_for(k_eval<WIN, 0>); g[1] = grid_for(k_eval<WIN, 1>); g[2] = grid_for(k_eval<WIN, 2>);
@@ -984,9 +981,17 @@ static void launch_eval_t(const DevInst &I, const DevPop &P, const LsParams &L, 
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_eval_c<WIN, 2>, 32 * MDR_CU, sm);
       gc[2] = sms * (per < 1 ? 1 : per);
     }
-    k_eval_c<WIN, 0><<<gc[0], 32 * MDR_CU, sm, s>>>(I, P, L);
-    k_eval_c<WIN, 1><<<gc[1], 32 * MDR_CU, sm, s>>>(I, P, L);
-    k_eval_c<WIN, 2><<<gc[2], 32 * MDR_CU, sm, s>>>(I, P, L);
+    // relocate / swap / 2-opt* as parallel branches (fork/join): their
+    // persistent grids back-fill each other's tails
+    cudaEventRecord(ev[0], s);
+    for (int q = 0; q < 3; q++) cudaStreamWaitEvent(side[q], ev[0], 0);
+    k_eval_c<WIN, 0><<<gc[0], 32 * MDR_CU, sm, side[0]>>>(I, P, L);
+    k_eval_c<WIN, 1><<<gc[1], 32 * MDR_CU, sm, side[1]>>>(I, P, L);
+    k_eval_c<WIN, 2><<<gc[2], 32 * MDR_CU, sm, side[2]>>>(I, P, L);
+    for (int q = 0; q < 3; q++) {
+      cudaEventRecord(ev[1 + q], side[q]);
+      cudaStreamWaitEvent(s, ev[1 + q], 0);
+    }
   } else {
     k_eval<WIN, 0><<<g[0], 256, 0, s>>>(I, P, L);
     k_eval<WIN, 1><<<g[1], 256, 0, s>>>(I, P, L);
@@ -997,10 +1002,11 @@ static void launch_eval_t(const DevInst &I, const DevPop &P, const LsParams &L, 
   k_eval<WIN, 5><<<g[5], 256, 0, s>>>(I, P, L);
 }
 
-void launch_eval(const DevInst &I, const DevPop &P, const LsParams &L, int grid, bool win, cudaStream_t s) {
+void launch_eval(const DevInst &I, const DevPop &P, const LsParams &L, int grid, bool win, cudaStream_t s,
+                 const cudaStream_t *side, cudaEvent_t *ev) {
   (void)grid;
-  if (win) launch_eval_t<true>(I, P, L, s);
-  else launch_eval_t<false>(I, P, L, s);
+  if (win) launch_eval_t<true>(I, P, L, s, side, ev);
+  else launch_eval_t<false>(I, P, L, s, side, ev);
 }
 
 void launch_eval_g(const DevInst &I, const DevPop &P, const LsParams &L, int grid, bool win, cudaStream_t s) {

@@ -17,7 +17,8 @@ struct MatDeltas {
 
 void launch_rebuild(const DevInst &I, const DevPop &P, int B, bool win, cudaStream_t s);
 void launch_plan(const DevInst &I, const DevPop &P, const LsParams &L, cudaStream_t s);
-void launch_eval(const DevInst &I, const DevPop &P, const LsParams &L, int grid, bool win, cudaStream_t s);
+void launch_eval(const DevInst &I, const DevPop &P, const LsParams &L, int grid, bool win, cudaStream_t s,
+                 const cudaStream_t *side, cudaEvent_t *ev);
 void launch_eval_g(const DevInst &I, const DevPop &P, const LsParams &L, int grid, bool win, cudaStream_t s);
 void launch_select(const DevInst &I, const DevPop &P, const LsParams &L, bool win, cudaStream_t s);
 void launch_eval_mat(const DevInst &I, const DevPop &P, int b, int op, const MatCands &c, const double *lam,
