@@ -12,6 +12,7 @@
 //                  follower selection, apply, drop empties, rebuild, totals,
 //                  penalty adaptation, state machine (localsearch.py:97-140)
 #include <cstdio>
+#include <cstdlib>
 
 #include "mdr_fused.cuh"
 #include "mdr_staged.cuh"
@@ -966,6 +967,17 @@ static void launch_eval_t(const DevInst &I, const DevPop &P, const LsParams &L, 
       cudaFuncSetAttribute(k_eval_c<WIN, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
       cudaFuncSetAttribute(k_eval_c<WIN, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
       cudaFuncSetAttribute(k_eval_c<WIN, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      {
+        // shared-memory carveout just large enough for MDR_CMINB resident CTAs: the
+        // rest of the 228 KB stays L1 for the gathers (+2 % on C4 vs the default)
+        int pct = (int)((MDR_CMINB * (sm + 3 * 1024) * 100 + 228 * 1024 - 1) / (228 * 1024));
+        if (getenv("MDR_CARVEOUT")) pct = atoi(getenv("MDR_CARVEOUT"));
+        if (pct > 100) pct = 100;
+        cudaFuncSetAttribute(k_eval_c<WIN, 0>, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+        cudaFuncSetAttribute(k_eval_c<WIN, 1>, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+        cudaFuncSetAttribute(k_eval_c<WIN, 2>, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+        cudaFuncSetAttribute(k_eval_g<WIN>, cudaFuncAttributePreferredSharedMemoryCarveout, 0);
+      }
       sm_set = sm;
       gc[0] = 0;
     }
