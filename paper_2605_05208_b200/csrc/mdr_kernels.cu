@@ -339,13 +339,16 @@ __global__ void __launch_bounds__(256, MDR_EVAL_MINB) k_eval(DevInst I, DevPop P
   }
 }
 
+#ifndef MDR_TGC
+#define MDR_TGC 1
+#endif
 // CTA-task evaluators (relocate, swap, 2-opt*) with staged route boundaries
 template <bool WIN, int OP>
 __global__ void __launch_bounds__(32 * MDR_CU, MDR_CMINB) k_eval_c(DevInst I, DevPop P, LsParams L) {
   extern __shared__ __align__(16) unsigned char smx_c[];
   RB *R = reinterpret_cast<RB *>(smx_c);
   __shared__ double s_u[MDR_CU][MDR_USLOT];
-  __shared__ int s_t, s_b, s_lo;
+  __shared__ int s_t, s_b, s_lo, s_hi, s_next, s_end;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   double *U = s_u[wid];
   const int total = P.optasks[OP];
@@ -355,11 +358,19 @@ __global__ void __launch_bounds__(32 * MDR_CU, MDR_CMINB) k_eval_c(DevInst I, De
   const bool mm = L.multi_move != 0;
   const int nch = (I.NC + MDR_CU - 1) / MDR_CU;
   int staged = -1;
+  if (threadIdx.x == 0) { s_next = 0; s_end = 0; s_lo = 0; s_hi = 0; }
   for (;;) {
     if (threadIdx.x == 0) {
-      int t = atomicAdd(P.task_next + OP, 1);
+      // grab MDR_TGC consecutive tasks at a time: consecutive tasks belong to
+      // the same individual, so its tables stay hot in this SM's L1
+      if (s_next >= s_end) {
+        int t0 = atomicAdd(P.task_next + OP, MDR_TGC);
+        s_next = t0;
+        s_end = min(t0 + MDR_TGC, total);
+      }
+      int t = s_next < s_end ? s_next++ : total;
       s_t = t;
-      if (t < total) {
+      if (t < total && (t < s_lo || t >= s_hi)) {
         int l2 = 0, h2 = cnt - 1;
         while (l2 < h2) {
           int mid = (l2 + h2 + 1) >> 1;
@@ -367,6 +378,7 @@ __global__ void __launch_bounds__(32 * MDR_CU, MDR_CMINB) k_eval_c(DevInst I, De
         }
         s_b = OB[l2];
         s_lo = OFF[l2];
+        s_hi = OFF[l2 + 1];
       }
     }
     __syncthreads();
