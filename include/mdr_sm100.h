@@ -82,7 +82,8 @@ typedef struct mdr_ls_cfg {
   const uint8_t *perms;            /* [B][max_passes][n_ops]: rng.shuffle results, host */
   double deadline_s;               /* <0: none; else seconds from the call (checked between rounds) */
   int32_t rounds_per_sync;         /* device rounds per host poll (0 = default) */
-  int32_t use_graph;               /* capture the rounds in a CUDA graph */
+  int32_t use_graph;               /* reserved (graphs are used unless MDR_NO_GRAPH is set) */
+  int32_t snapshot_best;           /* keep the best feasible state for mdr_pop_download_best */
 } mdr_ls_cfg;
 
 typedef struct mdr_ls_stats {

@@ -50,7 +50,7 @@ class LsCfg(C.Structure):
     _fields_ = [("depth", C.c_int32), ("multi_move", C.c_int32), ("kappa", C.c_double),
                 ("lam_min", C.c_double), ("lam_max", C.c_double), ("max_passes", C.c_int32),
                 ("n_ops", C.c_int32), ("perms", u8p), ("deadline_s", C.c_double),
-                ("rounds_per_sync", C.c_int32), ("use_graph", C.c_int32)]
+                ("rounds_per_sync", C.c_int32), ("use_graph", C.c_int32), ("snapshot_best", C.c_int32)]
 
 
 class LsStats(C.Structure):

@@ -797,6 +797,7 @@ int mdr_local_search(mdr_pop *p, const mdr_ls_cfg *cfg, mdr_ls_stats *stats, voi
   L.lam_min = cfg->lam_min;
   L.lam_max = cfg->lam_max;
   L.B = B;
+  L.snapshot = cfg->snapshot_best ? 1 : 0;
   const int rps = cfg->rounds_per_sync > 0 ? cfg->rounds_per_sync : 8;
   auto t0 = std::chrono::steady_clock::now();
   int prof = p->profiling;

@@ -97,6 +97,7 @@ struct LsParams {
   int depth, multi_move;
   double kappa, lam_min, lam_max;
   int B;
+  int snapshot;  // keep the best-feasible snapshot (for on_feasible)
 };
 
 // ---------------------------------------------------------------------------

@@ -676,9 +676,12 @@ __global__ void __launch_bounds__(256) k_select(DevInst I, DevPop P, LsParams L)
       s_flag = 0;
     }
     __syncthreads();
-    for (int i = threadIdx.x; i < s_nt * P.Kp; i += blockDim.x) {
-      int r = tl[i / P.Kp], q = i % P.Kp;
-      P.scratch_seq[row_base(P, b, r) + q] = P.seq[row_base(P, b, r) + q];
+    {  // warp per touched route, its k+2 used sequence slots
+      const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+      for (int q = wid; q < s_nt; q += nw) {
+        const int r = tl[q], len = P.rmeta[(size_t)b * J + r].x + 2;
+        for (int x = lane; x < len; x += 32) P.scratch_seq[row_base(P, b, r) + x] = P.seq[row_base(P, b, r) + x];
+      }
     }
     for (int i = threadIdx.x; i < s_nt; i += blockDim.x)
       P.scratch_meta[(size_t)b * J + tl[i]] = P.rmeta[(size_t)b * J + tl[i]];
@@ -731,17 +734,25 @@ __global__ void __launch_bounds__(256) k_select(DevInst I, DevPop P, LsParams L)
       if (threadIdx.x == 0) s_mnew = carry;
     }
     __syncthreads();
-    for (int i = threadIdx.x; i < m2 * P.Kp; i += blockDim.x) {
-      int r = i / P.Kp, q = i - r * P.Kp;
-      if (newidx[r] >= 0) P.scratch_seq[row_base(P, b, newidx[r]) + q] = P.seq[row_base(P, b, r) + q];
+    {
+      const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+      for (int r = wid; r < m2; r += nw) {
+        if (newidx[r] < 0) continue;
+        const int len = P.rmeta[(size_t)b * J + r].x + 2;
+        for (int x = lane; x < len; x += 32)
+          P.scratch_seq[row_base(P, b, newidx[r]) + x] = P.seq[row_base(P, b, r) + x];
+      }
     }
     for (int r = threadIdx.x; r < m2; r += blockDim.x)
       if (newidx[r] >= 0) P.scratch_meta[(size_t)b * J + newidx[r]] = P.rmeta[(size_t)b * J + r];
     __syncthreads();
     const int mn_ = s_mnew;
-    for (int i = threadIdx.x; i < mn_ * P.Kp; i += blockDim.x) {
-      int r = i / P.Kp, q = i - r * P.Kp;
-      P.seq[row_base(P, b, r) + q] = P.scratch_seq[row_base(P, b, r) + q];
+    {
+      const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+      for (int r = wid; r < mn_; r += nw) {
+        const int len = P.scratch_meta[(size_t)b * J + r].x + 2;
+        for (int x = lane; x < len; x += 32) P.seq[row_base(P, b, r) + x] = P.scratch_seq[row_base(P, b, r) + x];
+      }
     }
     for (int r = threadIdx.x; r < mn_; r += blockDim.x)
       P.rmeta[(size_t)b * J + r] = P.scratch_meta[(size_t)b * J + r];
@@ -774,7 +785,7 @@ __global__ void __launch_bounds__(256) k_select(DevInst I, DevPop P, LsParams L)
       s_snap = 0;
       if (feas) {
         st.n_feasible++;
-        if (tot[0] < st.bestD) { st.bestD = tot[0]; st.n_improving++; s_snap = 1; }
+        if (tot[0] < st.bestD) { st.bestD = tot[0]; st.n_improving++; s_snap = L.snapshot; }
       }
       st.accepted++;
       st.any = 1;
@@ -783,10 +794,11 @@ __global__ void __launch_bounds__(256) k_select(DevInst I, DevPop P, LsParams L)
       P.st[b] = st;
     }
     __syncthreads();
-    if (s_snap) {
-      for (int i = threadIdx.x; i < mn * P.Kp; i += blockDim.x) {
-        int r = i / P.Kp, q = i - r * P.Kp;
-        P.best_seq[row_base(P, b, r) + q] = P.seq[row_base(P, b, r) + q];
+    if (s_snap) {  // best-feasible snapshot, only when the caller wants it (on_feasible)
+      const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+      for (int r = wid; r < mn; r += nw) {
+        const int len = P.rmeta[(size_t)b * J + r].x + 2;
+        for (int x = lane; x < len; x += 32) P.best_seq[row_base(P, b, r) + x] = P.seq[row_base(P, b, r) + x];
       }
       for (int r = threadIdx.x; r < mn; r += blockDim.x)
         P.best_meta[(size_t)b * J + r] = P.rmeta[(size_t)b * J + r];

@@ -157,7 +157,8 @@ class Population:
         return routes, bestD[:self.B]
 
     def local_search(self, perms: np.ndarray, depth: int, multi_move: bool, kappa: float, lam_min: float,
-                     lam_max: float, deadline_s: float = -1.0, rounds_per_sync: int = 8, stream=None):
+                     lam_max: float, deadline_s: float = -1.0, rounds_per_sync: int = 8, stream=None,
+                     snapshot_best: bool = False):
         """perms: uint8 [B, max_passes, n_ops]. Returns a list of per-individual stats dicts."""
         B = self.B
         perms = np.ascontiguousarray(perms, dtype=np.uint8)
@@ -170,6 +171,7 @@ class Population:
         cfg.deadline_s = float(deadline_s)
         cfg.rounds_per_sync = int(rounds_per_sync)
         cfg.use_graph = 0
+        cfg.snapshot_best = int(bool(snapshot_best))
         st = (LsStats * max(B, 1))()
         s = stream if stream is not None else _cur_stream(self.dinst.device)
         rc = _lib.lib().mdr_local_search(self.handle, C.byref(cfg), st, s)

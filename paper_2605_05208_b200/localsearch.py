@@ -149,14 +149,15 @@ class DeviceSearch:
         return p
 
     def run(self, sols, lams, perms, cfg: SearchConfig, kappa=0.5, lam_min=0.01, lam_max=1e4,
-            deadline_s: float = -1.0):
+            deadline_s: float = -1.0, snapshot_best: bool = False):
         """Descents of all `sols` (not modified). Returns (routes, lams, stats)."""
         need = None
         for attempt in range(8):
             pop = self._ensure(sols, need)
             pop.upload(sols, lams)
             try:
-                stats = pop.local_search(perms, cfg.depth, cfg.multi_move, kappa, lam_min, lam_max, deadline_s)
+                stats = pop.local_search(perms, cfg.depth, cfg.multi_move, kappa, lam_min, lam_max, deadline_s,
+                                         snapshot_best=snapshot_best)
                 break
             except CapacityError as e:
                 need = getattr(e, "need", None) or dict(F=1, G=0, J=0, K=0)
@@ -187,7 +188,7 @@ def local_search(sol, penalties, cfg: SearchConfig, nbr, consts, inst, rng, dead
     perms = draw_permutations(rng, ops, cfg.depth + 1)[None]
     dl = -1.0 if deadline is None else max(0.0, deadline - time.monotonic())
     routes, lam, stats = search.run([sol], [penalties.lam], perms, cfg, penalties.kappa, penalties.lam_min,
-                                    penalties.lam_max, dl)
+                                    penalties.lam_max, dl, snapshot_best=on_feasible is not None)
     st = stats[0]
     _advance(rng, ops, st["passes"])
     _apply_result(sol, routes[0])
