@@ -356,7 +356,8 @@ __global__ void __launch_bounds__(32 * MDR_CU, MDR_CMINB) k_eval_c(DevInst I, De
   const int *OFF = P.opoff + OP * (P.Bcap + 1);
   const int *OB = P.opb + OP * P.Bcap;
   const bool mm = L.multi_move != 0;
-  const int nch = (I.NC + MDR_CU - 1) / MDR_CU;
+  const int nch = (I.NC + MDR_CT - 1) / MDR_CT;
+  __shared__ int s_item;
   int staged = -1;
   if (threadIdx.x == 0) { s_next = 0; s_end = 0; s_lo = 0; s_hi = 0; }
   for (;;) {
@@ -370,6 +371,7 @@ __global__ void __launch_bounds__(32 * MDR_CU, MDR_CMINB) k_eval_c(DevInst I, De
       }
       int t = s_next < s_end ? s_next++ : total;
       s_t = t;
+      s_item = 0;
       if (t < total && (t < s_lo || t >= s_hi)) {
         int l2 = 0, h2 = cnt - 1;
         while (l2 < h2) {
@@ -395,15 +397,21 @@ __global__ void __launch_bounds__(32 * MDR_CU, MDR_CMINB) k_eval_c(DevInst I, De
 #pragma unroll
     for (int i = 0; i < 4; i++) lam[i] = P.lam[b * 4 + i];
     Acc acc{~0ull, ~0ull, 0};
-    if (OP == 2 && local >= nch) {
-      const int ra = (local - nch) * MDR_CU + wid;
-      if (ra < v.M) stos_r<WIN>(I, P, v, R, b, ra, lam, mm, acc);
-    } else {
-      const int u = I.ND + local * MDR_CU + wid;
-      if (u < I.N) {
-        if (OP == 0) srelocate<WIN>(I, P, v, R, b, u, lam, mm, acc, U);
-        else if (OP == 1) sswap<WIN>(I, P, v, R, b, u, lam, mm, acc, U);
-        else stos_u<WIN>(I, P, v, R, b, u, lam, mm, acc, U);
+    for (;;) {  // warps take the task's items dynamically
+      int it = 0;
+      if (lane == 0) it = atomicAdd(&s_item, 1);
+      it = __shfl_sync(0xffffffffu, it, 0);
+      if (it >= MDR_CT) break;
+      if (OP == 2 && local >= nch) {
+        const int ra = (local - nch) * MDR_CT + it;
+        if (ra < v.M) stos_r<WIN>(I, P, v, R, b, ra, lam, mm, acc);
+      } else {
+        const int u = I.ND + local * MDR_CT + it;
+        if (u < I.N) {
+          if (OP == 0) srelocate<WIN>(I, P, v, R, b, u, lam, mm, acc, U);
+          else if (OP == 1) sswap<WIN>(I, P, v, R, b, u, lam, mm, acc, U);
+          else stos_u<WIN>(I, P, v, R, b, u, lam, mm, acc, U);
+        }
       }
     }
     OK r = warp_min(OK{acc.o, acc.k});
