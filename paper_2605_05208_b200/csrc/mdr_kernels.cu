@@ -339,6 +339,9 @@ __global__ void __launch_bounds__(256, MDR_EVAL_MINB) k_eval(DevInst I, DevPop P
   }
 }
 
+#ifndef MDR_WDMAX
+#define MDR_WDMAX 32  // depot-indexed precomputes only up to this many depots
+#endif
 #ifndef MDR_TGC
 #define MDR_TGC 1
 #endif
@@ -347,6 +350,9 @@ template <bool WIN, int OP>
 __global__ void __launch_bounds__(32 * MDR_CU, MDR_CMINB) k_eval_c(DevInst I, DevPop P, LsParams L) {
   extern __shared__ __align__(16) unsigned char smx_c[];
   RB *R = reinterpret_cast<RB *>(smx_c);
+  // per-warp depot-indexed precomputes (front-insertion prefixes, 2-opt* A sides)
+  const int WS = I.ND <= MDR_WDMAX ? 18 * I.ND : 0;
+  double *Wd = WS ? reinterpret_cast<double *>(smx_c + sizeof(RB) * P.J) + (threadIdx.x >> 5) * WS : nullptr;
   __shared__ double s_u[MDR_CU][MDR_USLOT];
   __shared__ int s_t, s_b, s_lo, s_hi, s_next, s_end;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -408,9 +414,9 @@ __global__ void __launch_bounds__(32 * MDR_CU, MDR_CMINB) k_eval_c(DevInst I, De
       } else {
         const int u = I.ND + local * MDR_CT + it;
         if (u < I.N) {
-          if (OP == 0) srelocate<WIN>(I, P, v, R, b, u, lam, mm, acc, U);
+          if (OP == 0) srelocate<WIN>(I, P, v, R, b, u, lam, mm, acc, U, Wd);
           else if (OP == 1) sswap<WIN>(I, P, v, R, b, u, lam, mm, acc, U);
-          else stos_u<WIN>(I, P, v, R, b, u, lam, mm, acc, U);
+          else stos_u<WIN>(I, P, v, R, b, u, lam, mm, acc, U, Wd);
         }
       }
     }
@@ -993,7 +999,8 @@ static void launch_eval_t(const DevInst &I, const DevPop &P, const LsParams &L, 
   }
   if (P.staged) {
     static int gc[3] = {0, 0, 0};
-    const size_t sm = sizeof(RB) * (size_t)P.J;
+    const size_t sm = sizeof(RB) * (size_t)P.J +
+                      (I.ND <= MDR_WDMAX ? sizeof(double) * 18 * (size_t)I.ND * MDR_CU : 0);
     static size_t sm_set = 0;
     if (sm_set < sm) {
       cudaFuncSetAttribute(k_eval_c<WIN, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);

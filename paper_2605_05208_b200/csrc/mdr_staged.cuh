@@ -90,7 +90,7 @@ __device__ __forceinline__ bool two_route_delta(const DevInst &I, const double c
 // ---------------------------------------------------------------------------
 template <bool WIN>
 __device__ void srelocate(const DevInst &I, const DevPop &P, const IV &v, const RB *R, int b, int u,
-                          const double lam[4], bool mm, Acc &acc, double *U) {
+                          const double lam[4], bool mm, Acc &acc, double *U, double *Wd) {
   const int lane = threadIdx.x & 31;
   const int lu = __ldg(v.loc + u);
   if (lu < 0) return;
@@ -115,6 +115,20 @@ __device__ void srelocate(const DevInst &I, const DevPop &P, const IV &v, const 
   }
   __syncwarp();
   constexpr int nvar = WIN ? 2 : 3;
+  // front insertion (depot d) + seg is a per-(variant, depot) constant of this u:
+  // Wd[(vi*ND + d)*6 ..] = node(d) (+) seg_vi, the first concat of (node(d) (+) seg) (+) S[rb][1]
+  if (Wd) {
+    for (int idx = lane; idx < nvar * I.ND; idx += 32) {
+      const int vi = idx / I.ND, d = idx - vi * I.ND;
+      const int len = vi == 0 ? 1 : 2, rev = vi == 2;
+      if (pu + len <= k1) {
+        At<WIN> seg = ld_at<WIN>(U + (len == 1 ? 10 : 16), rev ? (len == 1 ? u : nxt) : u,
+                                 rev ? u : (len == 1 ? u : nxt));
+        st_at<WIN>(Wd + idx * 6, a_cat_l<WIN>(a_node<WIN>(I, d), seg, link_of(I, d, seg.first)));
+      }
+    }
+    __syncwarp();
+  }
   const double fdec1 = I.nv_on ? __ldg(v.fl + X1.dep).y : 0.0;
   // one candidate: target (r2, tgt) with prefix P2 and (possibly empty) suffix S2
   auto eval_inter = [&](int len, int rev, int r2, int tgt, const At<WIN> &P2, const At<WIN> &S2,
@@ -195,7 +209,21 @@ __device__ void srelocate(const DevInst &I, const DevPop &P, const IV &v, const 
         unsigned long long o = 0, key = 0;
         if (ok) {
           if (same) { gqf = true; key = key_of(ru, pu, rb, tgt, len, 0, rev, 0, -1, -1); }
-          else fol = eval_inter(len, rev, rb, tgt, P2, S2, R[rb], o, key);
+          else if (side == 0 && Wd) {
+            // B = (node(dep_rb) (+) seg) (+) S[rb][1] from the precomputed prefix
+            const RB &X2 = R[rb];
+            const int sl = rev ? u : (len == 1 ? u : nxt);
+            At<WIN> B = ld_at<WIN>(Wd + (vi * I.ND + X2.dep) * 6, X2.dep, sl);
+            if (S2.first >= 0) B = a_cat_l<WIN>(B, S2, link_of(I, sl, S2.first));
+            double cB[5];
+            contrib_fast<WIN>(I, B, X2.dep, X2.arr, X2.k + len, cB);
+            double fleet_delta = 0.0;
+            int fn = 1;
+            if (I.nv_on && k1 - len == 0) { fleet_delta = 0.0 + fdec1; fn = 0; }
+            fol = two_route_delta<WIN>(I, U + 5 * (len - 1), cB, X1.rc, X2.rc, X1.clo, X2.clo, fleet_delta, fn, lam,
+                                       acc, [&] { return key_of(ru, pu, rb, 0, len, 0, rev, 0, -1, -1); }, key, mm,
+                                       P.nanflag + b, o);
+          } else fol = eval_inter(len, rev, rb, tgt, P2, S2, R[rb], o, key);
         }
         append_fol(P, b, fol, o, key);
         enqueue_g(P, b, 0, gqf, key);
@@ -348,10 +376,33 @@ __device__ __forceinline__ bool tos_eval(const DevInst &I, const DevPop &P, cons
                               [&] { return key_of(r1, p1, r2, p2, 0, 0, 0, 0, -1, -1); }, key, mm, P.nanflag + b, o);
 }
 
+// A-side terms given (cA precomputed, nullptr = zero route); B = PB (+) SA computed
+template <bool WIN>
+__device__ __forceinline__ bool tos_eval_pre(const DevInst &I, const DevPop &P, const IV &v, int b, const RB &X1,
+                                             const RB &X2, int r1, int p1, int r2, int p2, const double *cA,
+                                             const At<WIN> &PB, const At<WIN> &SA, int uB, const double lam[4],
+                                             Acc &acc, bool mm, unsigned long long &o, unsigned long long &key) {
+  At<WIN> B = PB;
+  if (SA.first >= 0)
+    B = a_cat_l<WIN>(B, SA, uB ? link_to_u(I, PB.last, SA.first) : link_of(I, PB.last, SA.first));
+  const int kA = p1 + (X2.k - p2), kB = p2 + (X1.k - p1);
+  double cB[5];
+  const double z[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+  contrib_fast<WIN>(I, B, X2.dep, X1.arr, kB, cB);
+  double fleet_delta = 0.0;
+  int fn = 1;
+  if (I.nv_on) {
+    fleet_delta = (0.0 + (kA == 0 ? __ldg(v.fl + X1.dep).y : 0.0)) + (kB == 0 ? __ldg(v.fl + X2.dep).y : 0.0);
+    fn = (kA > 0) && (kB > 0);
+  }
+  return two_route_delta<WIN>(I, cA ? cA : z, cB, X1.rc, X2.rc, X1.clo, X2.clo, fleet_delta, fn, lam, acc,
+                              [&] { return key_of(r1, p1, r2, p2, 0, 0, 0, 0, -1, -1); }, key, mm, P.nanflag + b, o);
+}
+
 // warp task = customer u: granular cut and the two boundary families
 template <bool WIN>
 __device__ void stos_u(const DevInst &I, const DevPop &P, const IV &v, const RB *R, int b, int u, const double lam[4],
-                       bool mm, Acc &acc, double *U) {
+                       bool mm, Acc &acc, double *U, double *Wd) {
   const int lane = threadIdx.x & 31;
   const int lu = __ldg(v.loc + u);
   if (lu < 0) return;
@@ -396,6 +447,18 @@ __device__ void stos_u(const DevInst &I, const DevPop &P, const IV &v, const RB 
   // boundary families for every route rb != ru
   const At<WIN> PU0 = ld_at<WIN>(U + 12, X1.dep, lastP0);
   const At<WIN> SU1 = ld_at<WIN>(U + 18, u, lastS);
+  // their A sides depend on u and one depot only: Wd[d*5..] = terms of P[ru][pu+1] (+) arrival d,
+  // Wd[(ND+d)*5..] = terms of departure d (+) S[ru][pu+1]
+  if (Wd) {
+    for (int d = lane; d < I.ND; d += 32) {
+      At<WIN> A1 = PU1;
+      if (!I.open) A1 = a_cat_l<WIN>(PU1, a_node<WIN>(I, d), link_of(I, u, d));
+      contrib_fast<WIN>(I, A1, X1.dep, d, pu + 1, Wd + d * 5);
+      At<WIN> A2 = a_cat_l<WIN>(a_node<WIN>(I, d), SU1, link_of(I, d, u));
+      contrib_fast<WIN>(I, A2, d, X1.arr, X1.k - pu, Wd + (I.ND + d) * 5);
+    }
+    __syncwarp();
+  }
   for (int base = 0; base < v.M; base += 32) {
     const int rb = base + lane;
     const bool in = rb < v.M && rb != ru;
@@ -408,9 +471,14 @@ __device__ void stos_u(const DevInst &I, const DevPop &P, const IV &v, const RB 
         bool drop = (pu + 1 == X1.k);
         if (!I.open) drop = drop && (X1.arr == X2.arr);
         if (!drop) {
-          At<WIN> SB = I.open ? a_empty<WIN>() : a_node<WIN>(I, X2.arr);
-          fol = tos_eval<WIN>(I, P, v, b, X1, X2, ru, pu + 1, rb, X2.k, PU1, SB, rb_pb<WIN>(X2), SU2, 0, 1, lam, acc,
-                              mm, o, key);
+          if (Wd) {
+            fol = tos_eval_pre<WIN>(I, P, v, b, X1, X2, ru, pu + 1, rb, X2.k, Wd + (I.open ? 0 : X2.arr) * 5,
+                                    rb_pb<WIN>(X2), SU2, 1, lam, acc, mm, o, key);
+          } else {
+            At<WIN> SB = I.open ? a_empty<WIN>() : a_node<WIN>(I, X2.arr);
+            fol = tos_eval<WIN>(I, P, v, b, X1, X2, ru, pu + 1, rb, X2.k, PU1, SB, rb_pb<WIN>(X2), SU2, 0, 1, lam,
+                                acc, mm, o, key);
+          }
         }
       }
       append_fol(P, b, fol, o, key);
@@ -422,8 +490,12 @@ __device__ void stos_u(const DevInst &I, const DevPop &P, const IV &v, const RB 
       if (in) {
         const RB &X2 = R[rb];
         At<WIN> SB = X2.sf_first >= 0 ? rb_sf<WIN>(X2) : a_empty<WIN>();
-        fol = tos_eval<WIN>(I, P, v, b, X2, X1, rb, 0, ru, pu, a_node<WIN>(I, X2.dep), SU1, PU0, SB, 1, 0, lam, acc,
-                            mm, o, key);
+        if (Wd)
+          fol = tos_eval_pre<WIN>(I, P, v, b, X2, X1, rb, 0, ru, pu, Wd + (I.ND + X2.dep) * 5, PU0, SB, 0, lam, acc,
+                                  mm, o, key);
+        else
+          fol = tos_eval<WIN>(I, P, v, b, X2, X1, rb, 0, ru, pu, a_node<WIN>(I, X2.dep), SU1, PU0, SB, 1, 0, lam,
+                              acc, mm, o, key);
       }
       append_fol(P, b, fol, o, key);
     }
@@ -444,10 +516,10 @@ __device__ void stos_r(const DevInst &I, const DevPop &P, const IV &v, const RB 
     bool fol = false;
     unsigned long long o = 0, key = 0;
     if (rb < v.M && rb != ra) {
+      // kA = 0 + (k_rb - k_rb) = 0: route ra empties, its new terms are exact zeros
       const RB &X2 = R[rb];
-      At<WIN> SB = I.open ? a_empty<WIN>() : a_node<WIN>(I, X2.arr);
-      fol = tos_eval<WIN>(I, P, v, b, X1, X2, ra, 0, rb, X2.k, PA, SB, rb_pb<WIN>(X2), SA, 0, 1, lam, acc, mm, o,
-                          key);
+      fol = tos_eval_pre<WIN>(I, P, v, b, X1, X2, ra, 0, rb, X2.k, nullptr, rb_pb<WIN>(X2), SA, 1, lam, acc, mm, o,
+                              key);
     }
     append_fol(P, b, fol, o, key);
   }
