@@ -435,7 +435,10 @@ __global__ void __launch_bounds__(32 * MDR_CU, MDR_CMINB) k_eval_c(DevInst I, De
 // generic evaluator: intra-route relocate/swap, 2-opt, depot operators,
 // one thread per queued candidate through eval_cand (batch.py:365-553)
 template <bool WIN>
-__global__ void __launch_bounds__(256) k_eval_g(DevInst I, DevPop P, LsParams L) {
+#ifndef MDR_GMINB
+#define MDR_GMINB 3
+#endif
+__global__ void __launch_bounds__(256, MDR_GMINB) k_eval_g(DevInst I, DevPop P, LsParams L) {
   const int lane = threadIdx.x & 31;
   const int total = min(*P.gcount, P.Gcap);
   const bool mm = L.multi_move != 0;
@@ -1061,8 +1064,15 @@ void launch_eval(const DevInst &I, const DevPop &P, const LsParams &L, int grid,
 }
 
 void launch_eval_g(const DevInst &I, const DevPop &P, const LsParams &L, int grid, bool win, cudaStream_t s) {
-  if (win) k_eval_g<true><<<grid, 256, 0, s>>>(I, P, L);
-  else k_eval_g<false><<<grid, 256, 0, s>>>(I, P, L);
+  (void)grid;
+  static int gt = 0, gf = 0;  // full occupancy of the (latency-bound) generic evaluator
+  if (win) {
+    if (!gt) gt = grid_for(k_eval_g<true>);
+    k_eval_g<true><<<gt, 256, 0, s>>>(I, P, L);
+  } else {
+    if (!gf) gf = grid_for(k_eval_g<false>);
+    k_eval_g<false><<<gf, 256, 0, s>>>(I, P, L);
+  }
 }
 
 void launch_select(const DevInst &I, const DevPop &P, const LsParams &L, bool win, cudaStream_t s) {

@@ -1,5 +1,5 @@
 # quick A/B of library variants on C4 (1 step)
-for L in libmdr_sm100.so libmdr_sm100_ct16.so libmdr_sm100_ct32.so; do
+for L in libmdr_sm100.so libmdr_sm100_g2.so libmdr_sm100_g3.so libmdr_sm100_g4.so; do
   echo "== $L"
   MDR_LIB=$PWD/paper_2605_05208_b200/$L timeout 300 python bench.py --config C4 --steps 1 --warmup 1 --no-cpu-baseline --no-e2e 2>&1 | python -c "
 import sys,json
