@@ -779,16 +779,24 @@ __global__ void __launch_bounds__(256) k_select(DevInst I, DevPop P, LsParams L)
     }
     const int mn = s_mnew;
     // ---- totals, adapt_penalties, bookkeeping (localsearch.py:128-138)
-    if (threadIdx.x == 0) {
+    // the four pairwise sums run on four warps; the closure count (0/1 values,
+    // exact in any order) on a fifth
+    __shared__ double s_tot[5];
+    {
+      const int wid = threadIdx.x >> 5;
       const double4 *RC = P.rcon + (size_t)b * J;
-      double tot[5];
-      tot[0] = pw_sum(RC, 0, mn);
-      tot[1] = pw_sum(RC, 1, mn);
-      tot[2] = pw_sum(RC, 2, mn);
-      tot[3] = pw_sum(RC, 3, mn);
-      double clo = 0.0;  // sum of 0/1 values: exact in any order
-      for (int r = 0; r < mn; r++) clo += (double)P.rmeta[(size_t)b * J + r].w;
-      tot[4] = I.theta * (clo + P.fexcess[b]);
+      if ((threadIdx.x & 31) == 0) {
+        if (wid < 4) s_tot[wid] = pw_sum(RC, wid, mn);
+        else if (wid == 4) {
+          double clo = 0.0;
+          for (int r = 0; r < mn; r++) clo += (double)P.rmeta[(size_t)b * J + r].w;
+          s_tot[4] = I.theta * (clo + P.fexcess[b]);
+        }
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double tot[5] = {s_tot[0], s_tot[1], s_tot[2], s_tot[3], s_tot[4]};
       LsState st = P.st[b];
       bool feas = true;
       for (int i = 0; i < 4; i++) {
