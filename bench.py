@@ -16,6 +16,7 @@ whole job; descents/s is reported beside it.
 from __future__ import annotations
 
 import argparse
+import ctypes
 import json
 import os
 import random
@@ -109,6 +110,24 @@ def flush_l2(torch, dev):
     buf = torch.empty(64 << 22, dtype=torch.float32, device=dev)  # 1 GiB > 126 MB L2
     buf.fill_(1.0)
     del buf
+
+
+def measure_l2_gbs(device, mib=32, iters=200):
+    """L2 read bandwidth (native probe: L1-bypassing loads over a 32 MiB
+    L2-resident buffer) -- the on-chip denominator next to the HBM one."""
+    from paper_2605_05208_b200 import _lib
+    out = ctypes.c_double(0.0)
+    _lib.check(_lib.lib().mdr_probe_l2_gbs(device, mib << 20, iters, ctypes.byref(out)), "mdr_probe_l2_gbs")
+    return out.value
+
+
+def load_traffic():
+    """DRAM bytes of one evaluation phase from the committed ncu --set full capture."""
+    try:
+        t = json.load(open(os.path.join(ROOT, "profiles", "r1_traffic.json")))
+        return float(t["evaluation_phase_dram_bytes_per_round"]), t["source"]
+    except Exception:
+        return None, None
 
 
 def cpu_baseline(name, inst, consts, nbr, sols, depth, seconds=20.0):
@@ -287,6 +306,8 @@ def main():
     except Exception:
         pass
     hbm = float(peaks.get("hbm_gbs", 6650.0))
+    l2_gbs = measure_l2_gbs(local)
+    traffic, traffic_src = load_traffic()
 
     # e2e: through the public API with host Solution objects, H2D + D2H inside
     e2e = None
@@ -340,11 +361,15 @@ def main():
             "descents_per_s": desc_all / (tot_ms / 1000.0),
             "candidates_per_step": cands_all / args.steps,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                         "frac": achieved / hbm, "traffic": None,
+                         "frac": achieved / hbm, "traffic": traffic,
+                         "traffic_source": traffic_src,
+                         "l2": {"peak_measured_gbs": l2_gbs, "frac": achieved / l2_gbs,
+                                "how": "mdr_probe_l2_gbs: ld.global.cg 16 B loads over a 32 MiB buffer x200, CUDA events"},
                          "kernel": "evaluation phase: k_eval<op> (fused enumerate+evaluate+reduce) + k_eval_g",
                          "eval_share_of_step": (tm["eval_ms"] + tm["geval_ms"]) / max(tm["total_ms"], 1e-9),
-                         "note": "working set is L2-resident (ncu DRAM throughput ~0%); algorithmic bytes "
-                                 "per SURVEY.md 8(d) over the HBM peak can exceed 1",
+                         "note": "working set is L2/L1-resident (ncu: DRAM traffic ~1% of the algorithmic "
+                                 "bytes); algorithmic bytes per SURVEY.md 8(d) over the HBM peak exceed 1, "
+                                 "the kernels are latency/issue-bound (DESIGN.md 7)",
                          "eval_avg_launch_ms": eval_avg_ms,
                          "alg_bytes_per_launch": alg_bytes / max(tm["eval_launches"], 1),
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback"},

@@ -152,6 +152,11 @@ int mdr_get_timing(mdr_pop *pop, mdr_timing *out);
 int mdr_shuffle_stream(uint32_t *state, int32_t n_items, const uint8_t *items, int32_t n_passes, uint8_t *out);
 int mdr_set_profiling(mdr_pop *pop, int32_t on);
 
+/* Diagnostic (no reference counterpart): L2 read bandwidth in GB/s, measured
+ * with L1-bypassing 16-byte loads over a `bytes` buffer read `iters` times --
+ * the on-chip roofline denominator bench.py reports beside the HBM peak. */
+int mdr_probe_l2_gbs(int32_t device, int64_t bytes, int32_t iters, double *gbs);
+
 #ifdef __cplusplus
 }
 #endif

@@ -13,7 +13,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def _declared():
     src = open(os.path.join(ROOT, "include", "mdr_sm100.h")).read()
-    return sorted(set(re.findall(r"\b(mdr_[a-z_]+)\s*\(", src)))
+    return sorted(set(re.findall(r"\b(mdr_[a-z0-9_]+)\s*\(", src)))
 
 
 def test_header_declares_exactly_the_bound_symbols():
