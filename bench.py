@@ -40,6 +40,10 @@ from paper_2605_05208_b200.neighborhood import NeighborConfig, build  # noqa: E4
 # figures for relocate/swap.  Windows (C2, C4) / no windows (C1, C3, C5).
 ALG_BYTES_WIN = {0: 436, 1: 500, 2: 372, 3: 0, 4: 304, 5: 204}
 ALG_BYTES_NOWIN = {0: 316, 1: 356, 2: 276, 3: 204, 4: 208, 5: 148}
+# algorithmic fp64 ops (add/sub/mul/div/max/min of the
+# reference DAG) per candidate, inter-route figures for relocate/swap.
+ALG_FP64_WIN = {0: 111, 1: 133, 2: 89, 3: 0, 4: 106, 5: 69}
+ALG_FP64_NOWIN = {0: 50, 1: 55, 2: 45, 3: 30, 4: 45, 5: 30}
 
 
 def _init_one(args):
@@ -118,6 +122,14 @@ def measure_l2_gbs(device, mib=32, iters=200):
     from paper_2605_05208_b200 import _lib
     out = ctypes.c_double(0.0)
     _lib.check(_lib.lib().mdr_probe_l2_gbs(device, mib << 20, iters, ctypes.byref(out)), "mdr_probe_l2_gbs")
+    return out.value
+
+
+def measure_fp64_gops(device, iters=4096):
+    """fp64 dadd/dmul issue rate (native probe, FMA contraction off)."""
+    from paper_2605_05208_b200 import _lib
+    out = ctypes.c_double(0.0)
+    _lib.check(_lib.lib().mdr_probe_fp64_gops(device, iters, ctypes.byref(out)), "mdr_probe_fp64_gops")
     return out.value
 
 
@@ -297,9 +309,12 @@ def main():
     op_c = np.sum([s["cands"] for s in st_p], axis=0)
     ab = ALG_BYTES_WIN if inst.has_windows else ALG_BYTES_NOWIN
     alg_bytes = float(sum(op_c[o] * ab[o] for o in range(6)))
+    af = ALG_FP64_WIN if inst.has_windows else ALG_FP64_NOWIN
+    alg_fp64 = float(sum(op_c[o] * af[o] for o in range(6)))
     # the evaluation phase of a round = the per-operator fused kernels + the generic-path kernel
     eval_avg_ms = (tm["eval_ms"] + tm["geval_ms"]) / max(tm["eval_launches"], 1)
     achieved = alg_bytes / max(tm["eval_launches"], 1) / (eval_avg_ms * 1e-3) / 1e9
+    fp64_gops = alg_fp64 / max(tm["eval_launches"], 1) / (eval_avg_ms * 1e-3) / 1e9
     peaks = {}
     try:
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -307,7 +322,21 @@ def main():
         pass
     hbm = float(peaks.get("hbm_gbs", 6650.0))
     l2_gbs = measure_l2_gbs(local)
+    fp64_peak = measure_fp64_gops(local)
     traffic, traffic_src = load_traffic()
+
+    # the granular neighbour-list build on the device (one
+    # call incl. H2D of the matrix) vs the host restatement, on this instance
+    from paper_2605_05208_b200.neighborhood import build_device as nbr_device
+    t0 = time.perf_counter()
+    nb_dev = nbr_device(inst, NeighborConfig(spec.theta), consts, device=local)
+    nb_call_ms = 1000 * (time.perf_counter() - t0)
+    t0 = time.perf_counter()
+    nb_host = build(inst, NeighborConfig(spec.theta), consts)
+    nb_host_ms = 1000 * (time.perf_counter() - t0)
+    nbr_line = {"kernel_ms": nb_dev.kernel_ms, "call_ms": nb_call_ms, "host_numpy_ms": nb_host_ms,
+                "identical": bool(np.array_equal(nb_dev.lists, nb_host.lists)),
+                "nodes": inst.n_nodes, "theta": spec.theta}
 
     # e2e: through the public API with host Solution objects, H2D + D2H inside
     e2e = None
@@ -365,6 +394,11 @@ def main():
                          "traffic_source": traffic_src,
                          "l2": {"peak_measured_gbs": l2_gbs, "frac": achieved / l2_gbs,
                                 "how": "mdr_probe_l2_gbs: ld.global.cg 16 B loads over a 32 MiB buffer x200, CUDA events"},
+                         "fp64": {"achieved_gops": fp64_gops, "peak_measured_gops": fp64_peak,
+                                  "frac": fp64_gops / fp64_peak,
+                                  "how": "algorithmic fp64 ops per candidate (SURVEY.md 8(d)) / eval-phase time; "
+                                         "peak = mdr_probe_fp64_gops (dmul+dadd chains, no FMA)"},
+                         "binding_frac": max(achieved / l2_gbs, fp64_gops / fp64_peak),
                          "kernel": "evaluation phase: k_eval<op> (fused enumerate+evaluate+reduce) + k_eval_g",
                          "eval_share_of_step": (tm["eval_ms"] + tm["geval_ms"]) / max(tm["total_ms"], 1e-9),
                          "note": "working set is L2/L1-resident (ncu: DRAM traffic ~1% of the algorithmic "
@@ -376,6 +410,7 @@ def main():
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": int(launches),
+            "neighbor_build": nbr_line,
             "clocks": clocks,
             "profile": {"rounds_per_step": rounds / args.steps, "plan_ms": tm["plan_ms"], "eval_ms": tm["eval_ms"],
                         "geval_ms": tm["geval_ms"],

@@ -152,10 +152,22 @@ int mdr_get_timing(mdr_pop *pop, mdr_timing *out);
 int mdr_shuffle_stream(uint32_t *state, int32_t n_items, const uint8_t *items, int32_t n_passes, uint8_t *out);
 int mdr_set_profiling(mdr_pop *pop, int32_t on);
 
+/* Granular neighbour lists on the device; replaces neighborhood.build
+ * (neighborhood.py:60-101).  Host buffers: dist/time [n*n] (time NULL or ==
+ * dist: alias), tw_early/tw_late/service [n]; out lists [n*theta] (-1 padded,
+ * rows ascending by (eta, id)), mask [n*n] (0/1) or NULL.  kernel_ms (optional)
+ * receives the build kernel's device time.  theta <= 2048. */
+int mdr_neighbor_build(int32_t device, int32_t n, int32_t n_depots, const double *dist, const double *time,
+                       const double *tw_early, const double *tw_late, const double *service, double gamma,
+                       double alpha, double beta, int32_t theta, int32_t *lists, uint8_t *mask, float *kernel_ms);
+
 /* Diagnostic (no reference counterpart): L2 read bandwidth in GB/s, measured
  * with L1-bypassing 16-byte loads over a `bytes` buffer read `iters` times --
  * the on-chip roofline denominator bench.py reports beside the HBM peak. */
 int mdr_probe_l2_gbs(int32_t device, int64_t bytes, int32_t iters, double *gbs);
+/* Diagnostic: fp64 dadd/dmul throughput in G ops/s (FMA contraction off, as in
+ * the evaluators) -- the FP64-pipe roofline denominator of SURVEY.md 8(d). */
+int mdr_probe_fp64_gops(int32_t device, int32_t iters, double *gops);
 
 #ifdef __cplusplus
 }

@@ -11,7 +11,7 @@ the C-ABI of include/mdr_sm100.h (libmdr_sm100.so); there is no CPU fallback.
 """
 from .model import INF, Instance, Node, Route, Solution, Variant
 from .evaluation import LAMBDA_MAX, LAMBDA_MIN, PenaltyState, ScalingConstants, adapt_penalties
-from .neighborhood import NeighborConfig, NeighborLists, build as build_neighbors
+from .neighborhood import NeighborConfig, NeighborLists, build as build_neighbors, build_device as build_neighbors_device
 from .moves import (ALL_OPS, MODE_ARRIVE, MODE_BOTH, MODE_DEPART, CandidateSet, Move, Op, RoutePlan,
                     SolutionIndex, enumerate_candidates, move_plan)
 from .batch import DeltaArrays, SolutionCache, evaluate_candidates, leader_and_followers
@@ -20,7 +20,7 @@ from .localsearch import (DeviceSearch, SearchConfig, apply_moves, enabled_opera
 
 __all__ = [
     "INF", "Instance", "Node", "Route", "Solution", "Variant", "LAMBDA_MAX", "LAMBDA_MIN", "PenaltyState",
-    "ScalingConstants", "adapt_penalties", "NeighborConfig", "NeighborLists", "build_neighbors", "ALL_OPS",
+    "ScalingConstants", "adapt_penalties", "NeighborConfig", "NeighborLists", "build_neighbors", "build_neighbors_device", "ALL_OPS",
     "MODE_ARRIVE", "MODE_BOTH", "MODE_DEPART", "CandidateSet", "Move", "Op", "RoutePlan", "SolutionIndex",
     "enumerate_candidates", "move_plan", "DeltaArrays", "SolutionCache", "evaluate_candidates",
     "leader_and_followers", "DeviceSearch", "SearchConfig", "apply_moves", "enabled_operators",

@@ -196,6 +196,7 @@ int mdr_pop_create(mdr_instance *inst, int32_t Bcap, int32_t J, int32_t K, int32
   DA(A, P.rmeta, rows);
   DA(A, P.seq, slots);
   DA(A, P.loc, (size_t)Bcap * I.N);
+  DA(A, P.nxs, (size_t)Bcap * I.N);
   DA(A, P.rcon, rows);
   DA(A, P.tabP, slots * P.FE);
   DA(A, P.tabS, slots * P.FE);
@@ -241,6 +242,7 @@ int mdr_pop_create(mdr_instance *inst, int32_t Bcap, int32_t J, int32_t K, int32
   DA(A, P.best_meta, rows);
   DA(A, P.best_seq, slots);
   CK(cudaMemset(P.m, 0, sizeof(int) * Bcap));
+  CK(cudaMemset(P.nxs, 0xff, sizeof(int) * (size_t)Bcap * I.N));
   CK(cudaMemset(P.best_m, 0, sizeof(int) * Bcap));
   CK(cudaMemset(P.rmeta, 0, sizeof(int4) * rows));
   CK(cudaMemset(P.st, 0, sizeof(LsState) * Bcap));

@@ -54,6 +54,7 @@ struct DevPop {
   int4 *rmeta;
   int *seq;
   int *loc;
+  int *nxs;  // [B][N] node after this customer in its route's sequence (arrive depot), -1 past the end
   double4 *rcon;
   double *tabP, *tabS;
   double *tabT;  // [B][J][Kp][Kp][FE] full subsequence table (i..j), left fold from i

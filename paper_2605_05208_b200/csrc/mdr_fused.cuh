@@ -23,7 +23,7 @@ struct IV {
   const double *tP, *tS;
   const int4 *rm;
   const double4 *rc;
-  const int *loc;
+  const int *loc, *nxs;
   const double2 *fl;
   int Kp, M;
 };
@@ -48,6 +48,7 @@ __device__ __forceinline__ IV make_iv(const DevPop &P, int b) {
   v.rm = P.rmeta + rows;
   v.rc = P.rcon + rows;
   v.loc = P.loc + (size_t)b * P.N;
+  v.nxs = P.nxs + (size_t)b * P.N;
   v.fl = P.fleet + (size_t)b * P.ND;
   v.Kp = P.Kp;
   v.M = P.m[b];

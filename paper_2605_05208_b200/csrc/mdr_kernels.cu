@@ -119,6 +119,7 @@ __device__ double pw_sum(const double4 *a, int f, int n) {
 template <bool WIN>
 __device__ void rebuild_routes(const DevInst &I, const DevPop &P, int b, const int *list, int cnt) {
   int *LOC = P.loc + (size_t)b * P.N;
+  int *NXS = P.nxs + (size_t)b * P.N;
   int4 *RM = P.rmeta + (size_t)b * P.J;
   double4 *RC = P.rcon + (size_t)b * P.J;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
@@ -127,7 +128,10 @@ __device__ void rebuild_routes(const DevInst &I, const DevPop &P, int b, const i
     int4 mt = RM[r];
     int k = mt.x, n = k + (I.open ? 1 : 2);
     const int *sq = P.seq + row_base(P, b, r);
-    for (int p = lane; p < k; p += 32) LOC[sq[p + 1]] = (r << 9) | p;
+    for (int p = lane; p < k; p += 32) {
+      LOC[sq[p + 1]] = (r << 9) | p;
+      NXS[sq[p + 1]] = p + 2 <= n - 1 ? sq[p + 2] : -1;
+    }
     for (int i = lane; i < n; i += 32) {
       At<WIN> acc = a_node<WIN>(I, sq[i]);
       double *trow = P.tabT + (row_base(P, b, r) + i) * P.Kp * P.FE;  // T[r][i][*]
@@ -182,7 +186,7 @@ __device__ void rebuild_fleet(const DevInst &I, const DevPop &P, int b, int *sm_
 template <bool WIN>
 __device__ void rebuild_block(const DevInst &I, const DevPop &P, int b, int *sm_cnt) {
   int *LOC = P.loc + (size_t)b * P.N;
-  for (int v = threadIdx.x; v < P.N; v += blockDim.x) LOC[v] = -1;
+  for (int v = threadIdx.x; v < P.N; v += blockDim.x) { LOC[v] = -1; P.nxs[(size_t)b * P.N + v] = -1; }
   __syncthreads();
   rebuild_routes<WIN>(I, P, b, nullptr, P.m[b]);
   __syncthreads();

@@ -131,11 +131,13 @@ __device__ void srelocate(const DevInst &I, const DevPop &P, const IV &v, const 
   }
   const double fdec1 = I.nv_on ? __ldg(v.fl + X1.dep).y : 0.0;
   // one candidate: target (r2, tgt) with prefix P2 and (possibly empty) suffix S2
-  auto eval_inter = [&](int len, int rev, int r2, int tgt, const At<WIN> &P2, const At<WIN> &S2,
+  // one candidate: target (r2, tgt) with prefix P2 and (possibly empty) suffix S2,
+  // joined to the segment by the links Lp (P2.last -> seg.first) and Ls (seg.last -> S2.first)
+  auto eval_links = [&](int len, int rev, int r2, int tgt, const At<WIN> &P2, const At<WIN> &S2, Link Lp, Link Ls,
                         const RB &X2, unsigned long long &o, unsigned long long &key) -> bool {
     At<WIN> seg = ld_at<WIN>(U + (len == 1 ? 10 : 16), rev ? (len == 1 ? u : nxt) : u, rev ? u : (len == 1 ? u : nxt));
-    At<WIN> B = a_cat_l<WIN>(P2, seg, link_to_u(I, P2.last, seg.first));
-    if (S2.first >= 0) B = a_cat_l<WIN>(B, S2, link_of(I, seg.last, S2.first));
+    At<WIN> B = a_cat_l<WIN>(P2, seg, Lp);
+    if (S2.first >= 0) B = a_cat_l<WIN>(B, S2, Ls);
     double cB[5];
     contrib_fast<WIN>(I, B, X2.dep, X2.arr, X2.k + len, cB);
     double fleet_delta = 0.0;
@@ -145,24 +147,49 @@ __device__ void srelocate(const DevInst &I, const DevPop &P, const IV &v, const 
                                 [&] { return key_of(ru, pu, r2, tgt, len, 0, rev, 0, -1, -1); }, key, mm,
                                 P.nanflag + b, o);
   };
-  // granular targets: insert after v (p2 = pv + 1)
+  auto eval_inter = [&](int len, int rev, int r2, int tgt, const At<WIN> &P2, const At<WIN> &S2, const RB &X2,
+                        unsigned long long &o, unsigned long long &key) -> bool {
+    const int sf = rev ? (len == 1 ? u : nxt) : u, sl = rev ? u : (len == 1 ? u : nxt);
+    Link Ls{0.0, 0.0};
+    if (S2.first >= 0) Ls = link_of(I, sl, S2.first);
+    return eval_links(len, rev, r2, tgt, P2, S2, link_to_u(I, P2.last, sf), Ls, X2, o, key);
+  };
+  // granular targets: insert after v (p2 = pv + 1).  The node ids around the
+  // insertion point are v itself and nxs[v], so every distance link is issued
+  // as soon as those two ids are known (one dependent load after the list).
   const int W = I.W;
   const int *lst = I.lists + (size_t)(u - I.ND) * W;
+  const bool has2 = pu + 2 <= k1;
   for (int base = 0; base < W; base += 32) {
     const int t = base + lane;
-    int rv = -1, tgt = -1;
-    if (t < W) {
-      int vv = __ldg(lst + t);
-      if (vv >= 0) {
-        int lv = __ldg(v.loc + vv);
-        if (lv >= 0) { rv = loc_r(lv); tgt = loc_p(lv) + 1; }
+    int vv = -1, lv = -1, sv = -1;
+    if (t < W) vv = __ldg(lst + t);
+    Link Lvu{0.0, 0.0}, Lvn{0.0, 0.0}, Lus{0.0, 0.0}, Lns{0.0, 0.0};
+    if (vv >= 0) {
+      lv = __ldg(v.loc + vv);
+      sv = __ldg(v.nxs + vv);
+      Lvu = link_to_u(I, vv, u);
+      if (nvar == 3 && has2) Lvn = link_to_u(I, vv, nxt);
+      if (sv >= 0) {
+        Lus = link_of(I, u, sv);
+        if (has2) Lns = link_of(I, nxt, sv);
       }
     }
+    int rv = -1, tgt = -1;
+    if (lv >= 0) { rv = loc_r(lv); tgt = loc_p(lv) + 1; }
     const bool same = rv == ru;
     At<WIN> P2, S2;
     if (rv >= 0 && !same) {
-      P2 = pre<WIN>(v, rv, tgt);
-      S2 = suf<WIN>(v, rv, tgt + 1, R[rv].n);
+      P2 = ld_tab<WIN>(v.tP, rv * v.Kp + tgt);
+      P2.first = vv;  // (unused by the deltas)
+      P2.last = vv;
+      if (sv >= 0) {
+        S2 = ld_tab<WIN>(v.tS, rv * v.Kp + tgt + 1);
+        S2.first = sv;
+        S2.last = sv;  // (unused by the deltas)
+      } else {
+        S2 = a_empty<WIN>();
+      }
     }
 #pragma unroll
     for (int vi = 0; vi < nvar; vi++) {
@@ -173,7 +200,8 @@ __device__ void srelocate(const DevInst &I, const DevPop &P, const IV &v, const 
       unsigned long long o = 0, key = 0;
       if (ok) {
         if (same) { gqf = true; key = key_of(ru, pu, rv, tgt, len, 0, rev, 0, -1, -1); }
-        else fol = eval_inter(len, rev, rv, tgt, P2, S2, R[rv], o, key);
+        else fol = eval_links(len, rev, rv, tgt, P2, S2, (len == 2 && rev) ? Lvn : Lvu,
+                              (len == 1 || rev) ? Lus : Lns, R[rv], o, key);
       }
       append_fol(P, b, fol, o, key);
       enqueue_g(P, b, 0, gqf, key);

@@ -38,5 +38,6 @@ for row in csv.reader(io.StringIO(out)):
     tot += n
     stot += s
 print("total warp inst %.3g" % tot)
-for key, n in sorted(agg.items(), key=lambda kv: -stall[kv[0]])[:top]:
+order = sys.argv[4] if len(sys.argv) > 4 else "stall"
+for key, n in sorted(agg.items(), key=lambda kv: -(stall[kv[0]] if order == "stall" else kv[1]))[:top]:
     print(f"{n / tot * 100:5.1f}% inst {stall[key] / stot * 100:5.1f}% stall  {key[0]}:{key[1]:<4d} {src[key]}")
