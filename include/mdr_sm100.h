@@ -152,6 +152,22 @@ int mdr_get_timing(mdr_pop *pop, mdr_timing *out);
 int mdr_shuffle_stream(uint32_t *state, int32_t n_items, const uint8_t *items, int32_t n_passes, uint8_t *out);
 int mdr_set_profiling(mdr_pop *pop, int32_t on);
 
+/* Repair insertion (genetic.repair_insert, genetic.py:174-244) on the device
+ * for individuals 0..B-1 of the last upload: op FBI=0, IBI=1, FRI=2, IRI=3 (RI
+ * only draws from the rng; it stays with the caller).  pend_off [B+1], pend:
+ * the unrouted customers of each individual (any order; sorted as the
+ * reference does).  lam = the uploaded penalty weights.  On MDR_OK the
+ * population holds the repaired solutions, rebuilt and ready for
+ * mdr_local_search / mdr_pop_download.  MDR_ERR_CAPACITY: grow J_cap / K_cap
+ * to stats[b].need_j / need_k, re-upload and retry. */
+typedef struct mdr_repair_stats {
+  int32_t status, inserted, need_j, need_k;
+  int64_t slot_evals;     /* slot evaluations performed on the device */
+  int64_t ref_slot_evals; /* slot evaluations the reference's full re-scan performs */
+} mdr_repair_stats;
+int mdr_repair(mdr_pop *pop, int32_t op, const int32_t *pend_off, const int32_t *pend, mdr_repair_stats *stats,
+               void *stream);
+
 /* Granular neighbour lists on the device; replaces neighborhood.build
  * (neighborhood.py:60-101).  Host buffers: dist/time [n*n] (time NULL or ==
  * dist: alias), tw_early/tw_late/service [n]; out lists [n*theta] (-1 padded,

@@ -79,6 +79,8 @@ def lib():
         L.orc_local_search.restype = C.c_int
         L.orc_local_search_many.restype = C.c_int
         L.orc_eval_all_many.restype = C.c_int64
+        L.orc_repair.restype = C.c_int
+        L.orc_repair_many.restype = C.c_int
         _LIB = L
     return _LIB
 
@@ -306,3 +308,51 @@ def eval_all_many(oi: OracleInstance, sols, lams, nthreads):
     n = L.orc_eval_all_many(C.byref(oi.desc), C.c_int32(B), FS, _p(lam_a, _f64p),
                             C.c_int32(nthreads), C.byref(chk))
     return int(n), chk.value
+
+
+REPAIR_OPS = {"FBI": 0, "IBI": 1, "FRI": 2, "IRI": 3}
+
+
+def repair(oi: OracleInstance, sol, unrouted, op: int, lam):
+    """genetic.repair_insert (op 0..3) -> (routes as (depart, arrive, customers), slot_evals)."""
+    L = lib()
+    fl = _Flat(sol)
+    pend = np.ascontiguousarray(list(unrouted) or [0], np.int32)
+    npend = len(unrouted)
+    lam_a = np.ascontiguousarray(lam, np.float64)
+    nc = int(fl.off[-1]) + npend + 1
+    cap_r = len(sol.routes) + npend + 1
+    out_m = C.c_int32(0)
+    off = np.zeros(cap_r + 1, np.int32)
+    cust = np.zeros(nc, np.int32)
+    dep = np.zeros(cap_r, np.int32)
+    arr = np.zeros(cap_r, np.int32)
+    ev = C.c_int64(0)
+    rc = L.orc_repair(C.byref(oi.desc), C.byref(fl.s), _p(pend, _i32p), C.c_int32(npend), C.c_int32(op),
+                      _p(lam_a, _f64p), C.c_int32(cap_r), C.c_int32(nc), C.byref(out_m), _p(off, _i32p),
+                      _p(cust, _i32p), _p(dep, _i32p), _p(arr, _i32p), C.byref(ev))
+    if rc == 1:
+        raise ValueError("unknown insertion operator")
+    if rc:
+        raise RuntimeError(f"oracle repair status {rc}")
+    m = out_m.value
+    return [(int(dep[r]), int(arr[r]), [int(c) for c in cust[off[r]:off[r + 1]]]) for r in range(m)], ev.value
+
+
+def repair_many(oi: OracleInstance, sols, unrouteds, op: int, lams, nthreads):
+    """Independent repairs on nthreads threads; returns total slot evaluations."""
+    L = lib()
+    B = len(sols)
+    flats = [_Flat(s) for s in sols]
+    FS = (FlatSol * B)(*[f.s for f in flats])
+    off = np.zeros(B + 1, np.int32)
+    np.cumsum([len(u) for u in unrouteds], out=off[1:])
+    pend = np.ascontiguousarray([c for u in unrouteds for c in u] or [0], np.int32)
+    lam_a = np.ascontiguousarray(np.asarray(lams, np.float64).reshape(B, 4))
+    ev = np.zeros(B, np.int64)
+    st = np.zeros(B, np.int32)
+    L.orc_repair_many(C.byref(oi.desc), C.c_int32(B), FS, _p(off, _i32p), _p(pend, _i32p), C.c_int32(op),
+                      _p(lam_a, _f64p), C.c_int32(nthreads), _p(ev, _i64p), _p(st, _i32p))
+    if st.any():
+        raise RuntimeError(f"oracle repair_many status {st.max()}")
+    return int(ev.sum())

@@ -63,6 +63,12 @@ struct mdr_pop {
   cudaEvent_t join[2];
   cudaStream_t side[3];          // fork/join branches of the per-operator evaluators
   cudaEvent_t fev[4];
+  // repair scratch (mdr_repair), grown on demand
+  char *rp_pre = nullptr, *rp_suf = nullptr;
+  double *rp_c1 = nullptr, *rp_c2 = nullptr;
+  int *rp_p1 = nullptr, *rp_pend = nullptr, *rp_status = nullptr;
+  long long *rp_stats = nullptr;
+  size_t rp_cap[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 };
 
 template <typename T>
@@ -73,6 +79,17 @@ static int dalloc(std::vector<void *> &owner, T **p, size_t n) {
   if (e != cudaSuccess) return fail(MDR_ERR_CUDA, std::string("cudaMalloc: ") + cudaGetErrorString(e));
   owner.push_back(q);
   *p = reinterpret_cast<T *>(q);
+  return MDR_OK;
+}
+
+template <typename T>
+static int regrow(T **ptr, size_t &cap, size_t need) {
+  if (cap >= need && *ptr) return MDR_OK;
+  if (*ptr) cudaFree(*ptr);
+  *ptr = nullptr;
+  cap = 0;
+  CK(cudaMalloc((void **)ptr, need * sizeof(T)));
+  cap = need;
   return MDR_OK;
 }
 
@@ -278,6 +295,9 @@ void mdr_pop_destroy(mdr_pop *p) {
   cudaEventDestroy(p->join[1]);
   for (int q = 0; q < 3; q++) cudaStreamDestroy(p->side[q]);
   for (int q = 0; q < 4; q++) cudaEventDestroy(p->fev[q]);
+  for (void *q : {(void *)p->rp_pre, (void *)p->rp_suf, (void *)p->rp_c1, (void *)p->rp_c2, (void *)p->rp_p1, (void *)p->rp_pend,
+                  (void *)p->rp_status, (void *)p->rp_stats})
+    if (q) cudaFree(q);
   delete p;
 }
 
@@ -416,7 +436,7 @@ static int enumerate_keys(mdr_pop *p, int b, int op, unsigned long long **d_out,
   CK(cudaGetLastError());
   size_t tb = 0;
   CK(cub::DeviceSelect::If(nullptr, tb, keys, outk, nsel, (int)items, NonZero(), s));
-  void *tst = nullptr;
+  char *tst = nullptr;
   DA(tmp, tst, tb + 1);
   CK(cub::DeviceSelect::If(tst, tb, keys, outk, nsel, (int)items, NonZero(), s));
   int n = 0;
@@ -619,7 +639,7 @@ int mdr_leader_followers(mdr_pop *p, const mdr_cands *cs, const mdr_deltas *d, i
   size_t tb = 0;
   OKI init{~0ull, ~0ull, (long long)n};
   CK(cub::DeviceReduce::Reduce(nullptr, tb, it, dmin, (int)n, OKIMin(), init, s));
-  void *tst = nullptr;
+  char *tst = nullptr;
   TA(tst, tb + 1);
   CK(cub::DeviceReduce::Reduce(tst, tb, it, dmin, (int)n, OKIMin(), init, s));
   OKI hmin;
@@ -743,6 +763,76 @@ int mdr_shuffle_stream(uint32_t *state, int32_t n_items, const uint8_t *items, i
     if (out)
       for (int i = 0; i < n_items; i++) out[(size_t)p * n_items + i] = tmp[i];
   }
+  return MDR_OK;
+}
+
+int mdr_repair(mdr_pop *p, int32_t op, const int32_t *pend_off, const int32_t *pend, mdr_repair_stats *stats,
+               void *stream) {
+  if (!p || !pend_off || (pend_off[p->B] > 0 && !pend)) return fail(MDR_ERR_ARG, "null argument");
+  if (op < 0 || op > 3) return fail(MDR_ERR_ARG, "op must be FBI(0), IBI(1), FRI(2) or IRI(3)");
+  const int B = p->B;
+  cudaStream_t s = (cudaStream_t)stream;
+  CK(cudaSetDevice(p->inst->device));
+  const DevInst &I = p->inst->I;
+  DevPop &P = p->P;
+  // pending lists sorted ascending (repair_insert sorts, genetic.py:198); duplicates rejected
+  std::vector<int> off(B + 1, 0), srt;
+  int Pmax = 0;
+  for (int b = 0; b < B; b++) {
+    const int n = pend_off[b + 1] - pend_off[b];
+    if (n < 0) return fail(MDR_ERR_ARG, "pend_off must be non-decreasing");
+    std::vector<int> v(pend + pend_off[b], pend + pend_off[b + 1]);
+    std::sort(v.begin(), v.end());
+    for (int i = 0; i < n; i++) {
+      if (v[i] < I.ND || v[i] >= I.N) return fail(MDR_ERR_ARG, "pending node is not a customer");
+      if (i && v[i] == v[i - 1]) return fail(MDR_ERR_ARG, "pending customer listed twice");
+    }
+    srt.insert(srt.end(), v.begin(), v.end());
+    off[b + 1] = off[b] + n;
+    Pmax = std::max(Pmax, n);
+  }
+  if (Pmax > 4096) return fail(MDR_ERR_ARG, "more than 4096 pending customers in one individual");
+  const size_t tab = (size_t)P.Bcap * P.J * P.Kp * repair_attr_bytes();  // bytes
+  const size_t cache = (size_t)std::max(B, 1) * std::max(Pmax, 1) * P.J;
+  const size_t pn = (size_t)(B + 1) + srt.size() + 1, nb = (size_t)std::max(B, 1);
+  int rc;
+  if ((rc = regrow(&p->rp_pre, p->rp_cap[0], tab)) || (rc = regrow(&p->rp_suf, p->rp_cap[1], tab)) ||
+      (rc = regrow(&p->rp_c1, p->rp_cap[2], cache)) || (rc = regrow(&p->rp_c2, p->rp_cap[3], cache)) ||
+      (rc = regrow(&p->rp_p1, p->rp_cap[4], cache)) || (rc = regrow(&p->rp_pend, p->rp_cap[5], pn)) ||
+      (rc = regrow(&p->rp_status, p->rp_cap[6], nb)) || (rc = regrow(&p->rp_stats, p->rp_cap[7], 3 * nb)))
+    return rc;
+  int *d_off = p->rp_pend, *d_pend = p->rp_pend + B + 1;
+  CK(cudaMemcpyAsync(d_off, off.data(), sizeof(int) * (B + 1), cudaMemcpyHostToDevice, s));
+  if (!srt.empty()) CK(cudaMemcpyAsync(d_pend, srt.data(), sizeof(int) * srt.size(), cudaMemcpyHostToDevice, s));
+  launch_repair(I, P, B, op, d_off, d_pend, p->rp_pre, p->rp_suf, p->rp_c1, p->rp_c2, p->rp_p1,
+                std::max(Pmax, 1), p->rp_status, p->rp_stats, s);
+  CK(cudaGetLastError());
+  std::vector<int> st(std::max(B, 1));
+  std::vector<long long> ev((size_t)std::max(B, 1) * 3);
+  if (B) {
+    CK(cudaMemcpyAsync(st.data(), p->rp_status, sizeof(int) * B, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(ev.data(), p->rp_stats, sizeof(long long) * 3 * B, cudaMemcpyDeviceToHost, s));
+  }
+  CK(cudaStreamSynchronize(s));
+  int worst = MDR_OK;
+  for (int b = 0; b < B; b++) {
+    if (stats) {
+      stats[b].status = st[b];
+      stats[b].inserted = off[b + 1] - off[b];
+      stats[b].slot_evals = ev[3 * b];
+      stats[b].ref_slot_evals = ev[3 * b + 1];
+      stats[b].need_j = (int)(ev[3 * b + 2] >> 32);
+      stats[b].need_k = (int)(ev[3 * b + 2] & 0xffffffff);
+    }
+    if (st[b] && !worst) worst = st[b];
+  }
+  if (worst == MDR_ERR_ARG) return fail(MDR_ERR_ARG, "pending customer is already routed");
+  if (worst == MDR_ERR_CAPACITY) return fail(MDR_ERR_CAPACITY, "repair needs more routes (J) or a longer route (K)");
+  if (worst) return fail(worst, "repair failed");
+  // the population is left ready for mdr_local_search / mdr_pop_download
+  if (B > 0) launch_rebuild(I, P, B, I.win, s);
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(s));
   return MDR_OK;
 }
 

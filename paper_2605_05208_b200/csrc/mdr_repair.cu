@@ -1,0 +1,431 @@
+// Repair insertion on the device: genetic.repair_insert
+// (genetic.py:174-244) for FBI/IBI/FRI/IRI, batched over the individuals of a
+// population -- one CTA per individual, the whole insertion loop on the device.
+//
+// The reference re-scans every (pending customer x slot) after each insertion.
+// Only the inserted-into route's slots change, so this keeps, per (pending
+// customer q, route r), the route-local scan summary (m1 = first minimal cost,
+// its position, m2 = second-smallest cost of the multiset) and re-scans only
+// the touched route's column.  Folding the per-route summaries in route order,
+//   m1 <  C1: C2 = min(C1, m2), C1 = m1, slot = (r, pos1)
+//   m1 >= C1: C2 = min(C2, m1)
+// gives exactly _best_slot's (slot, c1, c2) over the full scan (strict '<'
+// keeps the first minimum; c2 is the second-smallest value, multiplicity kept).
+//
+// Arithmetic follows the scalar evaluation.concat (evaluation.py:74-94) with
+// Python's max/min (first argument unless the second is strictly larger /
+// smaller); _RouteEval's suffixes are RIGHT folds (genetic.py:87-90).
+#include <cuda_runtime.h>
+
+#include <math_constants.h>
+
+#include "../../include/mdr_sm100.h"
+#include "mdr_kernels.cuh"
+
+namespace mdr {
+
+struct RAt {
+  double dist, load, T, E, L, TW;
+};
+
+__device__ __forceinline__ double py_max(double a, double b) { return b > a ? b : a; }
+__device__ __forceinline__ double py_min(double a, double b) { return b < a ? b : a; }
+
+__device__ __forceinline__ RAt r_single(const DevInst &I, int v) {
+  const double4 nd = I.node[v];
+  RAt a;
+  a.dist = 0.0; a.load = nd.x; a.T = nd.y; a.E = nd.z; a.L = nd.w; a.TW = 0.0;
+  return a;
+}
+
+// concat(a, b) with a.last = x, b.first = y (both non-empty)
+__device__ __forceinline__ RAt r_cat(const DevInst &I, const RAt &a, int x, const RAt &b, int y) {
+  const size_t lk = (size_t)x * I.N + y;
+  const double c = I.dist[lk], t = I.talias ? c : I.time[lk];
+  const double delta = (a.T - a.TW) + t;
+  const double wait = py_max((b.E - delta) - a.L, 0.0);
+  const double warp = py_max((a.E + delta) - b.L, 0.0);
+  RAt o;
+  o.dist = (a.dist + c) + b.dist;
+  o.load = a.load + b.load;
+  o.T = ((a.T + b.T) + t) + wait;
+  o.E = py_max(b.E - delta, a.E) - wait;
+  o.L = py_min(b.L - delta, a.L) + warp;
+  o.TW = (a.TW + b.TW) + warp;
+  return o;
+}
+
+// _route_cost_terms (genetic.py:100-106)
+__device__ __forceinline__ void r_terms(const DevInst &I, const RAt &a, double o[4]) {
+  o[0] = a.dist;
+  o[1] = I.win ? I.gamma * a.TW : 0.0;
+  o[2] = (I.theta * py_max(a.load - I.Q, 0.0)) / I.Q;
+  o[3] = I.d_on ? (I.theta * py_max(a.T - I.Dmax, 0.0)) / I.Dmax : 0.0;
+}
+
+// _attr_feasible (genetic.py:109-116)
+__device__ __forceinline__ bool r_feasible(const DevInst &I, const RAt &a) {
+  if (a.load > I.Q + 1e-9) return false;
+  if (I.d_on && a.T > I.Dmax + 1e-9) return false;
+  if (I.win && a.TW > 1e-9) return false;
+  return true;
+}
+
+struct RepView {
+  int *seq;         // [J][Kp] this individual's rows
+  int4 *rm;         // [J]
+  RAt *pre, *suf;   // [J][Kp]
+  double *c1, *c2;  // [Pcap][J]
+  int *p1;          // [Pcap][J]
+  int Kp, J, K, Pcap;
+};
+
+__device__ __forceinline__ int r_len(const DevInst &I, int k) { return k + (I.open ? 1 : 2); }
+
+// pref (left fold) and suf (right fold) of route r; lane 0 / lane 1 of a warp
+__device__ void r_rebuild(const DevInst &I, const RepView &V, int r, int lane) {
+  const int4 mt = V.rm[r];
+  const int n = r_len(I, mt.x);
+  const int *sq = V.seq + (size_t)r * V.Kp;
+  RAt *pre = V.pre + (size_t)r * V.Kp, *suf = V.suf + (size_t)r * V.Kp;
+  if (lane == 0) {
+    RAt a = r_single(I, sq[0]);
+    pre[0] = a;
+    for (int i = 1; i < n; i++) {
+      a = r_cat(I, a, sq[i - 1], r_single(I, sq[i]), sq[i]);
+      pre[i] = a;
+    }
+  } else if (lane == 1) {
+    RAt a = r_single(I, sq[n - 1]);
+    suf[n - 1] = a;
+    for (int i = n - 2; i >= 0; i--) {
+      a = r_cat(I, r_single(I, sq[i]), sq[i], a, sq[i + 1]);
+      suf[i] = a;
+    }
+  }
+}
+
+// route-local scan of every slot of route r for `node` (_best_slot restricted to r)
+__device__ void r_scan(const DevInst &I, const RepView &V, int r, int node, bool feas_only, const double lam[4],
+                       double &m1, int &pos1, double &m2) {
+  const int4 mt = V.rm[r];
+  const int k = mt.x, n = r_len(I, k);
+  const int *sq = V.seq + (size_t)r * V.Kp;
+  const RAt *pre = V.pre + (size_t)r * V.Kp, *suf = V.suf + (size_t)r * V.Kp;
+  double o[4];
+  r_terms(I, pre[n - 1], o);
+  const RAt sn = r_single(I, node);
+  m1 = CUDART_INF;
+  m2 = CUDART_INF;
+  pos1 = -1;
+  for (int pos = 0; pos <= k; pos++) {
+    RAt a = r_cat(I, pre[pos], sq[pos], sn, node);
+    if (pos + 1 < n) a = r_cat(I, a, node, suf[pos + 1], sq[pos + 1]);
+    double x[4];
+    r_terms(I, a, x);
+    const double dd = x[0] - o[0];
+    double cost;
+    if (feas_only) {
+      if (!r_feasible(I, a)) continue;
+      cost = dd;
+    } else {
+      cost = ((dd + lam[0] * (x[1] - o[1])) + lam[1] * (x[2] - o[2])) + lam[2] * (x[3] - o[3]);
+    }
+    if (cost < m1) {
+      m2 = m1;
+      m1 = cost;
+      pos1 = pos;
+    } else if (cost < m2) {
+      m2 = cost;
+    }
+  }
+}
+
+__device__ __forceinline__ unsigned long long ord_d(double x) {  // order-preserving, -0 == +0
+  unsigned long long u = (unsigned long long)__double_as_longlong(x + 0.0);
+  return (u >> 63) ? ~u : (u | 0x8000000000000000ull);
+}
+
+constexpr int RP_THREADS = 256;
+constexpr int RP_MAXND = 256;
+
+__global__ void __launch_bounds__(RP_THREADS) k_repair(DevInst I, DevPop P, int B, int op, const int *pend_off,
+                                                       const int *pend, RAt *g_pre, RAt *g_suf, double *g_c1,
+                                                       double *g_c2, int *g_p1, int Pcap, int *status,
+                                                       long long *stats) {
+  const int b = blockIdx.x;
+  if (b >= B) return;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = RP_THREADS / 32;
+  RepView V;
+  V.Kp = P.Kp; V.J = P.J; V.K = P.K; V.Pcap = Pcap;
+  V.seq = P.seq + (size_t)b * P.J * P.Kp;
+  V.rm = P.rmeta + (size_t)b * P.J;
+  V.pre = g_pre + (size_t)b * P.J * P.Kp;
+  V.suf = g_suf + (size_t)b * P.J * P.Kp;
+  V.c1 = g_c1 + (size_t)b * Pcap * P.J;
+  V.c2 = g_c2 + (size_t)b * Pcap * P.J;
+  V.p1 = g_p1 + (size_t)b * Pcap * P.J;
+  const bool feas_only = op == 0 || op == 2, regret = op == 2 || op == 3;
+  const int q0 = pend_off[b], P0 = pend_off[b + 1] - q0;
+  const int *pd = pend + q0;
+  const int *LOC = P.loc + (size_t)b * P.N;
+
+  __shared__ int s_m, s_alive, s_err, s_needj, s_needk, s_touch;
+  __shared__ int s_cls, s_q;
+  __shared__ unsigned long long s_key;
+  __shared__ int s_cnt[RP_MAXND];
+  __shared__ unsigned char s_dead[4096];
+  __shared__ unsigned long long s_ev_dev;
+  double lam[4];
+  for (int i = 0; i < 4; i++) lam[i] = P.lam[b * 4 + i];
+
+  if (tid == 0) {
+    s_m = P.m[b];
+    s_alive = P0;
+    s_err = 0;
+    s_needj = s_needk = 0;
+    s_ev_dev = 0;
+  }
+  for (int q = tid; q < P0; q += RP_THREADS) {
+    s_dead[q] = 0;
+    const int v = pd[q];
+    if (v < I.ND || v >= I.N || LOC[v] >= 0 || (q > 0 && pd[q - 1] >= v)) atomicExch(&s_err, MDR_ERR_ARG);
+  }
+  __syncthreads();
+  if (s_err) {
+    if (tid == 0) status[b] = s_err;
+    return;
+  }
+  // open_route (genetic.py:148-166): depot of minimal (not free, cost, d)
+  auto open_route = [&](int node) -> int {  // thread 0 only; returns the new route or -1
+    const int m = s_m;
+    if (m >= V.J) { s_needj = m + 1; return -1; }
+    int best = -1, bnf = 0;
+    double bcost = 0.0;
+    for (int d = 0; d < I.ND; d++) {
+      const double cost = I.dist[(size_t)d * I.N + node] + (I.open ? 0.0 : I.dist[(size_t)node * I.N + d]);
+      const int nf = !(!I.nv_on || (double)s_cnt[d] < I.NV);
+      if (best < 0 || nf < bnf || (nf == bnf && cost < bcost)) { best = d; bnf = nf; bcost = cost; }
+    }
+    int *sq = V.seq + (size_t)m * V.Kp;
+    sq[0] = best;
+    sq[1] = node;
+    if (!I.open) sq[2] = best;
+    V.rm[m] = make_int4(1, best, best, 0);
+    s_cnt[best]++;
+    s_m = m + 1;
+    return m;
+  };
+  auto count_depots = [&]() {
+    for (int d = tid; d < I.ND; d += RP_THREADS) s_cnt[d] = 0;
+    __syncthreads();
+    for (int r = tid; r < s_m; r += RP_THREADS) {
+      const int4 mt = V.rm[r];
+      if (mt.x > 0) atomicAdd(&s_cnt[mt.y], 1);
+    }
+    __syncthreads();
+  };
+  count_depots();
+  if (!feas_only && s_m == 0 && P0 > 0) {  // degenerate guard of the relaxed modes (genetic.py:211-212)
+    if (tid == 0) {
+      if (open_route(pd[0]) < 0) s_err = MDR_ERR_CAPACITY;
+      s_dead[0] = 1;
+      s_alive = P0 - 1;
+    }
+    __syncthreads();
+  }
+  // prefix/suffix of every route: one warp per route (lane 0 prefix, lane 1 suffix)
+  for (int r = wid; r < s_m; r += nw) r_rebuild(I, V, r, lane);
+  __syncthreads();
+  // all columns
+  {
+    const int m = s_m;
+    for (long long it = tid; it < (long long)P0 * m; it += RP_THREADS) {
+      const int q = (int)(it / m), r = (int)(it - (long long)q * m);
+      if (s_dead[q]) continue;
+      double m1, m2;
+      int pos1;
+      r_scan(I, V, r, pd[q], feas_only, lam, m1, pos1, m2);
+      V.c1[(size_t)q * V.J + r] = m1;
+      V.c2[(size_t)q * V.J + r] = m2;
+      V.p1[(size_t)q * V.J + r] = pos1;
+    }
+  }
+  __syncthreads();
+  long long ev_dev = 0, ev_ref = 0;
+  while (s_alive > 0 && !s_err) {
+    const int m = s_m;
+    if (tid == 0) {
+      s_cls = regret ? -1 : 0;
+      s_key = regret ? 0ull : ~0ull;
+      s_q = 0x7fffffff;
+      int slots = 0;
+      for (int r = 0; r < m; r++) slots += V.rm[r].x + 1;
+      ev_ref += (long long)s_alive * slots;
+    }
+    __syncthreads();
+    // (a) per pending customer: fold the route summaries -> (slot, C1, C2) and its key
+    for (int q = tid; q < P0; q += RP_THREADS) {
+      if (s_dead[q]) continue;
+      double C1 = CUDART_INF, C2 = CUDART_INF;
+      bool found = false;
+      const double *c1 = V.c1 + (size_t)q * V.J, *c2 = V.c2 + (size_t)q * V.J;
+      const int *p1 = V.p1 + (size_t)q * V.J;
+      for (int r = 0; r < m; r++) {
+        const double a1 = c1[r];
+        if (a1 < C1) {
+          const double a2 = c2[r];
+          C2 = a2 < C1 ? a2 : C1;
+          C1 = a1;
+          found = p1[r] >= 0 || found;
+        } else if (a1 < C2) {
+          C2 = a1;
+        }
+      }
+      if (regret) {
+        int cls;
+        double val;
+        if (!found) { cls = 2; val = 0.0; }
+        else if (C2 == CUDART_INF) { cls = 1; val = 0.0; }
+        else { cls = 0; val = C2 - C1; }
+        (void)val;
+        atomicMax(&s_cls, cls);
+      } else if (found) {
+        atomicMin(&s_key, ord_d(C1));
+      }
+    }
+    __syncthreads();
+    // (b) the chosen customer: best = minimal C1, then smallest id; regret = maximal
+    // (cls, C2 - C1), then smallest id (keys (cls, val, -node), genetic.py:214-231)
+    if (regret) {
+      for (int q = tid; q < P0; q += RP_THREADS) {
+        if (s_dead[q]) continue;
+        // recompute this customer's class/value (cheap) to compare against the maxima
+        double C1 = CUDART_INF, C2 = CUDART_INF;
+        bool found = false;
+        const double *c1 = V.c1 + (size_t)q * V.J, *c2 = V.c2 + (size_t)q * V.J;
+        const int *p1 = V.p1 + (size_t)q * V.J;
+        for (int r = 0; r < m; r++) {
+          const double a1 = c1[r];
+          if (a1 < C1) {
+            const double a2 = c2[r];
+            C2 = a2 < C1 ? a2 : C1;
+            C1 = a1;
+            found = p1[r] >= 0 || found;
+          } else if (a1 < C2) {
+            C2 = a1;
+          }
+        }
+        const int cls = !found ? 2 : (C2 == CUDART_INF ? 1 : 0);
+        if (cls == s_cls) atomicMax(&s_key, ord_d(cls == 0 ? C2 - C1 : 0.0));
+      }
+      __syncthreads();
+    }
+    for (int q = tid; q < P0; q += RP_THREADS) {
+      if (s_dead[q]) continue;
+      double C1 = CUDART_INF, C2 = CUDART_INF;
+      bool found = false;
+      int R = -1, POS = -1;
+      const double *c1 = V.c1 + (size_t)q * V.J, *c2 = V.c2 + (size_t)q * V.J;
+      const int *p1 = V.p1 + (size_t)q * V.J;
+      for (int r = 0; r < m; r++) {
+        const double a1 = c1[r];
+        if (a1 < C1) {
+          const double a2 = c2[r];
+          C2 = a2 < C1 ? a2 : C1;
+          C1 = a1;
+          R = r;
+          POS = p1[r];
+          found = true;
+        } else if (a1 < C2) {
+          C2 = a1;
+        }
+      }
+      bool match;
+      if (regret) {
+        const int cls = !found ? 2 : (C2 == CUDART_INF ? 1 : 0);
+        match = cls == s_cls && ord_d(cls == 0 ? C2 - C1 : 0.0) == s_key;
+      } else {
+        match = found && ord_d(C1) == s_key;
+      }
+      if (match) atomicMin(&s_q, q);
+    }
+    __syncthreads();
+    if (tid == 0) {
+      int q = s_q;
+      int R = -1, POS = -1;
+      if (q == 0x7fffffff) {  // best modes: no customer has a slot -> first pending, new route
+        q = 0;
+        while (s_dead[q]) q++;
+      } else {
+        double C1 = CUDART_INF;
+        const double *c1 = V.c1 + (size_t)q * V.J;
+        const int *p1 = V.p1 + (size_t)q * V.J;
+        for (int r = 0; r < m; r++)
+          if (c1[r] < C1) { C1 = c1[r]; R = r; POS = p1[r]; }
+        if (R >= 0 && POS < 0) R = -1;
+      }
+      s_dead[q] = 1;
+      s_alive--;
+      const int node = pd[q];
+      if (R < 0) {
+        const int r = open_route(node);
+        if (r < 0) s_err = MDR_ERR_CAPACITY;
+        s_touch = r;
+      } else {
+        int4 mt = V.rm[R];
+        if (mt.x >= V.K) {
+          s_needk = mt.x + 1;
+          s_err = MDR_ERR_CAPACITY;
+        } else {
+          int *sq = V.seq + (size_t)R * V.Kp;
+          const int n = r_len(I, mt.x);
+          for (int i = n; i > POS + 1; i--) sq[i] = sq[i - 1];  // shifts the arrive depot too
+          sq[POS + 1] = node;
+          if (mt.x == 0) s_cnt[mt.y]++;
+          mt.x += 1;
+          V.rm[R] = mt;
+        }
+        s_touch = R;
+      }
+    }
+    __syncthreads();
+    if (s_err) break;
+    const int rt = s_touch;
+    if (wid == 0) r_rebuild(I, V, rt, lane);
+    __syncthreads();
+    // (e) the touched route's column for every pending customer
+    for (int q = tid; q < P0; q += RP_THREADS) {
+      if (s_dead[q]) continue;
+      double m1, m2;
+      int pos1;
+      r_scan(I, V, rt, pd[q], feas_only, lam, m1, pos1, m2);
+      V.c1[(size_t)q * V.J + rt] = m1;
+      V.c2[(size_t)q * V.J + rt] = m2;
+      V.p1[(size_t)q * V.J + rt] = pos1;
+      ev_dev += V.rm[rt].x + 1;
+    }
+    __syncthreads();
+  }
+  atomicAdd(&s_ev_dev, (unsigned long long)ev_dev);
+  __syncthreads();
+  if (tid == 0) {
+    P.m[b] = s_m;
+    status[b] = s_err;
+    stats[3 * b + 0] = (long long)s_ev_dev;
+    stats[3 * b + 1] = ev_ref;
+    stats[3 * b + 2] = ((long long)s_needj << 32) | (unsigned)s_needk;
+  }
+}
+
+void launch_repair(const DevInst &I, const DevPop &P, int B, int op, const int *pend_off, const int *pend,
+                   void *pre, void *suf, double *c1, double *c2, int *p1, int Pcap, int *status, long long *stats,
+                   cudaStream_t s) {
+  if (B <= 0) return;
+  k_repair<<<B, RP_THREADS, 0, s>>>(I, P, B, op, pend_off, pend, (RAt *)pre, (RAt *)suf, c1, c2, p1, Pcap, status,
+                                    stats);
+}
+
+size_t repair_attr_bytes() { return sizeof(RAt); }
+
+}  // namespace mdr

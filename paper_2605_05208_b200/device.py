@@ -189,6 +189,30 @@ class Population:
         check(rc, "mdr_local_search")
         return stats
 
+    def repair(self, op: int, unrouteds, stream=None):
+        """mdr_repair on the uploaded individuals; the population is left holding the
+        repaired solutions.  Returns per-individual stats dicts."""
+        B = self.B
+        off = np.zeros(B + 1, np.int32)
+        np.cumsum([len(u) for u in unrouteds], out=off[1:])
+        pend = np.ascontiguousarray([int(c) for u in unrouteds for c in u] or [0], np.int32)
+        st = (_lib.RepairStats * max(B, 1))()
+        s = stream if stream is not None else _cur_stream(self.dinst.device)
+        rc = _lib.lib().mdr_repair(self.handle, int(op), ptr(off, i32p), ptr(pend, i32p), st, s)
+        stats = [dict(status=x.status, inserted=x.inserted, slot_evals=x.slot_evals,
+                      ref_slot_evals=x.ref_slot_evals) for x in st[:B]]
+        if rc == _lib.MDR_ERR_CAPACITY:
+            need = dict(J=max(x.need_j for x in st[:B]), K=max(x.need_k for x in st[:B]))
+            try:
+                check(rc, "mdr_repair")
+            except CapacityError as e:
+                e.need = need
+                raise
+        check(rc, "mdr_repair")
+        self.n_cust += int(off[-1])  # download buffers hold the inserted customers too
+        self.h2d_bytes_repair = int(off.nbytes + pend.nbytes)
+        return stats
+
     def set_profiling(self, on: bool):
         check(_lib.lib().mdr_set_profiling(self.handle, int(on)))
 
