@@ -142,6 +142,73 @@ def load_traffic():
         return None, None
 
 
+def repair_workload(sols, ids, frac=0.2):
+    """GA-offspring-like repair inputs: individual i = its start with a seeded
+    `frac` of its customers removed (emptied routes kept)."""
+    out, pend = [], []
+    for s, i in zip(sols, ids):
+        rng = random.Random(7000 + i)
+        c = s.clone()
+        cust = [x for r in c.routes for x in r.customers]
+        removed = set(rng.sample(cust, int(len(cust) * frac)))
+        for r in c.routes:
+            r.customers = [x for x in r.customers if x not in removed]
+        out.append(c)
+        pend.append(sorted(removed))
+    return out, pend
+
+
+def bench_repair(name, inst, consts, sols, ids, device, steps, cpu=True, op=3):
+    """batched repair insertion (IRI by default) of the
+    population; slot evaluations counted as the reference's full re-scan does."""
+    import torch
+    from paper_2605_05208_b200.device import Population
+    from paper_2605_05208_b200.genetic import InsertionOperator, repair_population
+    from paper_2605_05208_b200.session import session_for
+    rs, pend = repair_workload(sols, ids)
+    lams = [[1.0] * 4] * len(rs)
+    sess = session_for(inst, consts, None, device)
+    J, K = Population.caps_for(rs, inst)
+    pop = Population(sess.dinst, len(rs), min(4094, J + max(len(u) for u in pend)), min(500, K + 32), 1 << 10)
+    dev_ms, ref_ev, dev_ev = [], 0, 0
+    for k in range(steps + 1):
+        pop.upload(rs, lams)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        st = pop.repair(op, pend)
+        torch.cuda.synchronize()
+        if k:  # first call: warm-up (scratch allocation)
+            dev_ms.append(1000 * (time.perf_counter() - t0))
+            ref_ev += sum(x["ref_slot_evals"] for x in st)
+            dev_ev += sum(x["slot_evals"] for x in st)
+    ms = sum(dev_ms) / len(dev_ms)
+    e2e = []
+    for k in range(2):  # first call allocates the session's population (warm-up)
+        work = [s.clone() for s in rs]
+        t0 = time.perf_counter()
+        repair_population(work, pend, InsertionOperator(op), inst, consts,
+                          [PenaltyState() for _ in rs], device=device)
+        e2e.append(1000 * (time.perf_counter() - t0))
+    e2e_ms = e2e[-1]
+    line = {"op": InsertionOperator(op).name, "individuals": len(rs),
+            "pending_per_individual": sum(len(u) for u in pend) / len(pend),
+            "device_call_ms": ms, "e2e_ms": e2e_ms, "repairs_per_s": len(rs) / (ms / 1000.0),
+            "ref_slot_evals_per_s": ref_ev / steps / (ms / 1000.0),
+            "device_slot_evals_per_repair": dev_ev / steps / len(rs),
+            "ref_slot_evals_per_repair": ref_ev / steps / len(rs)}
+    if cpu:
+        from oracle import oracle as O
+        threads = os.cpu_count() or 1
+        k = min(len(rs), threads)
+        oi = O.OracleInstance(inst, consts, build(inst, NeighborConfig(1), consts))
+        t0 = time.perf_counter()
+        ev = O.repair_many(oi, rs[:k], pend[:k], op, [[1.0] * 4] * k, threads)
+        dt = time.perf_counter() - t0
+        line["cpu_baseline"] = {"repairs_per_s": k / dt, "ref_slot_evals_per_s": ev / dt, "cores": threads,
+                                "kind": "port", "sample": f"{k} repairs on {threads} threads, {dt:.1f} s"}
+    return line
+
+
 def cpu_baseline(name, inst, consts, nbr, sols, depth, seconds=20.0):
     """Oracle (C port of the reference) descents on all host threads, bounded sample."""
     from oracle import oracle as O
@@ -213,6 +280,7 @@ def main():
     ap.add_argument("--depth", type=int, default=500)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-repair", action="store_true")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -338,6 +406,11 @@ def main():
                 "identical": bool(np.array_equal(nb_dev.lists, nb_host.lists)),
                 "nodes": inst.n_nodes, "theta": spec.theta}
 
+    repair_line = None
+    if not args.no_repair and world == 1:
+        repair_line = bench_repair(name, inst, consts, sols, ids, local, max(1, args.steps),
+                                   cpu=not args.no_cpu_baseline)
+
     # e2e: through the public API with host Solution objects, H2D + D2H inside
     e2e = None
     if not args.no_e2e:
@@ -411,6 +484,7 @@ def main():
             "e2e": e2e,
             "gpu_launches": int(launches),
             "neighbor_build": nbr_line,
+            "repair": repair_line,
             "clocks": clocks,
             "profile": {"rounds_per_step": rounds / args.steps, "plan_ms": tm["plan_ms"], "eval_ms": tm["eval_ms"],
                         "geval_ms": tm["geval_ms"],

@@ -95,7 +95,10 @@ def repair_population(sols, unrouteds, op, inst, consts, penalties, device: int 
         if need:
             J = min(4094, max(J * 2, need["J"] + 16))
             K = min(500, max(K * 2, need["K"] + 16))
-        pop = Population(sess.dinst, max(len(sols), 1), J, K, 1 << 10)
+        pop = getattr(sess, "_repair_pop", None)  # reused across calls while the caps fit
+        if pop is None or pop.B_cap < len(sols) or pop.J_cap < J or pop.K_cap < K:
+            sess._repair_pop = None
+            pop = sess._repair_pop = Population(sess.dinst, max(len(sols), 1), J, K, 1 << 10)
         pop.upload(sols, [p.lam for p in penalties])
         try:
             stats = pop.repair(int(op), unrouteds)
