@@ -17,6 +17,8 @@ from .moves import (ALL_OPS, MODE_ARRIVE, MODE_BOTH, MODE_DEPART, CandidateSet, 
 from .batch import DeltaArrays, SolutionCache, evaluate_candidates, leader_and_followers
 from .localsearch import (DeviceSearch, SearchConfig, apply_moves, enabled_operators, evaluate_batch,
                           local_search, local_search_population, select_moves)
+from .genetic import InsertionOperator, repair_insert, repair_population
+from .formats import ParseError, parse_instance, read_solution, write_solution
 
 __all__ = [
     "INF", "Instance", "Node", "Route", "Solution", "Variant", "LAMBDA_MAX", "LAMBDA_MIN", "PenaltyState",
@@ -25,4 +27,6 @@ __all__ = [
     "enumerate_candidates", "move_plan", "DeltaArrays", "SolutionCache", "evaluate_candidates",
     "leader_and_followers", "DeviceSearch", "SearchConfig", "apply_moves", "enabled_operators",
     "evaluate_batch", "local_search", "local_search_population", "select_moves",
+    "InsertionOperator", "repair_insert", "repair_population",
+    "ParseError", "parse_instance", "read_solution", "write_solution",
 ]
