@@ -68,7 +68,9 @@ struct mdr_pop {
   double *rp_c1 = nullptr, *rp_c2 = nullptr;
   int *rp_p1 = nullptr, *rp_pend = nullptr, *rp_status = nullptr;
   long long *rp_stats = nullptr;
-  size_t rp_cap[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  double *rp_fold = nullptr;
+  int *rp_foldi = nullptr;
+  size_t rp_cap[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
 };
 
 template <typename T>
@@ -296,7 +298,7 @@ void mdr_pop_destroy(mdr_pop *p) {
   for (int q = 0; q < 3; q++) cudaStreamDestroy(p->side[q]);
   for (int q = 0; q < 4; q++) cudaEventDestroy(p->fev[q]);
   for (void *q : {(void *)p->rp_pre, (void *)p->rp_suf, (void *)p->rp_c1, (void *)p->rp_c2, (void *)p->rp_p1, (void *)p->rp_pend,
-                  (void *)p->rp_status, (void *)p->rp_stats})
+                  (void *)p->rp_status, (void *)p->rp_stats, (void *)p->rp_fold, (void *)p->rp_foldi})
     if (q) cudaFree(q);
   delete p;
 }
@@ -799,13 +801,15 @@ int mdr_repair(mdr_pop *p, int32_t op, const int32_t *pend_off, const int32_t *p
   if ((rc = regrow(&p->rp_pre, p->rp_cap[0], tab)) || (rc = regrow(&p->rp_suf, p->rp_cap[1], tab)) ||
       (rc = regrow(&p->rp_c1, p->rp_cap[2], cache)) || (rc = regrow(&p->rp_c2, p->rp_cap[3], cache)) ||
       (rc = regrow(&p->rp_p1, p->rp_cap[4], cache)) || (rc = regrow(&p->rp_pend, p->rp_cap[5], pn)) ||
-      (rc = regrow(&p->rp_status, p->rp_cap[6], nb)) || (rc = regrow(&p->rp_stats, p->rp_cap[7], 3 * nb)))
+      (rc = regrow(&p->rp_status, p->rp_cap[6], nb)) || (rc = regrow(&p->rp_stats, p->rp_cap[7], 3 * nb)) ||
+      (rc = regrow(&p->rp_fold, p->rp_cap[8], nb * std::max(Pmax, 1) * 2)) ||
+      (rc = regrow(&p->rp_foldi, p->rp_cap[9], nb * std::max(Pmax, 1) * 3)))
     return rc;
   int *d_off = p->rp_pend, *d_pend = p->rp_pend + B + 1;
   CK(cudaMemcpyAsync(d_off, off.data(), sizeof(int) * (B + 1), cudaMemcpyHostToDevice, s));
   if (!srt.empty()) CK(cudaMemcpyAsync(d_pend, srt.data(), sizeof(int) * srt.size(), cudaMemcpyHostToDevice, s));
-  launch_repair(I, P, B, op, d_off, d_pend, p->rp_pre, p->rp_suf, p->rp_c1, p->rp_c2, p->rp_p1,
-                std::max(Pmax, 1), p->rp_status, p->rp_stats, s);
+  launch_repair(I, P, B, op, d_off, d_pend, p->rp_pre, p->rp_suf, p->rp_c1, p->rp_c2, p->rp_p1, p->rp_fold,
+                p->rp_foldi, std::max(Pmax, 1), p->rp_status, p->rp_stats, s);
   CK(cudaGetLastError());
   std::vector<int> st(std::max(B, 1));
   std::vector<long long> ev((size_t)std::max(B, 1) * 3);

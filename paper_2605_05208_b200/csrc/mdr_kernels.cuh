@@ -17,8 +17,8 @@ struct MatDeltas {
 
 void launch_rebuild(const DevInst &I, const DevPop &P, int B, bool win, cudaStream_t s);
 void launch_repair(const DevInst &I, const DevPop &P, int B, int op, const int *pend_off, const int *pend,
-                   void *pre, void *suf, double *c1, double *c2, int *p1, int Pcap, int *status, long long *stats,
-                   cudaStream_t s);
+                   void *pre, void *suf, double *c1, double *c2, int *p1, double *fold, int *foldi, int Pcap,
+                   int *status, long long *stats, cudaStream_t s);
 size_t repair_attr_bytes();
 void launch_plan(const DevInst &I, const DevPop &P, const LsParams &L, cudaStream_t s);
 void launch_eval(const DevInst &I, const DevPop &P, const LsParams &L, int grid, bool win, cudaStream_t s,

@@ -77,8 +77,38 @@ struct RepView {
   RAt *pre, *suf;   // [J][Kp]
   double *c1, *c2;  // [Pcap][J]
   int *p1;          // [Pcap][J]
+  double *fC1, *fC2;  // [Pcap] per-customer fold over all routes
+  int *fR1, *fP1, *fR2;
   int Kp, J, K, Pcap;
 };
+
+// fold the per-route summaries of customer q in route order (see the header)
+__device__ void r_fold(const RepView &V, int q, int m) {
+  double C1 = CUDART_INF, C2 = CUDART_INF;
+  int R1 = -1, P1 = -1, R2 = -1;
+  const double *c1 = V.c1 + (size_t)q * V.J, *c2 = V.c2 + (size_t)q * V.J;
+  const int *p1 = V.p1 + (size_t)q * V.J;
+  for (int r = 0; r < m; r++) {
+    const double a1 = c1[r];
+    if (a1 < C1) {
+      const double a2 = c2[r];
+      if (a2 < C1) { C2 = a2; R2 = r; }
+      else { C2 = C1; R2 = R1; }
+      C1 = a1; R1 = r; P1 = p1[r];
+    } else if (a1 < C2) {
+      C2 = a1; R2 = r;
+    }
+  }
+  V.fC1[q] = C1; V.fC2[q] = C2; V.fR1[q] = R1; V.fP1[q] = P1; V.fR2[q] = R2;
+}
+
+// regret key class: 2 no slot, 1 a single slot value, 0 otherwise (genetic.py:218-223)
+__device__ __forceinline__ int r_class(const RepView &V, int q) {
+  return V.fR1[q] < 0 ? 2 : (V.fC2[q] == CUDART_INF ? 1 : 0);
+}
+__device__ __forceinline__ double r_regret(const RepView &V, int q) {
+  return r_class(V, q) == 0 ? V.fC2[q] - V.fC1[q] : 0.0;
+}
 
 __device__ __forceinline__ int r_len(const DevInst &I, int k) { return k + (I.open ? 1 : 2); }
 
@@ -151,8 +181,8 @@ constexpr int RP_MAXND = 256;
 
 __global__ void __launch_bounds__(RP_THREADS) k_repair(DevInst I, DevPop P, int B, int op, const int *pend_off,
                                                        const int *pend, RAt *g_pre, RAt *g_suf, double *g_c1,
-                                                       double *g_c2, int *g_p1, int Pcap, int *status,
-                                                       long long *stats) {
+                                                       double *g_c2, int *g_p1, double *g_fold, int *g_foldi,
+                                                       int Pcap, int *status, long long *stats) {
   const int b = blockIdx.x;
   if (b >= B) return;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = RP_THREADS / 32;
@@ -165,12 +195,17 @@ __global__ void __launch_bounds__(RP_THREADS) k_repair(DevInst I, DevPop P, int 
   V.c1 = g_c1 + (size_t)b * Pcap * P.J;
   V.c2 = g_c2 + (size_t)b * Pcap * P.J;
   V.p1 = g_p1 + (size_t)b * Pcap * P.J;
+  V.fC1 = g_fold + (size_t)b * Pcap * 2;
+  V.fC2 = V.fC1 + Pcap;
+  V.fR1 = g_foldi + (size_t)b * Pcap * 3;
+  V.fP1 = V.fR1 + Pcap;
+  V.fR2 = V.fP1 + Pcap;
   const bool feas_only = op == 0 || op == 2, regret = op == 2 || op == 3;
   const int q0 = pend_off[b], P0 = pend_off[b + 1] - q0;
   const int *pd = pend + q0;
   const int *LOC = P.loc + (size_t)b * P.N;
 
-  __shared__ int s_m, s_alive, s_err, s_needj, s_needk, s_touch;
+  __shared__ int s_m, s_alive, s_err, s_needj, s_needk, s_touch, s_slots;
   __shared__ int s_cls, s_q;
   __shared__ unsigned long long s_key;
   __shared__ int s_cnt[RP_MAXND];
@@ -252,103 +287,42 @@ __global__ void __launch_bounds__(RP_THREADS) k_repair(DevInst I, DevPop P, int 
     }
   }
   __syncthreads();
+  // per-customer fold of the route summaries (the state of _best_slot after the
+  // whole scan): C1 at (R1, POS1), C2 from route R2 (-1: no second value)
+  for (int q = tid; q < P0; q += RP_THREADS)
+    if (!s_dead[q]) r_fold(V, q, s_m);
+  if (tid == 0) {
+    int slots = 0;
+    for (int r = 0; r < s_m; r++) slots += V.rm[r].x + 1;
+    s_slots = slots;
+  }
+  __syncthreads();
   long long ev_dev = 0, ev_ref = 0;
   while (s_alive > 0 && !s_err) {
-    const int m = s_m;
     if (tid == 0) {
       s_cls = regret ? -1 : 0;
       s_key = regret ? 0ull : ~0ull;
       s_q = 0x7fffffff;
-      int slots = 0;
-      for (int r = 0; r < m; r++) slots += V.rm[r].x + 1;
-      ev_ref += (long long)s_alive * slots;
+      ev_ref += (long long)s_alive * s_slots;
     }
     __syncthreads();
-    // (a) per pending customer: fold the route summaries -> (slot, C1, C2) and its key
-    for (int q = tid; q < P0; q += RP_THREADS) {
-      if (s_dead[q]) continue;
-      double C1 = CUDART_INF, C2 = CUDART_INF;
-      bool found = false;
-      const double *c1 = V.c1 + (size_t)q * V.J, *c2 = V.c2 + (size_t)q * V.J;
-      const int *p1 = V.p1 + (size_t)q * V.J;
-      for (int r = 0; r < m; r++) {
-        const double a1 = c1[r];
-        if (a1 < C1) {
-          const double a2 = c2[r];
-          C2 = a2 < C1 ? a2 : C1;
-          C1 = a1;
-          found = p1[r] >= 0 || found;
-        } else if (a1 < C2) {
-          C2 = a1;
-        }
-      }
-      if (regret) {
-        int cls;
-        double val;
-        if (!found) { cls = 2; val = 0.0; }
-        else if (C2 == CUDART_INF) { cls = 1; val = 0.0; }
-        else { cls = 0; val = C2 - C1; }
-        (void)val;
-        atomicMax(&s_cls, cls);
-      } else if (found) {
-        atomicMin(&s_key, ord_d(C1));
-      }
-    }
-    __syncthreads();
-    // (b) the chosen customer: best = minimal C1, then smallest id; regret = maximal
-    // (cls, C2 - C1), then smallest id (keys (cls, val, -node), genetic.py:214-231)
+    // (a)/(b) the chosen customer: best = minimal C1, then smallest id; regret =
+    // maximal (class, C2 - C1), then smallest id (keys (cls, val, -node), genetic.py:214-231)
     if (regret) {
-      for (int q = tid; q < P0; q += RP_THREADS) {
-        if (s_dead[q]) continue;
-        // recompute this customer's class/value (cheap) to compare against the maxima
-        double C1 = CUDART_INF, C2 = CUDART_INF;
-        bool found = false;
-        const double *c1 = V.c1 + (size_t)q * V.J, *c2 = V.c2 + (size_t)q * V.J;
-        const int *p1 = V.p1 + (size_t)q * V.J;
-        for (int r = 0; r < m; r++) {
-          const double a1 = c1[r];
-          if (a1 < C1) {
-            const double a2 = c2[r];
-            C2 = a2 < C1 ? a2 : C1;
-            C1 = a1;
-            found = p1[r] >= 0 || found;
-          } else if (a1 < C2) {
-            C2 = a1;
-          }
-        }
-        const int cls = !found ? 2 : (C2 == CUDART_INF ? 1 : 0);
-        if (cls == s_cls) atomicMax(&s_key, ord_d(cls == 0 ? C2 - C1 : 0.0));
-      }
+      for (int q = tid; q < P0; q += RP_THREADS)
+        if (!s_dead[q]) atomicMax(&s_cls, r_class(V, q));
       __syncthreads();
-    }
-    for (int q = tid; q < P0; q += RP_THREADS) {
-      if (s_dead[q]) continue;
-      double C1 = CUDART_INF, C2 = CUDART_INF;
-      bool found = false;
-      int R = -1, POS = -1;
-      const double *c1 = V.c1 + (size_t)q * V.J, *c2 = V.c2 + (size_t)q * V.J;
-      const int *p1 = V.p1 + (size_t)q * V.J;
-      for (int r = 0; r < m; r++) {
-        const double a1 = c1[r];
-        if (a1 < C1) {
-          const double a2 = c2[r];
-          C2 = a2 < C1 ? a2 : C1;
-          C1 = a1;
-          R = r;
-          POS = p1[r];
-          found = true;
-        } else if (a1 < C2) {
-          C2 = a1;
-        }
-      }
-      bool match;
-      if (regret) {
-        const int cls = !found ? 2 : (C2 == CUDART_INF ? 1 : 0);
-        match = cls == s_cls && ord_d(cls == 0 ? C2 - C1 : 0.0) == s_key;
-      } else {
-        match = found && ord_d(C1) == s_key;
-      }
-      if (match) atomicMin(&s_q, q);
+      for (int q = tid; q < P0; q += RP_THREADS)
+        if (!s_dead[q] && r_class(V, q) == s_cls) atomicMax(&s_key, ord_d(r_regret(V, q)));
+      __syncthreads();
+      for (int q = tid; q < P0; q += RP_THREADS)
+        if (!s_dead[q] && r_class(V, q) == s_cls && ord_d(r_regret(V, q)) == s_key) atomicMin(&s_q, q);
+    } else {
+      for (int q = tid; q < P0; q += RP_THREADS)
+        if (!s_dead[q] && V.fR1[q] >= 0) atomicMin(&s_key, ord_d(V.fC1[q]));
+      __syncthreads();
+      for (int q = tid; q < P0; q += RP_THREADS)
+        if (!s_dead[q] && V.fR1[q] >= 0 && ord_d(V.fC1[q]) == s_key) atomicMin(&s_q, q);
     }
     __syncthreads();
     if (tid == 0) {
@@ -358,12 +332,8 @@ __global__ void __launch_bounds__(RP_THREADS) k_repair(DevInst I, DevPop P, int 
         q = 0;
         while (s_dead[q]) q++;
       } else {
-        double C1 = CUDART_INF;
-        const double *c1 = V.c1 + (size_t)q * V.J;
-        const int *p1 = V.p1 + (size_t)q * V.J;
-        for (int r = 0; r < m; r++)
-          if (c1[r] < C1) { C1 = c1[r]; R = r; POS = p1[r]; }
-        if (R >= 0 && POS < 0) R = -1;
+        R = V.fR1[q];
+        POS = V.fP1[q];
       }
       s_dead[q] = 1;
       s_alive--;
@@ -372,6 +342,7 @@ __global__ void __launch_bounds__(RP_THREADS) k_repair(DevInst I, DevPop P, int 
         const int r = open_route(node);
         if (r < 0) s_err = MDR_ERR_CAPACITY;
         s_touch = r;
+        s_slots += 2;
       } else {
         int4 mt = V.rm[R];
         if (mt.x >= V.K) {
@@ -387,14 +358,19 @@ __global__ void __launch_bounds__(RP_THREADS) k_repair(DevInst I, DevPop P, int 
           V.rm[R] = mt;
         }
         s_touch = R;
+        s_slots += 1;
       }
     }
     __syncthreads();
     if (s_err) break;
-    const int rt = s_touch;
+    const int rt = s_touch, m = s_m;
     if (wid == 0) r_rebuild(I, V, rt, lane);
     __syncthreads();
-    // (e) the touched route's column for every pending customer
+    // (e) the touched route's column for every pending customer; refold a
+    // customer only when its top two can change: rt supplied C1 or C2, or the
+    // new minimum of rt reaches C2 (otherwise every value of rt is > C2 before
+    // and after, and the first minimum lies in another route)
+    const int kk = V.rm[rt].x + 1;
     for (int q = tid; q < P0; q += RP_THREADS) {
       if (s_dead[q]) continue;
       double m1, m2;
@@ -403,7 +379,8 @@ __global__ void __launch_bounds__(RP_THREADS) k_repair(DevInst I, DevPop P, int 
       V.c1[(size_t)q * V.J + rt] = m1;
       V.c2[(size_t)q * V.J + rt] = m2;
       V.p1[(size_t)q * V.J + rt] = pos1;
-      ev_dev += V.rm[rt].x + 1;
+      ev_dev += kk;
+      if (V.fR1[q] == rt || V.fR2[q] == rt || !(m1 > V.fC2[q])) r_fold(V, q, m);
     }
     __syncthreads();
   }
@@ -419,11 +396,11 @@ __global__ void __launch_bounds__(RP_THREADS) k_repair(DevInst I, DevPop P, int 
 }
 
 void launch_repair(const DevInst &I, const DevPop &P, int B, int op, const int *pend_off, const int *pend,
-                   void *pre, void *suf, double *c1, double *c2, int *p1, int Pcap, int *status, long long *stats,
-                   cudaStream_t s) {
+                   void *pre, void *suf, double *c1, double *c2, int *p1, double *fold, int *foldi, int Pcap,
+                   int *status, long long *stats, cudaStream_t s) {
   if (B <= 0) return;
-  k_repair<<<B, RP_THREADS, 0, s>>>(I, P, B, op, pend_off, pend, (RAt *)pre, (RAt *)suf, c1, c2, p1, Pcap, status,
-                                    stats);
+  k_repair<<<B, RP_THREADS, 0, s>>>(I, P, B, op, pend_off, pend, (RAt *)pre, (RAt *)suf, c1, c2, p1, fold, foldi,
+                                    Pcap, status, stats);
 }
 
 size_t repair_attr_bytes() { return sizeof(RAt); }

@@ -15,7 +15,7 @@ for r in rows[1:]:
     n[k] += 1
 T = sum(tot.values())
 lines = [f"# {tag}: ncu launch list (gpu__time_duration.sum, --clock-control none; cold-cache, serialised)",
-         "# command: python bench.py --config C4 --steps 1 --warmup 0 --no-cpu-baseline --no-e2e (launches 2000..3600)", ""]
+         f"# command: {sys.argv[5] if len(sys.argv) > 5 else 'python bench.py --config C4 --steps 1 --warmup 0 --no-cpu-baseline --no-e2e (launches 2000..3600)'}", ""]
 for k, v in tot.most_common():
     lines.append(f"{k:34s} launches {n[k]:5d}  total {v / 1e6:8.2f} ms  share {v / T * 100:5.1f}%  avg {v / n[k] / 1e3:8.1f} us")
 
@@ -24,7 +24,7 @@ def q(*args):
     return subprocess.run(["ncu", "-i", rep, *args], capture_output=True, text=True).stdout
 
 
-lines += ["", f"# full-set capture of one round's evaluation kernels ({rep.split('/')[-1]})", ""]
+lines += ["", f"# full-set capture ({rep.split('/')[-1]})", ""]
 det = list(csv.reader(io.StringIO(q("--page", "details", "--csv"))))
 hd = det[0]
 want = ("Duration", "Compute (SM) Throughput", "L1/TEX Cache Throughput", "L2 Cache Throughput", "DRAM Throughput",
