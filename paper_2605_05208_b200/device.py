@@ -72,12 +72,13 @@ def flatten_population(sols):
     rb = [0]
     coff = [0]
     cust, dep, arr = [], [], []
+    ext, cap, dap, aap = cust.extend, coff.append, dep.append, arr.append
     for s in sols:
         for r in s.routes:
-            cust.extend(r.customers)
-            coff.append(len(cust))
-            dep.append(r.depart)
-            arr.append(r.arrive)
+            ext(r.customers)
+            cap(len(cust))
+            dap(r.depart)
+            aap(r.arrive)
         rb.append(len(dep))
     f = lambda x: np.ascontiguousarray(np.asarray(x, dtype=np.int32).reshape(-1)) if len(x) else np.zeros(1, np.int32)
     return (np.asarray(rb, np.int32), np.asarray(coff, np.int32), f(cust), f(dep), f(arr))
@@ -139,12 +140,10 @@ class Population:
                                     ptr(dep, i32p), ptr(arr, i32p), ptr(extra, f64p), C.byref(nr), C.byref(nc), s)
         check(rc, "mdr_pop_download")
         self.d2h_bytes = int(rbase.nbytes + 4 * (nr.value + 1) + 4 * nc.value + 8 * nr.value + extra.nbytes)
-        out = []
-        for b in range(B):
-            routes = []
-            for r in range(rbase[b], rbase[b + 1]):
-                routes.append((int(dep[r]), int(arr[r]), cust[coff[r]:coff[r + 1]].tolist()))
-            out.append(routes)
+        R = int(rbase[B]) if B else 0
+        cl, ol = cust[:int(coff[R])].tolist(), coff[:R + 1].tolist()
+        dl, al, bl = dep[:R].tolist(), arr[:R].tolist(), rbase.tolist()
+        out = [[(dl[r], al[r], cl[ol[r]:ol[r + 1]]) for r in range(bl[b], bl[b + 1])] for b in range(B)]
         return out, extra
 
     def download(self, stream=None):

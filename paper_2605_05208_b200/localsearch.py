@@ -120,7 +120,7 @@ def _advance(rng, ops, passes: int) -> None:
     items = np.ascontiguousarray([int(o) for o in ops], dtype=np.uint8)
     _lib.check(_lib.lib().mdr_shuffle_stream(_lib.ptr(mt, C.POINTER(C.c_uint32)), len(items),
                                              _lib.ptr(items, _lib.u8p), passes, None), "mdr_shuffle_stream")
-    rng.setstate((st[0], tuple(int(x) for x in mt), st[2]))
+    rng.setstate((st[0], tuple(mt.tolist()), st[2]))
 
 
 class DeviceSearch:
