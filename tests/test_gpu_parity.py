@@ -1,6 +1,7 @@
 """GPU parity: the sm_100a path (through the C-ABI) against the reference's
 golden outputs and the C oracle.  Bit-exact (`==`, -0.0 == +0.0) everywhere."""
 import random
+import zlib
 
 import numpy as np
 import pytest
@@ -111,7 +112,7 @@ def _synthetic_states(variant, n_customers, n_depots, seed, count, **kw):
     ("mdvrp", None, None, True), ("mdvrp", 3, 250.0, False), ("mdvrptw", 4, 500.0, True),
     ("mdvrptw", None, None, False), ("mdovrp", 2, None, True), ("mdovrp", None, None, False)])
 def test_population_descents_bit_exact_vs_oracle(variant, fleet, dur, mm):
-    inst, consts, nbr, sols = _synthetic_states(variant, 60, 3, hash((variant, fleet, mm)) % 1000, 12,
+    inst, consts, nbr, sols = _synthetic_states(variant, 60, 3, zlib.crc32(repr((variant, fleet, mm)).encode()) % 1000, 12,
                                                 fleet=fleet, max_duration=dur)
     cfg = P.SearchConfig(depth=500, multi_move=mm)
     ops = P.enabled_operators(inst)
@@ -129,6 +130,50 @@ def test_population_descents_bit_exact_vs_oracle(variant, fleet, dur, mm):
         assert pens[i].lam == lam
         assert stats[i]["passes"] == st["passes"] and stats[i]["accepted"] == st["accepted"]
         assert stats[i]["cands"] == st["cands"], "candidate counts per operator must equal the reference's"
+
+
+FUZZ = list(range(64))
+
+
+@pytest.mark.parametrize("seed", FUZZ)
+def test_fuzz_descents_bit_exact_vs_oracle(seed):
+    """Randomised shapes: variant, 2-120 customers, 1-6 depots, fleet limits
+    (incl. one vehicle per depot), tight or loose capacity and duration,
+    theta 1-30, depth 1-300, single/multi-move, lambda != 1 starts."""
+    r = random.Random(9000 + seed)
+    variant = r.choice(["mdvrp", "mdvrptw", "mdovrp"])
+    nc, nd = r.randint(2, 120), r.randint(1, 6)
+    fleet = r.choice([None, None, 1, 2, 4])
+    cap = r.choice([None, 15, 40, 1000])
+    dur = r.choice([None, None, 150.0, 400.0]) if variant != "mdovrp" else None
+    inst = W.make_instance(r, variant, n_customers=nc, n_depots=nd, capacity=cap, max_duration=dur, fleet=fleet)
+    consts = P.ScalingConstants.from_instance(inst)
+    nbr = P.build_neighbors(inst, P.NeighborConfig(r.choice([1, 3, 8, 30])), consts)
+    count = r.randint(1, 6)
+    sols = [W.random_solution(random.Random(seed * 100 + i), inst, scramble_depots=r.random() < 0.5)
+            for i in range(count)]
+    depth, mm = r.randint(1, 300), r.random() < 0.6
+    lams = [[r.choice([0.01, 0.3, 1.0, 7.0]) for _ in range(4)] for _ in range(count)]
+    cfg = P.SearchConfig(depth=depth, multi_move=mm)
+    ops = P.enabled_operators(inst)
+    oi = O.OracleInstance(inst, consts, nbr)
+    want = []
+    for i, s in enumerate(sols):
+        perms = draw_permutations(random.Random(i), ops, depth + 1)
+        want.append(O.local_search(oi, s, lams[i], depth, mm, 0.5, 0.01, 1e4, perms))
+    work = [s.clone() for s in sols]
+    pens = [P.PenaltyState(lam=list(l)) for l in lams]
+    rngs = [random.Random(i) for i in range(count)]
+    stats = P.local_search_population(work, pens, cfg, nbr, consts, inst, rngs)
+    for i in range(count):
+        routes, lam, st, _ = want[i]
+        assert G.routes_of(work[i]) == routes, f"seed {seed} individual {i}"
+        assert pens[i].lam == lam
+        assert stats[i]["passes"] == st["passes"] and stats[i]["cands"] == st["cands"]
+        ref_rng = random.Random(i)
+        for _ in range(st["passes"]):
+            ref_rng.shuffle(list(ops))
+        assert rngs[i].getstate() == ref_rng.getstate()
 
 
 def test_appendix_a_c2_shape_descents_vs_oracle():
