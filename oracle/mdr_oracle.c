@@ -961,6 +961,7 @@ static int ls_core(const orc_instance_desc *I, sol_t *s, double lam[4], const or
                    orc_ls_stats *st, orc_ls_trace *tr) {
   memset(st, 0, sizeof(*st));
   st->best_feasible_D = INFINITY;
+  if (tr && tr->snap_m) *tr->snap_m = -1;
   work_t W;
   memset(&W, 0, sizeof(W));
   cache_t C;
@@ -1024,7 +1025,23 @@ static int ls_core(const orc_instance_desc *I, sol_t *s, double lam[4], const or
       }
       if (feas) {
         st->n_feasible++;
-        if (tot[0] < st->best_feasible_D) st->best_feasible_D = tot[0];
+        if (tot[0] < st->best_feasible_D) {
+          st->best_feasible_D = tot[0];
+          if (tr && tr->snap_m) { /* snapshot of the new best feasible state */
+            int64_t nc = 0;
+            for (int r = 0; r < s->m; r++) nc += s->r[r].k;
+            if (s->m <= tr->snap_cap_routes && nc <= tr->snap_cap_cust) {
+              *tr->snap_m = s->m;
+              tr->snap_off[0] = 0;
+              for (int r = 0; r < s->m; r++) {
+                tr->snap_dep[r] = s->r[r].dep;
+                tr->snap_arr[r] = s->r[r].arr;
+                memcpy(tr->snap_cust + tr->snap_off[r], s->r[r].c, sizeof(int32_t) * (size_t)s->r[r].k);
+                tr->snap_off[r + 1] = tr->snap_off[r] + s->r[r].k;
+              }
+            }
+          }
+        }
       }
       accepted++;
       any = 1;

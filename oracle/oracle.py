@@ -62,7 +62,9 @@ class LsStats(C.Structure):
 
 class LsTrace(C.Structure):
     _fields_ = [("cap", C.c_int32), ("op", _i32p), ("n_moves", _i32p), ("lam", _f64p),
-                ("D", _f64p), ("feasible", _u8p)]
+                ("D", _f64p), ("feasible", _u8p), ("snap_cap_routes", C.c_int32), ("snap_cap_cust", C.c_int32),
+                ("snap_m", _i32p), ("snap_off", _i32p), ("snap_cust", _i32p), ("snap_dep", _i32p),
+                ("snap_arr", _i32p)]
 
 
 def lib():
@@ -234,7 +236,7 @@ def _cfg(depth, multi_move, kappa, lam_min, lam_max, perms):
 
 
 def local_search(oi: OracleInstance, sol, lam, depth, multi_move, kappa, lam_min, lam_max,
-                 perms, trace_cap=0):
+                 perms, trace_cap=0, snapshot=False):
     """Returns (routes as (depart, arrive, customers) list, lam, stats dict, trace dict)."""
     L = lib()
     fl = _Flat(sol)
@@ -250,15 +252,24 @@ def local_search(oi: OracleInstance, sol, lam, depth, multi_move, kappa, lam_min
     st = LsStats()
     tr = None
     tarr = None
-    if trace_cap:
-        tarr = dict(op=np.zeros(trace_cap, np.int32), n_moves=np.zeros(trace_cap, np.int32),
-                    lam=np.zeros(trace_cap * 4), D=np.zeros(trace_cap),
-                    feasible=np.zeros(trace_cap, np.uint8))
+    if trace_cap or snapshot:
+        tc = max(trace_cap, 1)
+        tarr = dict(op=np.zeros(tc, np.int32), n_moves=np.zeros(tc, np.int32),
+                    lam=np.zeros(tc * 4), D=np.zeros(tc),
+                    feasible=np.zeros(tc, np.uint8))
         tr = LsTrace()
         tr.cap = trace_cap
         tr.op, tr.n_moves = _p(tarr["op"], _i32p), _p(tarr["n_moves"], _i32p)
         tr.lam, tr.D = _p(tarr["lam"], _f64p), _p(tarr["D"], _f64p)
         tr.feasible = _p(tarr["feasible"], _u8p)
+        if snapshot:
+            sm = np.zeros(1, np.int32)
+            so, sc = np.zeros(cap_r + 1, np.int32), np.zeros(ncust, np.int32)
+            sd, sa = np.zeros(cap_r, np.int32), np.zeros(cap_r, np.int32)
+            tarr.update(snap_m=sm, snap_off=so, snap_cust=sc, snap_dep=sd, snap_arr=sa)
+            tr.snap_cap_routes, tr.snap_cap_cust = cap_r, ncust
+            tr.snap_m, tr.snap_off, tr.snap_cust = _p(sm, _i32p), _p(so, _i32p), _p(sc, _i32p)
+            tr.snap_dep, tr.snap_arr = _p(sd, _i32p), _p(sa, _i32p)
     rc = L.orc_local_search(C.byref(oi.desc), C.byref(fl.s), _p(lam_a, _f64p), C.byref(cfg),
                             C.c_int32(cap_r), C.c_int32(ncust), C.byref(out_m), _p(off, _i32p),
                             _p(cust, _i32p), _p(dep, _i32p), _p(arr, _i32p), C.byref(st),
@@ -278,6 +289,12 @@ def local_search(oi: OracleInstance, sol, lam, depth, multi_move, kappa, lam_min
         trace = dict(op=tarr["op"][:k], n_moves=tarr["n_moves"][:k],
                      lam=tarr["lam"][:4 * k].reshape(k, 4), D=tarr["D"][:k],
                      feasible=tarr["feasible"][:k].astype(bool))
+        if snapshot:
+            m = int(tarr["snap_m"][0])
+            so, sc = tarr["snap_off"], tarr["snap_cust"]
+            trace["best_feasible"] = None if m < 0 else [
+                (int(tarr["snap_dep"][r]), int(tarr["snap_arr"][r]), [int(c) for c in sc[so[r]:so[r + 1]]])
+                for r in range(m)]
     return routes, [float(x) for x in lam_a], stats, trace
 
 

@@ -1,9 +1,16 @@
-"""Penalty scaling constants and adaptive penalty state (mirrors `mdroute.evaluation`).
+"""Penalty scaling constants, adaptive penalty state and the scalar evaluation
+(mirrors `mdroute.evaluation`).
 
 `ScalingConstants.from_instance` restates evaluation.py:117-132, `PenaltyState`
 evaluation.py:135-150 and `adapt_penalties` evaluation.py:153-161.  The device
-local search applies the same update on the GPU (csrc/mdr_ls.cu); this host
-copy is used by the operator-level API and for argument checking.
+local search applies the same update on the GPU (csrc/mdr_kernels.cu); this
+host copy is used by the operator-level API and for argument checking.
+
+The scalar sequence algebra (`single_attr`, `concat`, `fold_attrs`,
+`route_attr`, evaluation.py:22-106) and the from-scratch `evaluate`
+(evaluation.py:164-224) are what the generation loop (engine.py) scores each
+offspring with; they keep Python's `max`/`min` semantics (first argument unless
+the second compares strictly larger / smaller).
 """
 from __future__ import annotations
 
@@ -59,3 +66,105 @@ def adapt_penalties(penalties, violated):
             penalties.lam[i] *= penalties.kappa
         penalties.lam[i] = min(max(penalties.lam[i], penalties.lam_min), penalties.lam_max)
     return penalties
+
+
+INF = float("inf")
+
+
+class SeqAttr:
+    """dist, load, T, E, L, TW of a node sequence plus its end nodes (evaluation.py:22-57)."""
+
+    __slots__ = ("dist", "load", "T", "E", "L", "TW", "first", "last")
+
+    def __init__(self, dist=0.0, load=0.0, T=0.0, E=0.0, L=INF, TW=0.0, first=-1, last=-1):
+        self.dist, self.load, self.T, self.E, self.L, self.TW = dist, load, T, E, L, TW
+        self.first, self.last = first, last
+
+    def is_empty(self) -> bool:
+        return self.first < 0
+
+
+def single_attr(node: int, inst) -> SeqAttr:
+    return SeqAttr(0.0, float(inst.demand[node]), float(inst.service[node]), float(inst.tw_early[node]),
+                   float(inst.tw_late[node]), 0.0, node, node)
+
+
+def concat(a: SeqAttr, b: SeqAttr, inst) -> SeqAttr:
+    if b.first < 0:
+        return a
+    if a.first < 0:
+        return b
+    t = float(inst.time[a.last, b.first])
+    c = float(inst.dist[a.last, b.first])
+    delta = a.T - a.TW + t
+    wait = max(b.E - delta - a.L, 0.0)
+    warp = max(a.E + delta - b.L, 0.0)
+    return SeqAttr(a.dist + c + b.dist, a.load + b.load, a.T + b.T + t + wait,
+                   max(b.E - delta, a.E) - wait, min(b.L - delta, a.L) + warp,
+                   a.TW + b.TW + warp, a.first, b.last)
+
+
+def fold_attrs(seq, inst) -> SeqAttr:
+    acc = single_attr(seq[0], inst)
+    for node in seq[1:]:
+        acc = concat(acc, single_attr(node, inst), inst)
+    return acc
+
+
+def route_attr(route, inst) -> SeqAttr:
+    return fold_attrs(route.sequence(inst.open_routes), inst)
+
+
+class EvalBreakdown:
+    """D, the four unweighted violation terms and the penalised total (evaluation.py:164-176)."""
+
+    __slots__ = ("D", "V1", "V2", "V3", "V4", "F")
+
+    def __init__(self, D=0.0, V1=0.0, V2=0.0, V3=0.0, V4=0.0, F=0.0):
+        self.D, self.V1, self.V2, self.V3, self.V4, self.F = D, V1, V2, V3, V4, F
+
+    def violations(self):
+        return [self.V1, self.V2, self.V3, self.V4]
+
+
+def route_contributions(attr: SeqAttr, depart: int, arrive: int, consts, inst):
+    v1 = consts.gamma * attr.TW if inst.has_windows else 0.0
+    v2 = consts.theta * max(attr.load - inst.capacity, 0.0) / inst.capacity
+    v3 = 0.0
+    if inst.max_duration != INF:
+        v3 = consts.theta * max(attr.T - inst.max_duration, 0.0) / inst.max_duration
+    closure = 0 if inst.open_routes else int(depart != arrive)
+    return attr.dist, v1, v2, v3, closure
+
+
+def depot_counts(sol, inst) -> list:
+    counts = [0] * inst.n_depots
+    for r in sol.routes:
+        if r.customers:
+            counts[r.depart] += 1
+    return counts
+
+
+def fleet_excess(counts, inst) -> int:
+    if inst.fleet_per_depot == INF:
+        return 0
+    return int(sum(max(k - inst.fleet_per_depot, 0) for k in counts))
+
+
+def evaluate(sol, penalties, consts, inst) -> EvalBreakdown:
+    """Full penalised evaluation of a solution from scratch (evaluation.py:206-224)."""
+    out = EvalBreakdown()
+    closures = 0
+    for r in sol.routes:
+        if not r.customers:
+            continue
+        d, v1, v2, v3, clo = route_contributions(route_attr(r, inst), r.depart, r.arrive, consts, inst)
+        out.D += d
+        out.V1 += v1
+        out.V2 += v2
+        out.V3 += v3
+        closures += clo
+    out.V4 = consts.theta * (closures + fleet_excess(depot_counts(sol, inst), inst))
+    lam = penalties.lam
+    out.F = out.D + lam[0] * out.V1 + lam[1] * out.V2 + lam[2] * out.V3 + lam[3] * out.V4
+    return out

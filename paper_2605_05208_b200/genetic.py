@@ -1,5 +1,7 @@
-"""Repair insertion on the GPU (mirrors `mdroute.genetic.repair_insert`,
-genetic.py:174-244).
+"""Offspring construction: repair insertion on the GPU (mirrors
+`mdroute.genetic.repair_insert`, genetic.py:174-244)
+and the route-exchange crossover, bandits and population initialisation the
+generation loop drives (genetic.py:25-66, 296-446; sec. 8(f) row 3).
 
 `repair_insert` keeps the reference signature and semantics: `sol` is modified
 in place (existing routes keep their order, new routes are appended), pending
@@ -15,12 +17,19 @@ repaired together (one CTA per individual) and can then be handed straight to
 """
 from __future__ import annotations
 
+import math
+from dataclasses import dataclass
 from enum import IntEnum
+from typing import Optional, Sequence
 
 from ._lib import CapacityError
 from .device import Population
-from .model import INF, Route
+from .evaluation import route_attr
+from .model import INF, Route, Solution, route_edges, solution_edges
 from .session import session_for
+from .workload import initial_solution
+
+DIVERSITY_LEVELS = 20
 
 
 class InsertionOperator(IntEnum):
@@ -125,3 +134,186 @@ def repair_insert(sol, unrouted, op, inst, consts, penalties, rng):
         return sol
     repair_population([sol], [pending], op, inst, consts, [penalties])
     return sol
+
+
+# --------------------------------------------------------------------------- #
+# learning pieces (genetic.py:25-66)
+# --------------------------------------------------------------------------- #
+
+class DiscountedUCB1:
+    """Discounted UCB1 over a fixed action set; unplayed actions first, in index order."""
+
+    def __init__(self, n_actions: int, discount: float = 0.99):
+        self.n_actions = n_actions
+        self.discount = discount
+        self.rewards = [0.0] * n_actions
+        self.counts = [0.0] * n_actions
+
+    def select(self) -> int:
+        for i, c in enumerate(self.counts):
+            if c == 0.0:
+                return i
+        total = sum(self.counts)
+        best, best_val = 0, -INF
+        for i in range(self.n_actions):
+            val = self.rewards[i] / self.counts[i] + math.sqrt(2.0 * math.log(total) / self.counts[i])
+            if val > best_val:
+                best, best_val = i, val
+        return best
+
+    def update(self, action: int, reward: float) -> None:
+        g = self.discount
+        self.rewards = [x * g for x in self.rewards]
+        self.counts = [x * g for x in self.counts]
+        self.rewards[action] += reward
+        self.counts[action] += 1.0
+
+
+def improvement_reward(parent_value: float, offspring_value: float) -> float:
+    """Percent improvement of the offspring over the main parent."""
+    return 100.0 * (parent_value - offspring_value) / parent_value
+
+
+def initialize_population(inst, mu: int, consts, penalties, rng) -> list:
+    if mu < 2:
+        raise ValueError("population size must be >= 2")
+    return [initial_solution(inst, consts, penalties, rng) for _ in range(mu)]
+
+
+# --------------------------------------------------------------------------- #
+# route-exchange crossover (genetic.py:300-446)
+# --------------------------------------------------------------------------- #
+
+@dataclass
+class RoutePairScore:
+    new_edges: int
+    missing: int
+    duplicated: int
+    conflicting: int
+    score: int
+    delta_sigma: int
+
+
+def score_route_pair(route_out, route_in, main_edges: set, main_customers: set, introduced_customers: set,
+                     inst) -> RoutePairScore:
+    """Exchange `route_out` (leaves the offspring) for `route_in` (donor)."""
+    cin, cout = set(route_in.customers), set(route_out.customers)
+    new_edges = len(route_edges(route_in, inst.open_routes) - main_edges)
+    missing = len(cout - cin)
+    duplicated = len(cin & (main_customers - cout))
+    conflicting = len(cin & introduced_customers)
+    return RoutePairScore(new_edges, missing, duplicated, conflicting,
+                          -(new_edges - missing - duplicated - 10 * conflicting), new_edges + missing + duplicated)
+
+
+def diversity_bounds(level: int, inst, main_parent) -> tuple:
+    base = inst.n_customers + len(main_parent.routes)
+    return level / DIVERSITY_LEVELS * base, (level + 1) / DIVERSITY_LEVELS * base
+
+
+@dataclass
+class CrossoverResult:
+    offspring: Solution
+    diversity_level: int
+    insertion_op: InsertionOperator
+    sigma: float
+    main_index: int = -1
+
+
+def _removal_saving(route, pos: int, inst) -> float:
+    seq = route.sequence(inst.open_routes)
+    i = pos + 1
+    prev, here = seq[i - 1], seq[i]
+    if i + 1 >= len(seq):
+        return float(inst.dist[prev, here])
+    nxt = seq[i + 1]
+    return float(inst.dist[prev, here] + inst.dist[here, nxt] - inst.dist[prev, nxt])
+
+
+def _remove_redundant(offspring, origin_main: list, inst) -> None:
+    """One copy per duplicated customer: donor copies first, then the copy whose
+    removal saves the least distance is kept (genetic.py:424-446)."""
+    where: dict = {}
+    for ri, r in enumerate(offspring.routes):
+        for pos, c in enumerate(r.customers):
+            where.setdefault(c, []).append((ri, pos))
+    drop = []
+    for occ in where.values():
+        if len(occ) > 1:
+            keep = min(occ, key=lambda it: (origin_main[it[0]], _removal_saving(offspring.routes[it[0]], it[1], inst)))
+            drop.extend(o for o in occ if o != keep)
+    for ri, pos in sorted(drop, key=lambda t: (t[0], -t[1])):
+        del offspring.routes[ri].customers[pos]
+
+
+def route_exchange(population: Sequence, inst, diversity_bandit: DiscountedUCB1, rng,
+                   main_index: Optional[int] = None):
+    """The exchange half of DCREX (genetic.py:343-405): returns (offspring with
+    duplicates removed, unrouted customers, level, sigma, main_index)."""
+    if len(population) < 2:
+        raise ValueError("crossover needs at least two parents")
+    if main_index is None:
+        main_index = rng.randrange(len(population))
+    main = population[main_index]
+    level = diversity_bandit.select()
+    sigma_min, sigma_max = diversity_bounds(level, inst, main)
+    off = main.clone()
+    origin_main = [True] * len(off.routes)
+    main_edges = solution_edges(main, inst.open_routes)
+    main_customers = set()
+    for r in off.routes:
+        main_customers.update(r.customers)
+    introduced: set = set()
+    donors = [p for i, p in enumerate(population) if i != main_index]
+    rng.shuffle(donors)
+    sigma = 0.0
+    for donor in donors:
+        used: set = set()
+        reached = False
+        while True:
+            pairs = []
+            for oi, r_out in enumerate(off.routes):
+                if not origin_main[oi]:
+                    continue
+                for dj, r_in in enumerate(donor.routes):
+                    if dj in used or not r_in.customers:
+                        continue
+                    sc = score_route_pair(r_out, r_in, main_edges, main_customers, introduced, inst)
+                    pairs.append((sc.score, oi, dj, sc))
+            if not pairs:
+                break
+            pairs.sort(key=lambda t: (t[0], t[1], t[2]))
+            _, oi, dj, sc = rng.choice(pairs[:5])
+            if sigma + sc.delta_sigma >= sigma_max:
+                break
+            main_customers.difference_update(off.routes[oi].customers)
+            del off.routes[oi]
+            del origin_main[oi]
+            r_new = donor.routes[dj].clone()
+            off.routes.append(r_new)
+            origin_main.append(False)
+            introduced.update(r_new.customers)
+            used.add(dj)
+            sigma += sc.delta_sigma
+            if sigma >= sigma_min:
+                reached = True
+                break
+        if reached:
+            break
+    _remove_redundant(off, origin_main, inst)
+    covered = set(off.customer_list())
+    unrouted = [c for c in inst.customers() if c not in covered]
+    return off, unrouted, level, sigma, main_index
+
+
+def dcrex(population: Sequence, inst, consts, penalties, diversity_bandit: DiscountedUCB1,
+          insertion_bandit: DiscountedUCB1, rng, main_index: Optional[int] = None) -> CrossoverResult:
+    """Diversity-controlled route exchange over multiple parents, then repair
+    on the GPU (genetic.py:343-421)."""
+    off, unrouted, level, sigma, main_index = route_exchange(population, inst, diversity_bandit, rng, main_index)
+    op = InsertionOperator(insertion_bandit.select())
+    repair_insert(off, unrouted, op, inst, consts, penalties, rng)
+    off.drop_empty_routes()
+    for r in off.routes:
+        r.attr = route_attr(r, inst)
+    return CrossoverResult(off, level, op, sigma, main_index)

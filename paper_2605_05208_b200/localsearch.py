@@ -214,18 +214,26 @@ def _searcher(inst, consts, nbr, device: int = 0) -> DeviceSearch:
 
 
 def local_search_population(sols, penalties, cfg: SearchConfig, nbr, consts, inst, rngs,
-                            deadline: Optional[float] = None, device: int = 0):
+                            deadline: Optional[float] = None, device: int = 0, on_feasible=None):
     """B independent descents in one device run; solutions and penalty states
-    are updated in place.  Returns the per-individual stats."""
+    are updated in place.  Returns the per-individual stats.  on_feasible(D, sol),
+    if given, is called per individual (in order) with its lowest-D feasible
+    state passed through, as `local_search` does."""
     search = _searcher(inst, consts, nbr, device)
     ops = enabled_operators(inst)
     perms = np.stack([draw_permutations(r, ops, cfg.depth + 1) for r in rngs])
     lams = [p.lam for p in penalties]
     dl = -1.0 if deadline is None else max(0.0, deadline - time.monotonic())
     p0 = penalties[0]
-    routes, lam, stats = search.run(sols, lams, perms, cfg, p0.kappa, p0.lam_min, p0.lam_max, dl)
+    routes, lam, stats = search.run(sols, lams, perms, cfg, p0.kappa, p0.lam_min, p0.lam_max, dl,
+                                    snapshot_best=on_feasible is not None)
+    best = search.pop.download_best() if on_feasible is not None else None
     for b, (sol, pen, rng) in enumerate(zip(sols, penalties, rngs)):
         _advance(rng, ops, stats[b]["passes"])
         _apply_result(sol, routes[b])
         pen.lam[:] = [float(x) for x in lam[b]]
+        if best is not None and stats[b]["n_feasible"] > 0:
+            snap = sol.clone()
+            _apply_result(snap, best[0][b])
+            on_feasible(float(best[1][b]), snap)
     return stats

@@ -170,6 +170,26 @@ class Solution:
         return f"Solution({len(self.routes)} routes)"
 
 
+def route_edges(route, open_routes: bool) -> set:
+    """Undirected arcs of a route, the return arc omitted when open (model.py:217-220)."""
+    seq = route.sequence(open_routes)
+    return {(a, b) if a <= b else (b, a) for a, b in zip(seq, seq[1:])}
+
+
+def solution_edges(sol, open_routes: bool) -> set:
+    out: set = set()
+    for r in sol.routes:
+        if r.customers:
+            out |= route_edges(r, open_routes)
+    return out
+
+
+def route_distance(route, inst) -> float:
+    seq = route.sequence(inst.open_routes)
+    d = inst.dist
+    return float(sum(d[a, b] for a, b in zip(seq, seq[1:])))
+
+
 def flatten(sol):
     """Solution -> (off[m+1], cust, depart[m], arrive[m]) int32 arrays."""
     routes = sol.routes

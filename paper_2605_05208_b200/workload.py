@@ -15,7 +15,7 @@ import math
 import random
 from dataclasses import dataclass
 
-from .evaluation import PenaltyState, ScalingConstants
+from .evaluation import PenaltyState, ScalingConstants, concat, single_attr
 from .model import INF, Instance, Route, Solution, Variant
 from .neighborhood import NeighborConfig, build
 
@@ -129,33 +129,8 @@ def build_config(name: str, population: int | None = None, seed: int = 2026, sta
 # --------------------------------------------------------------------------- #
 # initial_solution (genetic.py:251-294) and its IBI repair (genetic.py:71-244)
 # --------------------------------------------------------------------------- #
-class _Attr:
-    __slots__ = ("dist", "load", "T", "E", "L", "TW", "first", "last")
-
-    def __init__(self, dist, load, T, E, L, TW, first, last):
-        self.dist, self.load, self.T, self.E, self.L, self.TW = dist, load, T, E, L, TW
-        self.first, self.last = first, last
-
-
-def _single(v, inst):
-    return _Attr(0.0, float(inst.demand[v]), float(inst.service[v]), float(inst.tw_early[v]),
-                 float(inst.tw_late[v]), 0.0, v, v)
-
-
-def _concat(a, b, inst):
-    """Scalar concat with Python max/min tie semantics (evaluation.py:74-94)."""
-    if b.first < 0:
-        return a
-    if a.first < 0:
-        return b
-    t = float(inst.time[a.last, b.first])
-    c = float(inst.dist[a.last, b.first])
-    delta = a.T - a.TW + t
-    wait = max(b.E - delta - a.L, 0.0)
-    warp = max(a.E + delta - b.L, 0.0)
-    return _Attr(a.dist + c + b.dist, a.load + b.load, a.T + b.T + t + wait,
-                 max(b.E - delta, a.E) - wait, min(b.L - delta, a.L) + warp,
-                 a.TW + b.TW + warp, a.first, b.last)
+_single = single_attr  # scalar algebra with Python max/min semantics (evaluation.py:60-94)
+_concat = concat
 
 
 class _RouteEval:

@@ -1,0 +1,112 @@
+"""Generation loop against the reference's own engine.run
+(tests/golden/engine.json from make_engine_golden.py).
+
+CPU: the loop's host control plane (route exchange, bandits, population
+management, evaluation, best tracking) with the oracle standing in for the two
+device kernels it calls (local search, repair) -- the RunStats must equal the
+reference's exactly.  GPU: the same runs through the device path."""
+import json
+import os
+import random
+
+import pytest
+
+from oracle import oracle as O
+from paper_2605_05208_b200 import engine as E
+from paper_2605_05208_b200 import genetic as GN
+from paper_2605_05208_b200 import workload as W
+from paper_2605_05208_b200.localsearch import _advance, _apply_result, draw_permutations, enabled_operators
+from paper_2605_05208_b200.neighborhood import NeighborConfig, build
+
+GOLD = json.load(open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "engine.json")))
+
+
+def _instance(spec):
+    variant, nc, nd, kw, seed = spec
+    return W.make_instance(random.Random(seed), variant, n_customers=nc, n_depots=nd, **kw)
+
+
+def _routes(sol):
+    return None if sol is None else [[r.depart, r.arrive, list(r.customers)] for r in sol.routes]
+
+
+def _check(st, want):
+    assert st.generations == want["generations"]
+    assert [float(x).hex() for x in st.cost_curve] == want["cost_curve"]
+    assert list(st.stagnation_trace) == want["stagnation_trace"]
+    assert float(st.best_cost).hex() == want["best_cost"] and st.feasible_found == want["feasible_found"]
+    assert float(st.best_infeasible_cost).hex() == want["best_infeasible_cost"]
+    assert _routes(st.best) == want["best"]
+    assert _routes(st.best_infeasible) == want["best_infeasible"]
+
+
+@pytest.fixture
+def oracle_kernels(monkeypatch):
+    """Route the loop's two device calls through the oracle (CPU)."""
+    cache = {}
+
+    def oi_for(inst, consts, nbr):
+        k = (id(inst), id(nbr))
+        if k not in cache:
+            cache[k] = O.OracleInstance(inst, consts, nbr)
+        return cache[k]
+
+    def local_search(sol, penalties, cfg, nbr, consts, inst, rng, deadline=None, on_feasible=None):
+        ops = enabled_operators(inst)
+        perms = draw_permutations(rng, ops, cfg.depth + 1)
+        routes, lam, st, tr = O.local_search(oi_for(inst, consts, nbr), sol, penalties.lam, cfg.depth,
+                                             cfg.multi_move, penalties.kappa, penalties.lam_min, penalties.lam_max,
+                                             perms, snapshot=on_feasible is not None)
+        _advance(rng, ops, st["passes"])
+        _apply_result(sol, routes)
+        penalties.lam[:] = lam
+        if on_feasible is not None and tr["best_feasible"] is not None:
+            snap = sol.clone()
+            _apply_result(snap, tr["best_feasible"])
+            on_feasible(st["best_feasible_D"], snap)
+        return sol
+
+    def repair_population(sols, unrouteds, op, inst, consts, penalties, device=0):
+        if not isinstance(penalties, (list, tuple)):
+            penalties = [penalties] * len(sols)
+        oi = oi_for(inst, consts, build(inst, NeighborConfig(1), consts)) if id(inst) not in cache else cache[id(inst)]
+        cache[id(inst)] = oi
+        for s, u, p in zip(sols, unrouteds, penalties):
+            GN._write_back(s, O.repair(oi, s, u, int(op), p.lam)[0])
+        return [dict(inserted=len(u)) for u in unrouteds]
+
+    monkeypatch.setattr(E, "local_search", local_search)
+    monkeypatch.setattr(GN, "repair_population", repair_population)
+    monkeypatch.setattr(E, "build_device", build)
+
+
+@pytest.mark.parametrize("tag", sorted(GOLD))
+def test_engine_control_plane_equals_reference(tag, oracle_kernels):
+    want = GOLD[tag]
+    st = E.run(_instance(want["instance"]), E.SolverConfig(**want["config"]))
+    _check(st, want)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("tag", sorted(GOLD))
+def test_engine_on_device_equals_reference(tag):
+    want = GOLD[tag]
+    st = E.run(_instance(want["instance"]), E.SolverConfig(**want["config"]))
+    _check(st, want)
+
+
+@pytest.mark.gpu
+def test_batched_engine_runs_and_keeps_coverage():
+    """The lock-step form: B offspring per generation through the batched device
+    calls; every offspring keeps full coverage, the best is feasible and its
+    cost is the from-scratch evaluation of the returned solution."""
+    want = GOLD["tw_mm"]
+    inst = _instance(want["instance"])
+    cfg = E.SolverConfig(**dict(want["config"], generations=4))
+    st = E.run_batched(inst, cfg, batch=16)
+    assert st.offspring == 16 * st.generations and st.feasible_found
+    assert sorted(st.best.customer_list()) == list(inst.customers())
+    from paper_2605_05208_b200.evaluation import PenaltyState, ScalingConstants, evaluate
+    bd = evaluate(st.best, PenaltyState(), ScalingConstants.from_instance(inst), inst)
+    assert max(bd.V1, bd.V2, bd.V3, bd.V4) <= 1e-9
+    assert abs(bd.D - st.best_cost) <= 1e-9 * max(1.0, bd.D)
