@@ -70,6 +70,7 @@ class RunStats:
     cost_curve: list = field(default_factory=list)
     stagnation_trace: list = field(default_factory=list)
     offspring: int = 0
+    phase_s: dict = field(default_factory=dict)  # wall time per loop phase (run_batched)
 
 
 def gap(f: float, bks: float) -> float:
@@ -187,8 +188,12 @@ def run_batched(inst, cfg: SolverConfig, batch: int = 64, nbr=None, device: int 
     if batch < 1:
         raise ValueError("batch must be >= 1")
     R = _Run(inst, cfg, nbr)
+    ph = R.stats.phase_s
+    for k in ("exchange", "repair", "local_search", "update"):
+        ph[k] = 0.0
     while R.running():
         prev = R.stats.best_cost
+        t0 = time.perf_counter()
         parents = list(R.pop.members)
         members = [m.sol for m in parents]
         kids, info = [], []
@@ -197,6 +202,7 @@ def run_batched(inst, cfg: SolverConfig, batch: int = 64, nbr=None, device: int 
             op = InsertionOperator(R.ins_bandit.select())
             kids.append((off, unrouted))
             info.append((parents[main_index], level, op))
+        t1 = time.perf_counter()
         for op in InsertionOperator:  # one device call per operator; RI draws from the run's rng
             idx = [j for j in range(batch) if info[j][2] == op and kids[j][1]]
             if not idx:
@@ -213,13 +219,20 @@ def run_batched(inst, cfg: SolverConfig, batch: int = 64, nbr=None, device: int 
             for r in off.routes:
                 r.attr = route_attr(r, inst)
             offspring.append(off)
+        t2 = time.perf_counter()
         pens = [R.penalties.clone() for _ in offspring]
         rngs = [random.Random(R.rng.getrandbits(64)) for _ in offspring]
         local_search_population(offspring, pens, R.search, R.nbr, R.consts, inst, rngs, deadline=R.deadline,
                                 device=device, on_feasible=R.snapshot_feasible)
         R.penalties.lam[:] = pens[-1].lam
+        t3 = time.perf_counter()
         for off, (main, level, op) in zip(offspring, info):
             off.meta["generation"] = R.gen
             R.absorb(off, main, level, op)
         R.close_generation(prev)
+        t4 = time.perf_counter()
+        ph["exchange"] += t1 - t0
+        ph["repair"] += t2 - t1
+        ph["local_search"] += t3 - t2
+        ph["update"] += t4 - t3
     return R.finish()

@@ -106,8 +106,11 @@ def repair_population(sols, unrouteds, op, inst, consts, penalties, device: int 
             K = min(500, max(K * 2, need["K"] + 16))
         pop = getattr(sess, "_repair_pop", None)  # reused across calls while the caps fit
         if pop is None or pop.B_cap < len(sols) or pop.J_cap < J or pop.K_cap < K:
+            if pop is not None:  # grow with headroom so a GA's varying offspring do not re-allocate
+                J, K = min(4094, max(J, pop.J_cap * 3 // 2)), min(500, max(K, pop.K_cap * 3 // 2))
             sess._repair_pop = None
-            pop = sess._repair_pop = Population(sess.dinst, max(len(sols), 1), J, K, 1 << 10)
+            pop = sess._repair_pop = Population(sess.dinst, max(len(sols), 1, pop.B_cap if pop else 0), J, K,
+                                                1 << 10)
         pop.upload(sols, [p.lam for p in penalties])
         try:
             stats = pop.repair(int(op), unrouteds)
@@ -246,10 +249,59 @@ def _remove_redundant(offspring, origin_main: list, inst) -> None:
         del offspring.routes[ri].customers[pos]
 
 
+def _pair_scores(off, origin_main, donor, used, main_edges, main_customers, introduced, inst, donor_cache):
+    """Every admissible (offspring main-origin route oi, donor route dj) pair as
+    (score, oi, dj, delta_sigma), in the order of score_route_pair's formula:
+    new_edges(dj) = |E(dj) - E(main)|, missing = |C(oi)| - |C(oi) & C(dj)|,
+    duplicated = |C(dj) & MC| - |C(dj) & C(oi)| (C(oi) is part of MC),
+    conflicting = |C(dj) & introduced| -- exact integers from one incidence
+    product instead of per-pair set algebra."""
+    import numpy as np
+    outs = [oi for oi in range(len(off.routes)) if origin_main[oi]]
+    ins = [dj for dj, r in enumerate(donor.routes) if dj not in used and r.customers]
+    if not outs or not ins:
+        return None
+    n = inst.n_nodes
+    if "dc" not in donor_cache:  # per-donor flat customers / route ids and new-edge counts (main_edges is fixed)
+        dc = [c for r in donor.routes for c in r.customers]
+        donor_cache["dc"] = np.asarray(dc, np.int64)
+        donor_cache["dr"] = np.asarray([j for j, r in enumerate(donor.routes) for _ in r.customers], np.int64)
+        donor_cache["e"] = np.array([len(route_edges(r, inst.open_routes) - main_edges) for r in donor.routes],
+                                    np.int64)
+    dc, dr, nd = donor_cache["dc"], donor_cache["dr"], len(donor.routes)
+    row_of = np.full(n, -1, np.int64)
+    n_out = np.empty(len(outs), np.int64)
+    for a, oi in enumerate(outs):
+        cs = off.routes[oi].customers
+        row_of[cs] = a
+        n_out[a] = len(cs)
+    col_of = np.full(nd, -1, np.int64)
+    col_of[ins] = np.arange(len(ins))
+    rows, cols = row_of[dc], col_of[dr]
+    ok = (rows >= 0) & (cols >= 0)
+    inter = np.bincount(rows[ok] * len(ins) + cols[ok], minlength=len(outs) * len(ins)).reshape(len(outs), len(ins))
+    mc = np.zeros(n, np.int64)
+    mc[list(main_customers)] = 1
+    intro = np.zeros(n, np.int64)
+    if introduced:
+        intro[list(introduced)] = 1
+    in_mc = np.bincount(dr, weights=mc[dc], minlength=nd).astype(np.int64)[ins][None, :]
+    n_c = np.bincount(dr, weights=intro[dc], minlength=nd).astype(np.int64)[ins][None, :]
+    e = donor_cache["e"][ins][None, :]
+    missing = n_out[:, None] - inter
+    dup = in_mc - inter
+    score = -(e - missing - dup - 10 * n_c)
+    dsig = e + missing + dup
+    oi_a = np.broadcast_to(np.asarray(outs)[:, None], inter.shape)
+    dj_a = np.broadcast_to(np.asarray(ins)[None, :], inter.shape)
+    return score.ravel(), oi_a.ravel(), dj_a.ravel(), dsig.ravel()
+
+
 def route_exchange(population: Sequence, inst, diversity_bandit: DiscountedUCB1, rng,
                    main_index: Optional[int] = None):
     """The exchange half of DCREX (genetic.py:343-405): returns (offspring with
     duplicates removed, unrouted customers, level, sigma, main_index)."""
+    import numpy as np
     if len(population) < 2:
         raise ValueError("crossover needs at least two parents")
     if main_index is None:
@@ -269,22 +321,17 @@ def route_exchange(population: Sequence, inst, diversity_bandit: DiscountedUCB1,
     sigma = 0.0
     for donor in donors:
         used: set = set()
+        cache: dict = {}
         reached = False
         while True:
-            pairs = []
-            for oi, r_out in enumerate(off.routes):
-                if not origin_main[oi]:
-                    continue
-                for dj, r_in in enumerate(donor.routes):
-                    if dj in used or not r_in.customers:
-                        continue
-                    sc = score_route_pair(r_out, r_in, main_edges, main_customers, introduced, inst)
-                    pairs.append((sc.score, oi, dj, sc))
-            if not pairs:
+            ps = _pair_scores(off, origin_main, donor, used, main_edges, main_customers, introduced, inst, cache)
+            if ps is None:
                 break
-            pairs.sort(key=lambda t: (t[0], t[1], t[2]))
-            _, oi, dj, sc = rng.choice(pairs[:5])
-            if sigma + sc.delta_sigma >= sigma_max:
+            score, oi_a, dj_a, dsig = ps
+            top = np.lexsort((dj_a, oi_a, score))[:5]   # pairs.sort(key=(score, oi, dj))[:5]
+            k = top[rng.choice(range(len(top)))]         # rng.choice over the first five
+            oi, dj, ds = int(oi_a[k]), int(dj_a[k]), int(dsig[k])
+            if sigma + ds >= sigma_max:
                 break
             main_customers.difference_update(off.routes[oi].customers)
             del off.routes[oi]
@@ -294,7 +341,7 @@ def route_exchange(population: Sequence, inst, diversity_bandit: DiscountedUCB1,
             origin_main.append(False)
             introduced.update(r_new.customers)
             used.add(dj)
-            sigma += sc.delta_sigma
+            sigma += ds
             if sigma >= sigma_min:
                 reached = True
                 break
