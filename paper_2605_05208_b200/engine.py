@@ -29,7 +29,7 @@ from .evaluation import PenaltyState, ScalingConstants, evaluate, route_attr
 from .genetic import (DIVERSITY_LEVELS, DiscountedUCB1, InsertionOperator, dcrex, improvement_reward,
                       initialize_population, repair_insert, repair_population, route_exchange)
 from .localsearch import SearchConfig, local_search, local_search_population
-from .model import INF, Solution
+from .model import INF, Route, Solution
 from .neighborhood import NeighborConfig, build_device
 from .population import Population
 
@@ -71,6 +71,8 @@ class RunStats:
     stagnation_trace: list = field(default_factory=list)
     offspring: int = 0
     phase_s: dict = field(default_factory=dict)  # wall time per loop phase (run_batched)
+    migrants: int = 0          # elites received from other islands (run_islands)
+    global_best: float = INF   # lowest feasible cost over all islands (run_islands)
 
 
 def gap(f: float, bks: float) -> float:
@@ -183,56 +185,110 @@ def run(inst, cfg: SolverConfig, nbr=None) -> RunStats:
     return R.finish()
 
 
+def _batched_generation(R: "_Run", batch: int, device: int) -> None:
+    """One lock-step generation of `batch` offspring (see the module docstring)."""
+    inst, ph = R.inst, R.stats.phase_s
+    prev = R.stats.best_cost
+    t0 = time.perf_counter()
+    parents = list(R.pop.members)
+    members = [m.sol for m in parents]
+    kids, info = [], []
+    for _ in range(batch):
+        off, unrouted, level, _, main_index = route_exchange(members, inst, R.div_bandit, R.rng)
+        op = InsertionOperator(R.ins_bandit.select())
+        kids.append((off, unrouted))
+        info.append((parents[main_index], level, op))
+    t1 = time.perf_counter()
+    for op in InsertionOperator:  # one device call per operator; RI draws from the run's rng
+        idx = [j for j in range(batch) if info[j][2] == op and kids[j][1]]
+        if not idx:
+            continue
+        if op == InsertionOperator.RI:
+            for j in idx:
+                repair_insert(kids[j][0], kids[j][1], op, inst, R.consts, R.penalties, R.rng)
+        else:
+            repair_population([kids[j][0] for j in idx], [kids[j][1] for j in idx], op, inst, R.consts,
+                              R.penalties, device=device)
+    offspring = []
+    for off, _ in kids:
+        off.drop_empty_routes()
+        for r in off.routes:
+            r.attr = route_attr(r, inst)
+        offspring.append(off)
+    t2 = time.perf_counter()
+    pens = [R.penalties.clone() for _ in offspring]
+    rngs = [random.Random(R.rng.getrandbits(64)) for _ in offspring]
+    local_search_population(offspring, pens, R.search, R.nbr, R.consts, inst, rngs, deadline=R.deadline,
+                            device=device, on_feasible=R.snapshot_feasible)
+    R.penalties.lam[:] = pens[-1].lam
+    t3 = time.perf_counter()
+    for off, (main, level, op) in zip(offspring, info):
+        off.meta["generation"] = R.gen
+        R.absorb(off, main, level, op)
+    R.close_generation(prev)
+    t4 = time.perf_counter()
+    for k, v in (("exchange", t1 - t0), ("repair", t2 - t1), ("local_search", t3 - t2), ("update", t4 - t3)):
+        ph[k] = ph.get(k, 0.0) + v
+
+
 def run_batched(inst, cfg: SolverConfig, batch: int = 64, nbr=None, device: int = 0) -> RunStats:
     """Lock-step generations of `batch` offspring (see the module docstring)."""
     if batch < 1:
         raise ValueError("batch must be >= 1")
     R = _Run(inst, cfg, nbr)
-    ph = R.stats.phase_s
-    for k in ("exchange", "repair", "local_search", "update"):
-        ph[k] = 0.0
     while R.running():
-        prev = R.stats.best_cost
-        t0 = time.perf_counter()
-        parents = list(R.pop.members)
-        members = [m.sol for m in parents]
-        kids, info = [], []
-        for _ in range(batch):
-            off, unrouted, level, _, main_index = route_exchange(members, inst, R.div_bandit, R.rng)
-            op = InsertionOperator(R.ins_bandit.select())
-            kids.append((off, unrouted))
-            info.append((parents[main_index], level, op))
-        t1 = time.perf_counter()
-        for op in InsertionOperator:  # one device call per operator; RI draws from the run's rng
-            idx = [j for j in range(batch) if info[j][2] == op and kids[j][1]]
-            if not idx:
-                continue
-            if op == InsertionOperator.RI:
-                for j in idx:
-                    repair_insert(kids[j][0], kids[j][1], op, inst, R.consts, R.penalties, R.rng)
-            else:
-                repair_population([kids[j][0] for j in idx], [kids[j][1] for j in idx], op, inst, R.consts,
-                                  R.penalties, device=device)
-        offspring = []
-        for off, _ in kids:
-            off.drop_empty_routes()
-            for r in off.routes:
-                r.attr = route_attr(r, inst)
-            offspring.append(off)
-        t2 = time.perf_counter()
-        pens = [R.penalties.clone() for _ in offspring]
-        rngs = [random.Random(R.rng.getrandbits(64)) for _ in offspring]
-        local_search_population(offspring, pens, R.search, R.nbr, R.consts, inst, rngs, deadline=R.deadline,
-                                device=device, on_feasible=R.snapshot_feasible)
-        R.penalties.lam[:] = pens[-1].lam
-        t3 = time.perf_counter()
-        for off, (main, level, op) in zip(offspring, info):
-            off.meta["generation"] = R.gen
-            R.absorb(off, main, level, op)
-        R.close_generation(prev)
-        t4 = time.perf_counter()
-        ph["exchange"] += t1 - t0
-        ph["repair"] += t2 - t1
-        ph["local_search"] += t3 - t2
-        ph["update"] += t4 - t3
+        _batched_generation(R, batch, device)
     return R.finish()
+
+
+def _elite(R: "_Run"):
+    m = R.pop.best(R.penalties, feasible_only=True) or R.pop.best(R.penalties, feasible_only=False)
+    return m.sol, (m.breakdown.D if m.feasible else INF)
+
+
+def run_islands(inst, cfg: SolverConfig, batch: int = 64, exchange_every: int = 1, nbr=None, device: int = 0,
+                group=None, comm_device=None) -> RunStats:
+    """Island model over the ranks of an initialised torch.distributed group:
+    rank r runs `run_batched` generations with seed cfg.seed + r; every
+    `exchange_every` generations the ranks all_gather their elite (best feasible
+    member, else best penalised) as a fixed-size int32 vector -- the only
+    collective -- and each island adds the other islands' elites to its
+    population.  All ranks stop together (a MIN all_reduce of the loop
+    condition).  Returns this rank's RunStats; `global_best` holds the lowest
+    feasible cost over all islands after the last exchange."""
+    import torch
+    import torch.distributed as dist
+    from . import distributed as DS
+    from dataclasses import replace
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    R = _Run(inst, replace(cfg, seed=cfg.seed + rank), nbr)
+    cap = inst.n_customers  # routes with customers never exceed the customer count
+    while True:
+        flag = torch.tensor([1 if R.running() else 0], dtype=torch.int32, device=comm_device)
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=group)
+        if int(flag.item()) == 0:
+            break
+        _batched_generation(R, batch, device)
+        if world > 1 and R.gen % exchange_every == 0:
+            sol, D = _elite(R)
+            routes = [(r.depart, r.arrive, list(r.customers)) for r in sol.routes if r.customers]
+            vecs = DS.exchange_elites(DS.encode_elite(routes, D, inst.n_customers, cap), group=group,
+                                      device=comm_device)
+            for j, v in enumerate(vecs):
+                if j == rank:
+                    continue
+                rts, _ = DS.decode_elite(v)
+                mig = Solution([Route(d, a, c) for d, a, c in rts])
+                mig.meta["migrant_from"] = j
+                bd = evaluate(mig, R.penalties, R.consts, inst)
+                feas = _is_feasible(bd, mig, inst)
+                R.pop.add(mig, bd, feas, inst)
+                if R.pop.needs_selection:
+                    R.pop.survivor_selection(R.penalties)
+                _track_best(R.stats, mig, bd, feas)
+                R.stats.migrants += 1
+    st = R.finish()
+    best = torch.tensor([st.best_cost], dtype=torch.float64, device=comm_device)
+    dist.all_reduce(best, op=dist.ReduceOp.MIN, group=group)
+    st.global_best = float(best.item())
+    return st

@@ -40,8 +40,7 @@ def _check(st, want):
     assert _routes(st.best_infeasible) == want["best_infeasible"]
 
 
-@pytest.fixture
-def oracle_kernels(monkeypatch):
+def _oracle_kernels(setattr_):
     """Route the loop's two device calls through the oracle (CPU)."""
     cache = {}
 
@@ -66,6 +65,11 @@ def oracle_kernels(monkeypatch):
             on_feasible(st["best_feasible_D"], snap)
         return sol
 
+    def local_search_population(sols, penalties, cfg, nbr, consts, inst, rngs, deadline=None, device=0,
+                                on_feasible=None):
+        for s, p, r in zip(sols, penalties, rngs):
+            local_search(s, p, cfg, nbr, consts, inst, r, deadline, on_feasible)
+
     def repair_population(sols, unrouteds, op, inst, consts, penalties, device=0):
         if not isinstance(penalties, (list, tuple)):
             penalties = [penalties] * len(sols)
@@ -75,9 +79,16 @@ def oracle_kernels(monkeypatch):
             GN._write_back(s, O.repair(oi, s, u, int(op), p.lam)[0])
         return [dict(inserted=len(u)) for u in unrouteds]
 
-    monkeypatch.setattr(E, "local_search", local_search)
-    monkeypatch.setattr(GN, "repair_population", repair_population)
-    monkeypatch.setattr(E, "build_device", build)
+    setattr_(E, "local_search", local_search)
+    setattr_(E, "local_search_population", local_search_population)
+    setattr_(E, "repair_population", repair_population)
+    setattr_(GN, "repair_population", repair_population)
+    setattr_(E, "build_device", build)
+
+
+@pytest.fixture
+def oracle_kernels(monkeypatch):
+    _oracle_kernels(monkeypatch.setattr)
 
 
 @pytest.mark.parametrize("tag", sorted(GOLD))
@@ -110,3 +121,42 @@ def test_batched_engine_runs_and_keeps_coverage():
     bd = evaluate(st.best, PenaltyState(), ScalingConstants.from_instance(inst), inst)
     assert max(bd.V1, bd.V2, bd.V3, bd.V4) <= 1e-9
     assert abs(bd.D - st.best_cost) <= 1e-9 * max(1.0, bd.D)
+
+
+def _island_worker(rank, world, port, q):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    _oracle_kernels(setattr)
+    want = GOLD["tw_mm"]
+    inst = _instance(want["instance"])
+    cfg = E.SolverConfig(**dict(want["config"], generations=3, depth=20))
+    st = E.run_islands(inst, cfg, batch=3, exchange_every=2)
+    q.put((rank, st.generations, st.offspring, st.migrants, st.best_cost, st.global_best))
+    dist.destroy_process_group()
+
+
+def test_islands_gloo_world2_exchange_elites():
+    """Island model host logic on CPU (gloo, 2 ranks, oracle kernels): both
+    islands stop together, receive one migrant per exchange, and agree on the
+    global best."""
+    import socket
+    import torch.multiprocessing as mp
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_island_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=300) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    (_, g0, o0, m0, b0, gb0), (_, g1, o1, m1, b1, gb1) = res
+    assert g0 == g1 == 4 and o0 == o1 == 12
+    assert m0 == m1 == 2  # exchanges after generations 2 and 4
+    assert gb0 == gb1 == min(b0, b1)
