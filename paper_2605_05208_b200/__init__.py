@@ -19,7 +19,7 @@ from .localsearch import (DeviceSearch, SearchConfig, apply_moves, enabled_opera
                           local_search, local_search_population, select_moves)
 from .genetic import InsertionOperator, repair_insert, repair_population
 from .formats import ParseError, parse_instance, read_solution, write_solution
-from .engine import RunStats, SolverConfig, run, run_batched
+from .engine import RunStats, SolverConfig, run, run_batched, run_islands
 
 __all__ = [
     "INF", "Instance", "Node", "Route", "Solution", "Variant", "LAMBDA_MAX", "LAMBDA_MIN", "PenaltyState",
@@ -30,5 +30,5 @@ __all__ = [
     "evaluate_batch", "local_search", "local_search_population", "select_moves",
     "InsertionOperator", "repair_insert", "repair_population",
     "ParseError", "parse_instance", "read_solution", "write_solution",
-    "RunStats", "SolverConfig", "run", "run_batched",
+    "RunStats", "SolverConfig", "run", "run_batched", "run_islands",
 ]
