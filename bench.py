@@ -335,10 +335,10 @@ def main():
         its first) as a fixed-size int32 encoding -- the only collective of the job."""
         if world == 1:
             return None
-        routes_all, _ = pop.download(sh)
         Ds = [s["best_feasible_D"] for s in st]
         best = int(np.argmin(Ds))
-        enc = DS.encode_elite(routes_all[best], Ds[best], inst.n_customers, J)
+        routes = pop.download_range(best, 1, sh)[0]  # the elite only
+        enc = DS.encode_elite(routes, Ds[best], inst.n_customers, J)
         return DS.best_of(DS.exchange_elites(enc, device=dev))
 
     for _ in range(args.warmup):

@@ -127,6 +127,10 @@ int mdr_pop_upload(mdr_pop *pop, int32_t B, const int32_t *rbase, const int32_t 
 int mdr_pop_download(mdr_pop *pop, int32_t *rbase, int32_t *coff, int32_t *cust, int32_t *dep,
                      int32_t *arr, double *lam, int32_t *n_routes, int32_t *n_cust, void *stream);
 /* best feasible snapshot per individual (routes when D improved); same layout */
+/* individuals b0 .. b0+nb-1 only (e.g. one elite for the exchange), same layout
+ * as mdr_pop_download with rbase [nb+1] */
+int mdr_pop_download_range(mdr_pop *pop, int32_t b0, int32_t nb, int32_t *rbase, int32_t *coff, int32_t *cust,
+                           int32_t *dep, int32_t *arr, int32_t *n_routes, int32_t *n_cust, void *stream);
 int mdr_pop_download_best(mdr_pop *pop, int32_t *rbase, int32_t *coff, int32_t *cust, int32_t *dep,
                           int32_t *arr, double *bestD, int32_t *n_routes, int32_t *n_cust,
                           void *stream);

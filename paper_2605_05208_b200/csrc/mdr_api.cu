@@ -359,15 +359,15 @@ int mdr_pop_upload(mdr_pop *p, int32_t B, const int32_t *rbase, const int32_t *c
 }
 
 static int download_impl(mdr_pop *p, int best, int32_t *rbase, int32_t *coff, int32_t *cust, int32_t *dep,
-                         int32_t *arr, int32_t *n_routes, int32_t *n_cust, cudaStream_t s) {
-  int B = p->B;
+                         int32_t *arr, int32_t *n_routes, int32_t *n_cust, cudaStream_t s, int b0 = 0, int nb = -1) {
+  int B = nb < 0 ? p->B : nb;
   int cap_r = *n_routes, cap_c = *n_cust;
   size_t need = (size_t)(B + 1) + (cap_r + 1) + cap_c + 2 * (size_t)cap_r;
   int rc = ensure_xfer(p, need);
   if (rc) return rc;
   int *d_rbase = p->d_xfer, *d_coff = d_rbase + B + 1, *d_cust = d_coff + cap_r + 1, *d_dep = d_cust + cap_c,
       *d_arr = d_dep + cap_r;
-  launch_pack(p->P, B, best, d_rbase, d_coff, d_cust, d_dep, d_arr, p->d_hdr, cap_r, cap_c, s);
+  launch_pack(p->P, b0, B, best, d_rbase, d_coff, d_cust, d_dep, d_arr, p->d_hdr, cap_r, cap_c, s);
   CK(cudaGetLastError());
   CK(cudaMemcpyAsync(p->h_hdr, p->d_hdr, 2 * sizeof(int), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
@@ -399,6 +399,13 @@ int mdr_pop_download(mdr_pop *p, int32_t *rbase, int32_t *coff, int32_t *cust, i
     CK(cudaStreamSynchronize(s));
   }
   return MDR_OK;
+}
+
+int mdr_pop_download_range(mdr_pop *p, int32_t b0, int32_t nb, int32_t *rbase, int32_t *coff, int32_t *cust,
+                           int32_t *dep, int32_t *arr, int32_t *n_routes, int32_t *n_cust, void *stream) {
+  if (!p || b0 < 0 || nb < 0 || b0 + nb > p->B) return fail(MDR_ERR_ARG, "individual range out of bounds");
+  CK(cudaSetDevice(p->inst->device));
+  return download_impl(p, 0, rbase, coff, cust, dep, arr, n_routes, n_cust, (cudaStream_t)stream, b0, nb);
 }
 
 int mdr_pop_download_best(mdr_pop *p, int32_t *rbase, int32_t *coff, int32_t *cust, int32_t *dep, int32_t *arr,

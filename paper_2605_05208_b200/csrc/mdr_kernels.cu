@@ -926,12 +926,13 @@ __global__ void k_unpack(DevInst I, DevPop P, int B, const int *rbase, const int
 }
 
 // one CTA: flat arrays of all B individuals; hdr = {routes, customers}
-__global__ void __launch_bounds__(1024) k_pack(DevPop P, int B, int best, int *rbase, int *coff, int *cust,
+__global__ void __launch_bounds__(1024) k_pack(DevPop P, int b0, int B, int best, int *rbase, int *coff, int *cust,
                                                int *dep, int *arr, int *hdr, int cap_r, int cap_c) {
   __shared__ int s_r, s_c;
-  const int *M = best ? P.best_m : P.m;
-  const int4 *RM = best ? P.best_meta : P.rmeta;
-  const int *SQ = best ? P.best_seq : P.seq;
+  // individuals b0 .. b0+B-1
+  const int *M = (best ? P.best_m : P.m) + b0;
+  const int4 *RM = (best ? P.best_meta : P.rmeta) + (size_t)b0 * P.J;
+  const int *SQ = (best ? P.best_seq : P.seq) + (size_t)b0 * P.J * P.Kp;
   if (threadIdx.x == 0) {
     int r = 0, c = 0;
     for (int b = 0; b < B; b++) {
@@ -1130,9 +1131,9 @@ void launch_unpack(const DevInst &I, const DevPop &P, int B, const int *rbase, c
   k_unpack<<<B, 256, 0, s>>>(I, P, B, rbase, coff, cust, dep, arr);
 }
 
-void launch_pack(const DevPop &P, int B, int best, int *rbase, int *coff, int *cust, int *dep, int *arr, int *hdr,
-                 int cap_r, int cap_c, cudaStream_t s) {
-  k_pack<<<1, 1024, 0, s>>>(P, B, best, rbase, coff, cust, dep, arr, hdr, cap_r, cap_c);
+void launch_pack(const DevPop &P, int b0, int B, int best, int *rbase, int *coff, int *cust, int *dep, int *arr,
+                 int *hdr, int cap_r, int cap_c, cudaStream_t s) {
+  k_pack<<<1, 1024, 0, s>>>(P, b0, B, best, rbase, coff, cust, dep, arr, hdr, cap_r, cap_c);
 }
 
 void launch_lf_prep(const MatCands &c, const MatDeltas &d, unsigned long long *ord, unsigned long long *key,

@@ -35,7 +35,7 @@ void launch_lf_prep(const MatCands &c, const MatDeltas &d, unsigned long long *o
 int eval_grid_size(bool win);
 void launch_unpack(const DevInst &I, const DevPop &P, int B, const int *rbase, const int *coff, const int *cust,
                    const int *dep, const int *arr, cudaStream_t s);
-void launch_pack(const DevPop &P, int B, int best, int *rbase, int *coff, int *cust, int *dep, int *arr, int *hdr,
+void launch_pack(const DevPop &P, int b0, int B, int best, int *rbase, int *coff, int *cust, int *dep, int *arr, int *hdr,
                  int cap_r, int cap_c, cudaStream_t s);
 
 }  // namespace mdr

@@ -151,6 +151,23 @@ class Population:
         routes, lam = self._download(False, stream)
         return routes, lam.reshape(-1, 4)[:self.B]
 
+    def download_range(self, b0: int, nb: int, stream=None):
+        """Routes of individuals b0 .. b0+nb-1 only (mdr_pop_download_range)."""
+        cap_r = max(nb * self.J_cap, 1)
+        cap_c = max(self.n_cust, 1) + 16
+        rbase = np.zeros(nb + 1, np.int32)
+        coff = np.zeros(cap_r + 1, np.int32)
+        cust = np.zeros(cap_c, np.int32)
+        dep = np.zeros(cap_r, np.int32)
+        arr = np.zeros(cap_r, np.int32)
+        nr, nc = C.c_int32(cap_r), C.c_int32(cap_c)
+        s = stream if stream is not None else _cur_stream(self.dinst.device)
+        check(_lib.lib().mdr_pop_download_range(self.handle, b0, nb, ptr(rbase, i32p), ptr(coff, i32p),
+                                                ptr(cust, i32p), ptr(dep, i32p), ptr(arr, i32p), C.byref(nr),
+                                                C.byref(nc), s), "mdr_pop_download_range")
+        cl, ol, dl, al = cust.tolist(), coff.tolist(), dep.tolist(), arr.tolist()
+        return [[(dl[r], al[r], cl[ol[r]:ol[r + 1]]) for r in range(rbase[b], rbase[b + 1])] for b in range(nb)]
+
     def download_best(self, stream=None):
         routes, bestD = self._download(True, stream)
         return routes, bestD[:self.B]

@@ -350,3 +350,17 @@ def test_totals_pairwise_sum_many_routes():
             assert len(sol.routes) > 300
             cache = P.SolutionCache(sol, inst, consts)
             assert [x.hex() for x in cache.totals()] == [x.hex() for x in O.totals(oi, sol)]
+
+
+@pytest.mark.gpu
+def test_download_range_matches_full_download():
+    inst, consts, nbr, sols = _synthetic_states("mdvrptw", 40, 3, 77, 7)
+    dinst = DeviceInstance(inst, consts, nbr)
+    J, K = Population.caps_for(sols, inst)
+    pop = Population(dinst, 7, J, K)
+    pop.upload(sols, [[1.0] * 4] * 7)
+    full, _ = pop.download()
+    for b0, nb in ((0, 7), (3, 1), (6, 1), (2, 3), (4, 0)):
+        assert pop.download_range(b0, nb) == full[b0:b0 + nb]
+    with pytest.raises(ValueError):
+        pop.download_range(5, 3)
