@@ -60,7 +60,8 @@ def make_workload(name, ids):
     inst, _ = W.appendix_a_instance(spec)
     consts = ScalingConstants.from_instance(inst)
     nbr = build(inst, NeighborConfig(spec.theta), consts)
-    workers = max(1, min(len(ids), (os.cpu_count() or 2) - 1, 64))
+    world = int(os.environ.get("WORLD_SIZE", "1"))  # ranks share the host: split its cores
+    workers = max(1, min(len(ids), (os.cpu_count() or 2) // world - 1, 64))
     if workers > 1:
         with ProcessPoolExecutor(workers) as ex:
             raw = list(ex.map(_init_one, [(name, i) for i in ids], chunksize=4))
