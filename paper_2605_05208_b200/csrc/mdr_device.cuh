@@ -78,9 +78,11 @@ struct DevPop {
   int *opb;                   // [6][Bcap] individual ids per operator
   int *opoff;                 // [6][Bcap+1] first task of each individual within its operator
   ulonglong2 *leader;         // [B] running min {ord(dF), key} of the round
-  ulonglong2 *gq;             // [Gcap] generic-path queue {key, b | op << 24}
-  int *gcount;                // [1]
-  int Gcap;
+  ulonglong2 *gq;             // [Gcap] generic-path queue {key, b | op << 24}: region A [0, GcapA)
+                              // (2-opt, depot ops: drained while the staged evaluators run), region B
+                              // [GcapA, Gcap) (intra-route relocate/swap: drained after them)
+  int *gcount;                // [2] entries queued in region A, B
+  int Gcap, GcapA;
   int *tcount;                // [max tasks] candidates per task
   ulonglong2 *partial;        // [max tasks] {ord(dF), key}
   ulonglong2 *fol;            // [B][Fcap]

@@ -162,14 +162,18 @@ __device__ __forceinline__ unsigned long long key_of(int r1, int p1, int r2, int
 __device__ __forceinline__ void enqueue_g(const DevPop &P, int b, int op, bool q, unsigned long long key) {
   unsigned qm = __ballot_sync(0xffffffffu, q);
   if (!qm) return;
+  // 2-opt / depot ops -> A when region A exists (GcapA > 0), everything else -> B
+  const int region = (op >= 3 && P.GcapA > 0) ? 0 : 1;
+  const int cap = region ? P.Gcap - P.GcapA : P.GcapA;
+  ulonglong2 *Q = P.gq + (region ? P.GcapA : 0);
   int lane = threadIdx.x & 31;
   int leader = __ffs(qm) - 1;
   int base = 0;
-  if (lane == leader) base = atomicAdd(P.gcount, __popc(qm));
+  if (lane == leader) base = atomicAdd(P.gcount + region, __popc(qm));
   base = __shfl_sync(0xffffffffu, base, leader);
   if (q) {
     int at = base + __popc(qm & ((1u << lane) - 1));
-    if (at < P.Gcap) P.gq[at] = make_ulonglong2(key, (unsigned long long)(b | (op << 24)));
+    if (at < cap) Q[at] = make_ulonglong2(key, (unsigned long long)(b | (op << 24)));
   }
 }
 

@@ -274,7 +274,8 @@ __global__ void __launch_bounds__(1024) k_plan(DevInst I, DevPop P, LsParams L) 
   }
   if (threadIdx.x == 0) {
     *P.active = 0;
-    *P.gcount = 0;
+    P.gcount[0] = 0;
+    P.gcount[1] = 0;
   }
 }
 
@@ -442,9 +443,11 @@ template <bool WIN>
 #ifndef MDR_GMINB
 #define MDR_GMINB 3
 #endif
-__global__ void __launch_bounds__(256, MDR_GMINB) k_eval_g(DevInst I, DevPop P, LsParams L) {
+__global__ void __launch_bounds__(256, MDR_GMINB) k_eval_g(DevInst I, DevPop P, LsParams L, int region) {
   const int lane = threadIdx.x & 31;
-  const int total = min(*P.gcount, P.Gcap);
+  // region 0: A [0, GcapA), 1: B [GcapA, Gcap) (everything when GcapA == 0)
+  const int total = min(P.gcount[region], region ? P.Gcap - P.GcapA : P.GcapA);
+  const ulonglong2 *Q = P.gq + (region ? P.GcapA : 0);
   const bool mm = L.multi_move != 0;
   const int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
@@ -455,7 +458,7 @@ __global__ void __launch_bounds__(256, MDR_GMINB) k_eval_g(DevInst I, DevPop P, 
     unsigned long long key = 0, o = ~0ull;
     bool fol = false;
     if (valid) {
-      ulonglong2 e = P.gq[i];
+      ulonglong2 e = Q[i];
       key = e.x;
       b = (int)(e.y & 0xffffffu);
       op = (int)(e.y >> 24);
@@ -638,7 +641,10 @@ __global__ void __launch_bounds__(256) k_select(DevInst I, DevPop P, LsParams L)
     P.st[b].op_evals++;
     s_flag = 0;
     if (has && L.multi_move && nf > P.Fcap) { s_flag = 1; P.st[b].need_f = nf; }  // follower buffer overflow
-    if (*P.gcount > P.Gcap) { s_flag = 1; P.st[b].need_g = *P.gcount; }         // generic queue overflow
+    if (P.gcount[0] > P.GcapA || P.gcount[1] > P.Gcap - P.GcapA) {  // generic queue overflow
+      s_flag = 1;
+      P.st[b].need_g = 2 * max(P.gcount[0], P.gcount[1]);
+    }
   }
   __syncthreads();
   if (s_flag) {
@@ -1005,6 +1011,29 @@ static int grid_for(K kern) {
 
 int eval_grid_size(bool win) { return win ? grid_for(k_eval<true, 0>) : grid_for(k_eval<false, 0>); }
 
+// Drain generic-queue region A (2-opt, depot operators) concurrently with the
+// staged evaluators only when those leave the GPU under-filled (few CTA tasks
+// per round: small populations / instances); otherwise it would just compete
+// with them, and both regions are drained in one pass after the join.
+bool generic_overlap(const DevInst &I, const DevPop &P) {
+  static int slots = 0;
+  if (!slots) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    slots = sms * MDR_CMINB;
+  }
+  const long long tasks = (long long)P.Bcap * ((I.NC + MDR_CT - 1) / MDR_CT) / 5;  // per operator kernel
+  return P.staged && tasks < 8LL * slots;
+}
+
+template <bool WIN>
+static void launch_eval_g_region(const DevInst &I, const DevPop &P, const LsParams &L, cudaStream_t s, int region) {
+  static int g = 0;  // full occupancy of the (latency-bound) generic evaluator
+  if (!g) g = grid_for(k_eval_g<WIN>);
+  k_eval_g<WIN><<<g, 256, 0, s>>>(I, P, L, region);
+}
+
 template <bool WIN>
 static void launch_eval_t(const DevInst &I, const DevPop &P, const LsParams &L, cudaStream_t s, const cudaStream_t *side,
                           cudaEvent_t *ev) {
@@ -1055,18 +1084,30 @@ static void launch_eval_t(const DevInst &I, const DevPop &P, const LsParams &L, 
     k_eval_c<WIN, 0><<<gc[0], 32 * MDR_CU, sm, side[0]>>>(I, P, L);
     k_eval_c<WIN, 1><<<gc[1], 32 * MDR_CU, sm, side[1]>>>(I, P, L);
     k_eval_c<WIN, 2><<<gc[2], 32 * MDR_CU, sm, side[2]>>>(I, P, L);
+    const bool ov = P.GcapA > 0;  // decided at mdr_pop_create (generic_overlap)
+    if (ov) {  // meanwhile on s: 2-opt / depot enumeration and their generic-path evaluation (region A)
+      if (!WIN) k_eval<WIN, 3><<<g[3], 256, 0, s>>>(I, P, L);
+      k_eval<WIN, 4><<<g[4], 256, 0, s>>>(I, P, L);
+      k_eval<WIN, 5><<<g[5], 256, 0, s>>>(I, P, L);
+      launch_eval_g_region<WIN>(I, P, L, s, 0);
+    }
     for (int q = 0; q < 3; q++) {
       cudaEventRecord(ev[1 + q], side[q]);
       cudaStreamWaitEvent(s, ev[1 + q], 0);
+    }
+    if (!ov) {  // the staged evaluators fill the GPU: enumerate after them into the single queue
+      if (!WIN) k_eval<WIN, 3><<<g[3], 256, 0, s>>>(I, P, L);
+      k_eval<WIN, 4><<<g[4], 256, 0, s>>>(I, P, L);
+      k_eval<WIN, 5><<<g[5], 256, 0, s>>>(I, P, L);
     }
   } else {
     k_eval<WIN, 0><<<g[0], 256, 0, s>>>(I, P, L);
     k_eval<WIN, 1><<<g[1], 256, 0, s>>>(I, P, L);
     k_eval<WIN, 2><<<g[2], 256, 0, s>>>(I, P, L);
+    if (!WIN) k_eval<WIN, 3><<<g[3], 256, 0, s>>>(I, P, L);
+    k_eval<WIN, 4><<<g[4], 256, 0, s>>>(I, P, L);
+    k_eval<WIN, 5><<<g[5], 256, 0, s>>>(I, P, L);
   }
-  if (!WIN) k_eval<WIN, 3><<<g[3], 256, 0, s>>>(I, P, L);
-  k_eval<WIN, 4><<<g[4], 256, 0, s>>>(I, P, L);
-  k_eval<WIN, 5><<<g[5], 256, 0, s>>>(I, P, L);
 }
 
 void launch_eval(const DevInst &I, const DevPop &P, const LsParams &L, int grid, bool win, cudaStream_t s,
@@ -1077,15 +1118,9 @@ void launch_eval(const DevInst &I, const DevPop &P, const LsParams &L, int grid,
 }
 
 void launch_eval_g(const DevInst &I, const DevPop &P, const LsParams &L, int grid, bool win, cudaStream_t s) {
-  (void)grid;
-  static int gt = 0, gf = 0;  // full occupancy of the (latency-bound) generic evaluator
-  if (win) {
-    if (!gt) gt = grid_for(k_eval_g<true>);
-    k_eval_g<true><<<gt, 256, 0, s>>>(I, P, L);
-  } else {
-    if (!gf) gf = grid_for(k_eval_g<false>);
-    k_eval_g<false><<<gf, 256, 0, s>>>(I, P, L);
-  }
+  (void)grid;  // region B: intra-route relocate / swap (and, without region A, everything else)
+  if (win) launch_eval_g_region<true>(I, P, L, s, 1);
+  else launch_eval_g_region<false>(I, P, L, s, 1);
 }
 
 void launch_select(const DevInst &I, const DevPop &P, const LsParams &L, bool win, cudaStream_t s) {
