@@ -245,7 +245,7 @@ int mdr_pop_create(mdr_instance *inst, int32_t Bcap, int32_t J, int32_t K, int32
   DA(A, P.opb, (size_t)6 * Bcap);
   DA(A, P.opoff, (size_t)6 * (Bcap + 1));
   DA(A, P.leader, Bcap);
-  DA(A, P.gcount, 2);
+  DA(A, P.gcount, 3);
   {
     long long g = (long long)Bcap * std::max((long long)I.NC * 64, (long long)Fcap);
     if (g > 0x7fffffffLL) g = 0x7fffffffLL;
@@ -254,8 +254,11 @@ int mdr_pop_create(mdr_instance *inst, int32_t Bcap, int32_t J, int32_t K, int32
   DA(A, P.gq, (size_t)P.Gcap);
   // region A of the generic queue (drained concurrently with the staged
   // evaluators) only when those leave the GPU under-filled
-  P.GcapA = 0;
-  if (generic_overlap(I, P) && !getenv("MDR_NO_OVERLAP")) P.GcapA = P.Gcap / 2;
+  P.gbase[0] = 0; P.gbase[1] = 0; P.gbase[2] = P.Gcap; P.gbase[3] = P.Gcap;
+  if (generic_overlap(I, P) && !getenv("MDR_NO_OVERLAP")) {
+    P.gbase[1] = P.Gcap / 3;
+    P.gbase[2] = 2 * (P.Gcap / 3);
+  }
   DA(A, P.fol, (size_t)Bcap * Fcap);
   DA(A, P.fcount, Bcap);
   DA(A, P.nanflag, Bcap);

@@ -78,11 +78,12 @@ struct DevPop {
   int *opb;                   // [6][Bcap] individual ids per operator
   int *opoff;                 // [6][Bcap+1] first task of each individual within its operator
   ulonglong2 *leader;         // [B] running min {ord(dF), key} of the round
-  ulonglong2 *gq;             // [Gcap] generic-path queue {key, b | op << 24}: region A [0, GcapA)
-                              // (2-opt, depot ops: drained while the staged evaluators run), region B
-                              // [GcapA, Gcap) (intra-route relocate/swap: drained after them)
-  int *gcount;                // [2] entries queued in region A, B
-  int Gcap, GcapA;
+  ulonglong2 *gq;             // [Gcap] generic-path queue {key, b | op << 24}; region r = [gbase[r], gbase[r+1]):
+                              // overlap mode: 0 = 2-opt/depot ops, 1 = intra-route relocate, 2 = intra-route
+                              // swap, each drained right behind its producer; otherwise region 1 holds all
+  int *gcount;                // [3] entries queued per region
+  int Gcap;
+  int gbase[4];
   int *tcount;                // [max tasks] candidates per task
   ulonglong2 *partial;        // [max tasks] {ord(dF), key}
   ulonglong2 *fol;            // [B][Fcap]

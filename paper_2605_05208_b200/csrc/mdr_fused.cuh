@@ -162,10 +162,9 @@ __device__ __forceinline__ unsigned long long key_of(int r1, int p1, int r2, int
 __device__ __forceinline__ void enqueue_g(const DevPop &P, int b, int op, bool q, unsigned long long key) {
   unsigned qm = __ballot_sync(0xffffffffu, q);
   if (!qm) return;
-  // 2-opt / depot ops -> A when region A exists (GcapA > 0), everything else -> B
-  const int region = (op >= 3 && P.GcapA > 0) ? 0 : 1;
-  const int cap = region ? P.Gcap - P.GcapA : P.GcapA;
-  ulonglong2 *Q = P.gq + (region ? P.GcapA : 0);
+  const int region = P.gbase[1] > 0 ? (op >= 3 ? 0 : (op == 0 ? 1 : 2)) : 1;  // see DevPop::gq
+  const int cap = P.gbase[region + 1] - P.gbase[region];
+  ulonglong2 *Q = P.gq + P.gbase[region];
   int lane = threadIdx.x & 31;
   int leader = __ffs(qm) - 1;
   int base = 0;

@@ -276,6 +276,7 @@ __global__ void __launch_bounds__(1024) k_plan(DevInst I, DevPop P, LsParams L) 
     *P.active = 0;
     P.gcount[0] = 0;
     P.gcount[1] = 0;
+    P.gcount[2] = 0;
   }
 }
 
@@ -445,9 +446,8 @@ template <bool WIN>
 #endif
 __global__ void __launch_bounds__(256, MDR_GMINB) k_eval_g(DevInst I, DevPop P, LsParams L, int region) {
   const int lane = threadIdx.x & 31;
-  // region 0: A [0, GcapA), 1: B [GcapA, Gcap) (everything when GcapA == 0)
-  const int total = min(P.gcount[region], region ? P.Gcap - P.GcapA : P.GcapA);
-  const ulonglong2 *Q = P.gq + (region ? P.GcapA : 0);
+  const int total = min(P.gcount[region], P.gbase[region + 1] - P.gbase[region]);
+  const ulonglong2 *Q = P.gq + P.gbase[region];
   const bool mm = L.multi_move != 0;
   const int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
@@ -641,10 +641,12 @@ __global__ void __launch_bounds__(256) k_select(DevInst I, DevPop P, LsParams L)
     P.st[b].op_evals++;
     s_flag = 0;
     if (has && L.multi_move && nf > P.Fcap) { s_flag = 1; P.st[b].need_f = nf; }  // follower buffer overflow
-    if (P.gcount[0] > P.GcapA || P.gcount[1] > P.Gcap - P.GcapA) {  // generic queue overflow
-      s_flag = 1;
-      P.st[b].need_g = 2 * max(P.gcount[0], P.gcount[1]);
+    int gneed = 0;  // generic queue overflow: the region sizes scale with Gcap
+    for (int r = 0; r < 3; r++) {
+      const int cap = P.gbase[r + 1] - P.gbase[r];
+      if (P.gcount[r] > cap) gneed = max(gneed, (int)((long long)P.gcount[r] * P.Gcap / max(cap, 1)) + 1);
     }
+    if (gneed) { s_flag = 1; P.st[b].need_g = gneed; }
   }
   __syncthreads();
   if (s_flag) {
@@ -1084,7 +1086,12 @@ static void launch_eval_t(const DevInst &I, const DevPop &P, const LsParams &L, 
     k_eval_c<WIN, 0><<<gc[0], 32 * MDR_CU, sm, side[0]>>>(I, P, L);
     k_eval_c<WIN, 1><<<gc[1], 32 * MDR_CU, sm, side[1]>>>(I, P, L);
     k_eval_c<WIN, 2><<<gc[2], 32 * MDR_CU, sm, side[2]>>>(I, P, L);
-    const bool ov = P.GcapA > 0;  // decided at mdr_pop_create (generic_overlap)
+    const bool ov0 = P.gbase[1] > 0;
+    if (ov0) {  // each producer's intra-route queue drained right behind it, on its branch
+      launch_eval_g_region<WIN>(I, P, L, side[0], 1);
+      launch_eval_g_region<WIN>(I, P, L, side[1], 2);
+    }
+    const bool ov = P.gbase[1] > 0;  // decided at mdr_pop_create (generic_overlap)
     if (ov) {  // meanwhile on s: 2-opt / depot enumeration and their generic-path evaluation (region A)
       if (!WIN) k_eval<WIN, 3><<<g[3], 256, 0, s>>>(I, P, L);
       k_eval<WIN, 4><<<g[4], 256, 0, s>>>(I, P, L);
@@ -1118,7 +1125,8 @@ void launch_eval(const DevInst &I, const DevPop &P, const LsParams &L, int grid,
 }
 
 void launch_eval_g(const DevInst &I, const DevPop &P, const LsParams &L, int grid, bool win, cudaStream_t s) {
-  (void)grid;  // region B: intra-route relocate / swap (and, without region A, everything else)
+  (void)grid;  // single-queue mode only: overlap mode drains every region inside launch_eval
+  if (P.gbase[1] > 0) return;
   if (win) launch_eval_g_region<true>(I, P, L, s, 1);
   else launch_eval_g_region<false>(I, P, L, s, 1);
 }

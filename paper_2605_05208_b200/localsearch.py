@@ -135,10 +135,10 @@ class DeviceSearch:
     def _ensure(self, sols, need=None):
         J, K = Population.caps_for(sols, self.inst)
         F = 1 << 15
-        if need:  # grow exactly what the failed attempt reported (at least doubling it)
+        if need:  # grow what the failed attempt reported (at least doubling it); never shrink
             p = self.pop
-            J = max(J, 2 * p.J_cap if need["J"] else J, need["J"] + 64)
-            K = max(K, need["K"])
+            J = max(J, p.J_cap, 2 * p.J_cap if need["J"] else J, need["J"] + 64)
+            K = max(K, p.K_cap, need["K"])
             F = max(F, p.F_cap * 2 if (need["F"] or need["G"]) else p.F_cap, need["F"] + 1024,
                     (need["G"] + 1024) // max(len(sols), 1))
         J, K = min(4094, J), min(500, K)
