@@ -9,7 +9,6 @@ individuals' route storage and subsequence tables on that GPU
 from __future__ import annotations
 
 import ctypes as C
-import math
 import weakref
 
 import numpy as np

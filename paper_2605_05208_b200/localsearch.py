@@ -14,7 +14,6 @@ Each individual's trajectory is bit-identical to a separate reference call.
 from __future__ import annotations
 
 import ctypes as C
-import random
 import time
 from dataclasses import dataclass
 from typing import Optional

@@ -11,7 +11,6 @@ parity tests use.
 """
 from __future__ import annotations
 
-import math
 import random
 from dataclasses import dataclass
 

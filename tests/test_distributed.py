@@ -3,8 +3,6 @@ import os
 import random
 import socket
 
-import numpy as np
-import pytest
 import torch.multiprocessing as mp
 
 from paper_2605_05208_b200 import distributed as D

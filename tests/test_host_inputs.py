@@ -10,7 +10,7 @@ import golden_io as G
 from paper_2605_05208_b200 import workload as W
 from paper_2605_05208_b200.device import Population, flatten_population
 from paper_2605_05208_b200.evaluation import PenaltyState, ScalingConstants, adapt_penalties
-from paper_2605_05208_b200.model import Route, Solution, flatten, unflatten
+from paper_2605_05208_b200.model import Route, flatten, unflatten
 from paper_2605_05208_b200.neighborhood import NeighborConfig, build
 
 

@@ -4,7 +4,6 @@ path (mdr_repair) against the reference's own repair_insert outputs
 import random
 import zlib
 
-import numpy as np
 import pytest
 
 import repair_io as R

@@ -1,5 +1,5 @@
 """Time Population creation vs repair call for the C4 batched-engine shapes."""
-import os, sys, time, random
+import os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import bench
 from paper_2605_05208_b200.device import Population
