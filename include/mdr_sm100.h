@@ -172,6 +172,11 @@ typedef struct mdr_repair_stats {
 int mdr_repair(mdr_pop *pop, int32_t op, const int32_t *pend_off, const int32_t *pend, mdr_repair_stats *stats,
                void *stream);
 
+/* evaluation.evaluate (evaluation.py:206-224) of individuals 0..B-1 with the
+ * reference's scalar semantics: out[b*6 .. +6] = {D, V1, V2, V3, V4, F}, F under
+ * lam[b*4 .. +4] (NULL: the population's own lambda). */
+int mdr_pop_breakdown(mdr_pop *pop, const double *lam, double *out, void *stream);
+
 /* Granular neighbour lists on the device; replaces neighborhood.build
  * (neighborhood.py:60-101).  Host buffers: dist/time [n*n] (time NULL or ==
  * dist: alias), tw_early/tw_late/service [n]; out lists [n*theta] (-1 padded,

@@ -110,6 +110,7 @@ def lib():
         L.mdr_probe_fp64_gops.argtypes = [C.c_int32, C.c_int32, f64p]
         L.mdr_pop_download_range.argtypes = [vp, C.c_int32, C.c_int32, i32p, i32p, i32p, i32p, i32p,
                                              C.POINTER(C.c_int32), C.POINTER(C.c_int32), vp]
+        L.mdr_pop_breakdown.argtypes = [vp, f64p, f64p, vp]
         L.mdr_repair.argtypes = [vp, C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.POINTER(RepairStats),
                                  vp]
         L.mdr_neighbor_build.argtypes = [C.c_int32, C.c_int32, C.c_int32, f64p, f64p, f64p, f64p, f64p, C.c_double,
@@ -146,4 +147,5 @@ EXPORTED = ("mdr_last_error", "mdr_device_count", "mdr_build_info", "mdr_instanc
             "mdr_pop_download", "mdr_pop_download_best", "mdr_count", "mdr_enumerate", "mdr_evaluate",
             "mdr_leader_followers", "mdr_totals", "mdr_local_search", "mdr_get_timing",
             "mdr_set_profiling", "mdr_shuffle_stream", "mdr_probe_l2_gbs",
-            "mdr_probe_fp64_gops", "mdr_neighbor_build", "mdr_repair", "mdr_pop_download_range")
+            "mdr_probe_fp64_gops", "mdr_neighbor_build", "mdr_repair", "mdr_pop_download_range",
+            "mdr_pop_breakdown")

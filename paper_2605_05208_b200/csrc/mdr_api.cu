@@ -70,7 +70,8 @@ struct mdr_pop {
   long long *rp_stats = nullptr;
   double *rp_fold = nullptr;
   int *rp_foldi = nullptr;
-  size_t rp_cap[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+  double *bd_rt = nullptr, *bd_io = nullptr;  // mdr_pop_breakdown scratch
+  size_t rp_cap[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
 };
 
 template <typename T>
@@ -305,7 +306,8 @@ void mdr_pop_destroy(mdr_pop *p) {
   for (int q = 0; q < 3; q++) cudaStreamDestroy(p->side[q]);
   for (int q = 0; q < 4; q++) cudaEventDestroy(p->fev[q]);
   for (void *q : {(void *)p->rp_pre, (void *)p->rp_suf, (void *)p->rp_c1, (void *)p->rp_c2, (void *)p->rp_p1, (void *)p->rp_pend,
-                  (void *)p->rp_status, (void *)p->rp_stats, (void *)p->rp_fold, (void *)p->rp_foldi})
+                  (void *)p->rp_status, (void *)p->rp_stats, (void *)p->rp_fold, (void *)p->rp_foldi,
+                  (void *)p->bd_rt, (void *)p->bd_io})
     if (q) cudaFree(q);
   delete p;
 }
@@ -850,6 +852,26 @@ int mdr_repair(mdr_pop *p, int32_t op, const int32_t *pend_off, const int32_t *p
   // the population is left ready for mdr_local_search / mdr_pop_download
   if (B > 0) launch_rebuild(I, P, B, I.win, s);
   CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(s));
+  return MDR_OK;
+}
+
+int mdr_pop_breakdown(mdr_pop *p, const double *lam, double *out, void *stream) {
+  if (!p || !out) return fail(MDR_ERR_ARG, "null argument");
+  const int B = p->B;
+  if (B == 0) return MDR_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  CK(cudaSetDevice(p->inst->device));
+  int rc;
+  if ((rc = regrow(&p->bd_rt, p->rp_cap[10], (size_t)B * p->P.J * 5)) ||
+      (rc = regrow(&p->bd_io, p->rp_cap[11], (size_t)B * 10)))
+    return rc;
+  double *d_lam = p->bd_io, *d_out = p->bd_io + 4 * (size_t)B;
+  if (lam) CK(cudaMemcpyAsync(d_lam, lam, sizeof(double) * 4 * B, cudaMemcpyHostToDevice, s));
+  else CK(cudaMemcpyAsync(d_lam, p->P.lam, sizeof(double) * 4 * B, cudaMemcpyDeviceToDevice, s));
+  launch_breakdown(p->inst->I, p->P, B, d_lam, p->bd_rt, d_out, s);
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(out, d_out, sizeof(double) * 6 * B, cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
   return MDR_OK;
 }

@@ -20,6 +20,8 @@ void launch_repair(const DevInst &I, const DevPop &P, int B, int op, const int *
                    void *pre, void *suf, double *c1, double *c2, int *p1, double *fold, int *foldi, int Pcap,
                    int *status, long long *stats, cudaStream_t s);
 size_t repair_attr_bytes();
+void launch_breakdown(const DevInst &I, const DevPop &P, int B, const double *lam, double *rt, double *out,
+                      cudaStream_t s);
 bool generic_overlap(const DevInst &I, const DevPop &P);
 void launch_plan(const DevInst &I, const DevPop &P, const LsParams &L, cudaStream_t s);
 void launch_eval(const DevInst &I, const DevPop &P, const LsParams &L, int grid, bool win, cudaStream_t s,

@@ -405,4 +405,63 @@ void launch_repair(const DevInst &I, const DevPop &P, int B, int op, const int *
 
 size_t repair_attr_bytes() { return sizeof(RAt); }
 
+// evaluation.evaluate (evaluation.py:206-224) of every uploaded individual, with
+// the scalar algebra's semantics: each route folded left with Python max/min
+// (route_attr), route_contributions per route, then D/V1/V2/V3 summed in route
+// order skipping empty routes, V4 = theta * (closures + fleet excess) and
+// F = D + l0 V1 + l1 V2 + l2 V3 + l3 V4.  out[b] = {D, V1, V2, V3, V4, F}.
+__global__ void __launch_bounds__(128) k_breakdown(DevInst I, DevPop P, int B, const double *lam, double *rt,
+                                                   double *out) {
+  const int b = blockIdx.x;
+  if (b >= B) return;
+  const int m = P.m[b];
+  const int4 *RM = P.rmeta + (size_t)b * P.J;
+  double *T = rt + (size_t)b * P.J * 5;
+  for (int r = threadIdx.x; r < m; r += blockDim.x) {
+    const int4 mt = RM[r];
+    if (mt.x == 0) continue;
+    const int *sq = P.seq + ((size_t)b * P.J + r) * P.Kp;
+    const int n = mt.x + (I.open ? 1 : 2);
+    RAt a = r_single(I, sq[0]);
+    for (int i = 1; i < n; i++) a = r_cat(I, a, sq[i - 1], r_single(I, sq[i]), sq[i]);
+    double o[4];
+    r_terms(I, a, o);
+    T[r * 5 + 0] = o[0];
+    T[r * 5 + 1] = o[1];
+    T[r * 5 + 2] = o[2];
+    T[r * 5 + 3] = o[3];
+    T[r * 5 + 4] = I.open ? 0.0 : (mt.y != mt.z ? 1.0 : 0.0);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double D = 0.0, V1 = 0.0, V2 = 0.0, V3 = 0.0, clo = 0.0;
+    int cnt[RP_MAXND];
+    for (int d = 0; d < I.ND; d++) cnt[d] = 0;
+    for (int r = 0; r < m; r++) {
+      const int4 mt = RM[r];
+      if (mt.x == 0) continue;
+      D += T[r * 5 + 0];
+      V1 += T[r * 5 + 1];
+      V2 += T[r * 5 + 2];
+      V3 += T[r * 5 + 3];
+      clo += T[r * 5 + 4];
+      cnt[mt.y]++;
+    }
+    double ex = 0.0;
+    if (I.nv_on)
+      for (int d = 0; d < I.ND; d++) ex += py_max((double)cnt[d] - I.NV, 0.0);
+    const double V4 = I.theta * (clo + ex);
+    const double *l = lam + 4 * (size_t)b;
+    double *o = out + 6 * (size_t)b;
+    o[0] = D; o[1] = V1; o[2] = V2; o[3] = V3; o[4] = V4;
+    o[5] = (((D + l[0] * V1) + l[1] * V2) + l[2] * V3) + l[3] * V4;
+  }
+}
+
+void launch_breakdown(const DevInst &I, const DevPop &P, int B, const double *lam, double *rt, double *out,
+                      cudaStream_t s) {
+  if (B <= 0) return;
+  k_breakdown<<<B, 128, 0, s>>>(I, P, B, lam, rt, out);
+}
+
 }  // namespace mdr

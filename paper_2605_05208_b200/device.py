@@ -167,6 +167,16 @@ class Population:
         cl, ol, dl, al = cust.tolist(), coff.tolist(), dep.tolist(), arr.tolist()
         return [[(dl[r], al[r], cl[ol[r]:ol[r + 1]]) for r in range(rbase[b], rbase[b + 1])] for b in range(nb)]
 
+    def breakdowns(self, lams=None, stream=None) -> np.ndarray:
+        """[B, 6] {D, V1, V2, V3, V4, F} of the uploaded individuals, computed on the
+        device with evaluation.evaluate's scalar semantics (mdr_pop_breakdown)."""
+        out = np.zeros((max(self.B, 1), 6), np.float64)
+        lam = None if lams is None else np.ascontiguousarray(np.asarray(lams, np.float64).reshape(-1, 4))
+        s = stream if stream is not None else _cur_stream(self.dinst.device)
+        check(_lib.lib().mdr_pop_breakdown(self.handle, None if lam is None else ptr(lam, f64p), ptr(out, f64p), s),
+              "mdr_pop_breakdown")
+        return out[:self.B]
+
     def download_best(self, stream=None):
         routes, bestD = self._download(True, stream)
         return routes, bestD[:self.B]

@@ -25,10 +25,10 @@ import time
 from dataclasses import dataclass, field
 from typing import Optional
 
-from .evaluation import PenaltyState, ScalingConstants, evaluate, route_attr
+from .evaluation import EvalBreakdown, PenaltyState, ScalingConstants, evaluate, route_attr
 from .genetic import (DIVERSITY_LEVELS, DiscountedUCB1, InsertionOperator, dcrex, improvement_reward,
                       initialize_population, repair_insert, repair_population, route_exchange)
-from .localsearch import SearchConfig, local_search, local_search_population
+from .localsearch import SearchConfig, _searcher, local_search, local_search_population
 from .model import INF, Route, Solution
 from .neighborhood import NeighborConfig, build_device
 from .population import Population
@@ -139,11 +139,13 @@ class _Run:
             self.stats.best_cost = dist
             self.stats.best = sol.clone()
 
-    def absorb(self, offspring, main, level: int, op: int) -> None:
+    def absorb(self, offspring, main, level: int, op: int, bd=None) -> None:
         """Score one offspring against its main parent (a population Member),
-        reward the bandits, update population and best."""
+        reward the bandits, update population and best.  `bd`: its breakdown if
+        already computed (on the device, same semantics as evaluate)."""
         inst, pen = self.inst, self.penalties
-        bd = evaluate(offspring, pen, self.consts, inst)
+        if bd is None:
+            bd = evaluate(offspring, pen, self.consts, inst)
         feas = _is_feasible(bd, offspring, inst)
         if sorted(offspring.customer_list()) != self.full:
             raise AssertionError("offspring lost customer coverage")
@@ -222,9 +224,11 @@ def _batched_generation(R: "_Run", batch: int, device: int) -> None:
                             device=device, on_feasible=R.snapshot_feasible)
     R.penalties.lam[:] = pens[-1].lam
     t3 = time.perf_counter()
-    for off, (main, level, op) in zip(offspring, info):
+    # evaluation.evaluate of every offspring on the device, where the descent left them
+    bds = _searcher(inst, R.consts, R.nbr, device).pop.breakdowns([R.penalties.lam] * len(offspring))
+    for off, (main, level, op), x in zip(offspring, info, bds):
         off.meta["generation"] = R.gen
-        R.absorb(off, main, level, op)
+        R.absorb(off, main, level, op, EvalBreakdown(*(float(v) for v in x)))
     R.close_generation(prev)
     t4 = time.perf_counter()
     for k, v in (("exchange", t1 - t0), ("repair", t2 - t1), ("local_search", t3 - t2), ("update", t4 - t3)):

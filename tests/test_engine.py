@@ -85,6 +85,29 @@ def _oracle_kernels(setattr_):
     setattr_(GN, "repair_population", repair_population)
     setattr_(E, "build_device", build)
 
+    class _HostPop:  # breakdowns of the last oracle batch, by the host evaluate
+        sols = []
+
+        def breakdowns(self, lams):
+            from paper_2605_05208_b200.evaluation import PenaltyState, ScalingConstants, evaluate
+            out = []
+            for s, l in zip(self.sols, lams):
+                b = evaluate(s, PenaltyState(lam=l), self.consts, self.inst)
+                out.append([b.D, b.V1, b.V2, b.V3, b.V4, b.F])
+            return out
+
+    host_pop = _HostPop()
+
+    class _Searcher:
+        pop = host_pop
+
+    def lsp_capture(sols, penalties, cfg, nbr, consts, inst, rngs, deadline=None, device=0, on_feasible=None):
+        host_pop.sols, host_pop.consts, host_pop.inst = sols, consts, inst
+        return local_search_population(sols, penalties, cfg, nbr, consts, inst, rngs, deadline, device, on_feasible)
+
+    setattr_(E, "local_search_population", lsp_capture)
+    setattr_(E, "_searcher", lambda *a, **k: _Searcher())
+
 
 @pytest.fixture
 def oracle_kernels(monkeypatch):
@@ -104,6 +127,28 @@ def test_engine_on_device_equals_reference(tag):
     want = GOLD[tag]
     st = E.run(_instance(want["instance"]), E.SolverConfig(**want["config"]))
     _check(st, want)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("variant,fleet,dur", [("mdvrp", 2, None), ("mdvrptw", 3, 600.0), ("mdovrp", None, None),
+                                               ("mdvrp", None, 200.0)])
+def test_device_breakdown_equals_evaluate(variant, fleet, dur):
+    """mdr_pop_breakdown == evaluation.evaluate bit for bit (infeasible random states,
+    empty routes, fleet excess, closures)."""
+    from paper_2605_05208_b200.device import DeviceInstance, Population
+    from paper_2605_05208_b200.evaluation import PenaltyState, ScalingConstants, evaluate
+    inst = W.make_instance(random.Random(31), variant, n_customers=45, n_depots=3, fleet=fleet, max_duration=dur)
+    consts = ScalingConstants.from_instance(inst)
+    sols = [W.random_solution(random.Random(700 + i), inst) for i in range(9)]
+    sols[3].routes[0].customers = []  # an empty route is skipped
+    lams = [[random.Random(i).choice([0.1, 1.0, 30.0]) for _ in range(4)] for i in range(9)]
+    J, K = Population.caps_for(sols, inst)
+    pop = Population(DeviceInstance(inst, consts, None), 9, J, K)
+    pop.upload(sols, lams)
+    got = pop.breakdowns(lams)
+    for s, l, g in zip(sols, lams, got):
+        b = evaluate(s, PenaltyState(lam=l), consts, inst)
+        assert [float(x).hex() for x in g] == [float(x).hex() for x in (b.D, b.V1, b.V2, b.V3, b.V4, b.F)]
 
 
 @pytest.mark.gpu
