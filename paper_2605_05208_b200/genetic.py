@@ -328,7 +328,14 @@ def route_exchange(population: Sequence, inst, diversity_bandit: DiscountedUCB1,
             if ps is None:
                 break
             score, oi_a, dj_a, dsig = ps
-            top = np.lexsort((dj_a, oi_a, score))[:5]   # pairs.sort(key=(score, oi, dj))[:5]
+            # pairs.sort(key=(score, oi, dj))[:5] via one exact int64 key and a partial sort
+            nd = len(donor.routes)
+            key = (score - score.min()) * ((len(off.routes) + 1) * nd) + oi_a * nd + dj_a
+            if key.size > 5:
+                part = np.argpartition(key, 4)[:5]
+                top = part[np.argsort(key[part])]
+            else:
+                top = np.argsort(key)
             k = top[rng.choice(range(len(top)))]         # rng.choice over the first five
             oi, dj, ds = int(oi_a[k]), int(dj_a[k]), int(dsig[k])
             if sigma + ds >= sigma_max:
