@@ -1,5 +1,6 @@
 """GPU parity: the sm_100a path (through the C-ABI) against the reference's
 golden outputs and the C oracle.  Bit-exact (`==`, -0.0 == +0.0) everywhere."""
+import os
 import random
 import zlib
 
@@ -132,7 +133,7 @@ def test_population_descents_bit_exact_vs_oracle(variant, fleet, dur, mm):
         assert stats[i]["cands"] == st["cands"], "candidate counts per operator must equal the reference's"
 
 
-FUZZ = list(range(64))
+FUZZ = list(range(int(os.environ.get("MDR_FUZZ_N", "64"))))  # more: MDR_FUZZ_N=500
 
 
 @pytest.mark.parametrize("seed", FUZZ)

@@ -1,6 +1,7 @@
 """Repair insertion: the oracle restatement and the device
 path (mdr_repair) against the reference's own repair_insert outputs
 (tests/golden/repair.npz from make_repair_golden.py)."""
+import os
 import random
 import zlib
 
@@ -128,3 +129,36 @@ def test_device_repair_errors_and_noop():
     s = c.sol.clone()
     assert R.routes_of(repair_insert(s, [], InsertionOperator.FRI, c.inst, c.consts, c.penalties(), None)) == \
         R.routes_of(c.sol)
+
+
+RFUZZ = list(range(int(os.environ.get("MDR_FUZZ_N", "32"))))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("seed", RFUZZ)
+def test_fuzz_device_repair_vs_oracle(seed):
+    """Random shapes and partial solutions: every operator, a batch of 1-8
+    individuals with different pending sets and lambdas, vs the oracle."""
+    r = random.Random(5000 + seed)
+    variant = r.choice(["mdvrp", "mdvrptw", "mdovrp"])
+    inst = W.make_instance(r, variant, n_customers=r.randint(2, 90), n_depots=r.randint(1, 5),
+                           capacity=r.choice([None, 10, 30, 500]), fleet=r.choice([None, 1, 2, 5]),
+                           max_duration=r.choice([None, 300.0]) if variant != "mdovrp" else None)
+    consts = ScalingConstants.from_instance(inst)
+    oi = _oi(inst, consts)
+    op = r.choice(["FBI", "IBI", "FRI", "IRI"])
+    sols, pend, pens = [], [], []
+    for i in range(r.randint(1, 8)):
+        s, u = _partial(r, W.random_solution(random.Random(seed * 10 + i), inst), r.choice([0.05, 0.3, 0.7, 1.0]),
+                        r.random() < 0.5)
+        if r.random() < 0.15:
+            s.routes = []  # everything unrouted
+            u = list(inst.customers())
+        sols.append(s)
+        pend.append(u)
+        pens.append(PenaltyState(lam=[r.choice([0.01, 1.0, 50.0]) for _ in range(4)]))
+    want = [O.repair(oi, s, u, O.REPAIR_OPS[op], p.lam)[0] for s, u, p in zip(sols, pend, pens)]
+    work = [s.clone() for s in sols]
+    repair_population(work, pend, InsertionOperator[op], inst, consts, pens)
+    for b in range(len(sols)):
+        assert R.routes_of(work[b]) == want[b], (seed, b)
