@@ -407,11 +407,6 @@ def main():
                 "identical": bool(np.array_equal(nb_dev.lists, nb_host.lists)),
                 "nodes": inst.n_nodes, "theta": spec.theta}
 
-    repair_line = None
-    if not args.no_repair and world == 1:
-        repair_line = bench_repair(name, inst, consts, sols, ids, local, max(1, args.steps),
-                                   cpu=not args.no_cpu_baseline)
-
     # e2e: through the public API with host Solution objects, H2D + D2H inside
     e2e = None
     if not args.no_e2e:
@@ -433,6 +428,11 @@ def main():
             d2h = srch.pop.d2h_bytes
         e2e = {"value": e_cands / (work_ms / 1000.0), "unit": "move-evals/s", "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h), "ms_per_step": work_ms / max(1, args.steps)}
+
+    repair_line = None
+    if not args.no_repair and world == 1:
+        repair_line = bench_repair(name, inst, consts, sols, ids, local, max(1, args.steps),
+                                   cpu=not args.no_cpu_baseline)
 
     # max over ranks (time), sum over ranks (work)
     t = torch.tensor([tot_ms, float(cands), float(descents)], dtype=torch.float64, device=dev)
