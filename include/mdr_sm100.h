@@ -18,6 +18,11 @@
  *   mdr_totals            SolutionCache.totals (batch.py:161-165)
  *   mdr_local_search      local_search (localsearch.py:97-140), population-batched:
  *                         B independent descents advance together on the device
+ *   mdr_repair            repair_insert FBI/IBI/FRI/IRI (genetic.py:174-244), batched
+ *   mdr_pop_breakdown     evaluate (evaluation.py:206-224) of every individual
+ *   mdr_neighbor_build    neighborhood.build (neighborhood.py:60-101)
+ *   mdr_shuffle_stream    the rng.shuffle calls of local_search (localsearch.py:112-113)
+ *   mdr_probe_*           diagnostics: measured L2 / FP64 roofline denominators
  *
  * Conventions: plain pointers and sizes, host buffers unless stated, return
  * int status (MDR_OK ...), no C++ exceptions cross the ABI, a handle is used
@@ -101,7 +106,9 @@ typedef struct mdr_timing {
   double eval_ms, select_ms, plan_ms, total_ms; /* summed CUDA-event times */
   int64_t eval_launches, rounds;
   int64_t cands_total;
-  double geval_ms; /* generic-path evaluator (intra-route, 2-opt, depot operators) */
+  double geval_ms; /* generic-path evaluator after the evaluators (intra-route, 2-opt, depot
+                      operators; 0 when the population is small enough that these are
+                      drained on the evaluators' graph branches, inside eval_ms) */
 } mdr_timing;
 
 const char *mdr_last_error(void);
