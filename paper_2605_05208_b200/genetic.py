@@ -41,7 +41,11 @@ class InsertionOperator(IntEnum):
 
 
 def _route_cls(sol):
-    return type(sol.routes[0]) if sol.routes else Route
+    """The caller's Route class (the reference's when `sol` is a reference Solution)."""
+    if sol.routes:
+        return type(sol.routes[0])
+    import sys
+    return getattr(sys.modules.get(type(sol).__module__), "Route", Route)
 
 
 def _open_route_host(sol, node, inst):

@@ -168,9 +168,8 @@ class DeviceSearch:
 
 
 def _apply_result(sol, routes):
-    route_cls = type(sol.routes[0]) if sol.routes else None
-    if route_cls is None:
-        from .model import Route as route_cls
+    from .genetic import _route_cls
+    route_cls = _route_cls(sol)
     sol.routes = [route_cls(d, a, c) for d, a, c in routes]
 
 
