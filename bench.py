@@ -293,10 +293,16 @@ def main():
 
     import torch
     import torch.distributed as dist
+    backend = os.environ.get("MDR_BENCH_BACKEND", "nccl")  # "gloo": functional dry run of the N>1 flow
+    if backend != "nccl":
+        local = local % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
 
     import paper_2605_05208_b200 as P
     from paper_2605_05208_b200.device import DeviceInstance, Population
@@ -339,7 +345,8 @@ def main():
         Ds = [s["best_feasible_D"] for s in st]
         best = int(np.argmin(Ds))
         routes = pop.download_range(best, 1, sh)[0]  # the elite only
-        enc = DS.encode_elite(routes, Ds[best], inst.n_customers, J)
+        # fixed length on every rank: routes with customers never exceed the customer count
+        enc = DS.encode_elite(routes, Ds[best], inst.n_customers, inst.n_customers)
         return DS.best_of(DS.exchange_elites(enc, device=dev))
 
     for _ in range(args.warmup):
