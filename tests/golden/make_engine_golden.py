@@ -32,6 +32,12 @@ CASES = [
     ("tw_mm", ("mdvrptw", 20, 2, dict(fleet=3, max_duration=700.0), 13), dict(generations=25, mu=4, theta=8, depth=40, multi_move=True, seed=3)),
     ("open_mm", ("mdovrp", 24, 3, {}, 14), dict(generations=25, mu=4, theta=10, depth=40, multi_move=True, seed=4)),
     ("stagnate", ("mdvrp", 12, 2, {}, 15), dict(generations=60, patience=6, mu=3, theta=5, depth=30, multi_move=True, seed=5)),
+    ("tw_sm", ("mdvrptw", 26, 3, dict(fleet=2), 16), dict(generations=20, mu=6, theta=12, depth=30, multi_move=False, seed=6)),
+    ("open_sm", ("mdovrp", 30, 2, dict(fleet=3), 17), dict(generations=20, mu=5, theta=8, depth=35, multi_move=False, seed=7)),
+    ("vrp_dur", ("mdvrp", 28, 4, dict(max_duration=250.0, fleet=2), 18), dict(generations=22, mu=4, theta=9, depth=45, multi_move=True, xi=0.4, seed=8)),
+    ("tw_big", ("mdvrptw", 45, 4, dict(max_duration=900.0), 19), dict(generations=12, mu=8, theta=15, depth=60, multi_move=True, kappa=0.3, seed=9)),
+    ("vrp_one", ("mdvrp", 16, 1, {}, 20), dict(generations=15, mu=3, theta=4, depth=20, multi_move=True, seed=10)),
+    ("tight_cap", ("mdvrp", 24, 2, dict(capacity=25), 21), dict(generations=18, mu=4, theta=6, depth=40, multi_move=True, seed=11)),
 ]
 
 
