@@ -210,6 +210,21 @@ def bench_repair(name, inst, consts, sols, ids, device, steps, cpu=True, op=3):
     return line
 
 
+def eval_only_line(name, inst, consts, nbr, sols, cands, eval_s, cpu=True):
+    line = {"value": cands / eval_s, "unit": "move-evals/s", "how": "profiled step: candidates / (eval + generic) time"}
+    if cpu:
+        from oracle import oracle as O
+        threads = os.cpu_count() or 1
+        k = len(sols)
+        oi = O.OracleInstance(inst, consts, nbr)
+        t0 = time.perf_counter()
+        n, _ = O.eval_all_many(oi, sols[:k], [[1.0] * 4] * k, threads)
+        dt = time.perf_counter() - t0
+        line["cpu_baseline"] = {"value": n / dt, "unit": "move-evals/s", "cores": threads, "kind": "port",
+                                "sample": f"all operators of {k} start states on {threads} threads, {dt:.1f} s"}
+    return line
+
+
 def cpu_baseline(name, inst, consts, nbr, sols, depth, seconds=20.0):
     """Oracle (C port of the reference) descents on all host threads, bounded sample."""
     from oracle import oracle as O
@@ -497,6 +512,12 @@ def main():
             "profile": {"rounds_per_step": rounds / args.steps, "plan_ms": tm["plan_ms"], "eval_ms": tm["eval_ms"],
                         "geval_ms": tm["geval_ms"],
                         "select_ms": tm["select_ms"], "total_ms": tm["total_ms"]},
+            # SURVEY.md 8(d) flavour 1: candidates scored per second of evaluation
+            # phase only (enumerate + evaluate + leader/follower reduction), beside
+            # the oracle's evaluate-all-operators on the start states on all host threads
+            "eval_only": eval_only_line(name, inst, consts, nbr, sols, float(np.sum(op_c)),
+                                        (tm["eval_ms"] + tm["geval_ms"]) * 1e-3,
+                                        cpu=world == 1 and not args.no_cpu_baseline),
         }
         print(json.dumps(line), flush=True)
     if world > 1:
