@@ -20,6 +20,8 @@ from .localsearch import (DeviceSearch, SearchConfig, apply_moves, enabled_opera
 from .genetic import InsertionOperator, repair_insert, repair_population
 from .formats import ParseError, parse_instance, read_solution, write_solution
 from .engine import RunStats, SolverConfig, run, run_batched, run_islands
+from .evaluation import EvalBreakdown, evaluate, move_delta
+from .feasibility import FeasibilityReport, check_feasible, minimal_duration, simulate_route
 
 __all__ = [
     "INF", "Instance", "Node", "Route", "Solution", "Variant", "LAMBDA_MAX", "LAMBDA_MIN", "PenaltyState",
@@ -31,4 +33,6 @@ __all__ = [
     "InsertionOperator", "repair_insert", "repair_population",
     "ParseError", "parse_instance", "read_solution", "write_solution",
     "RunStats", "SolverConfig", "run", "run_batched", "run_islands",
+    "EvalBreakdown", "evaluate", "move_delta", "FeasibilityReport", "check_feasible", "minimal_duration",
+    "simulate_route",
 ]

@@ -168,3 +168,44 @@ def evaluate(sol, penalties, consts, inst) -> EvalBreakdown:
     lam = penalties.lam
     out.F = out.D + lam[0] * out.V1 + lam[1] * out.V2 + lam[2] * out.V3 + lam[3] * out.V4
     return out
+
+
+def move_delta(sol, move, penalties, consts, inst) -> EvalBreakdown:
+    """Recompute-from-scratch delta of one move over the affected routes only
+    (evaluation.py:227-275): the scalar cross-check of the batched evaluator
+    (agrees with it to ~1e-6, not bit for bit -- SURVEY.md 8(c))."""
+    from .moves import move_plan
+    from .model import Route
+    delta = EvalBreakdown()
+    closure_delta = 0
+    changes: dict = {}
+    for plan in move_plan(sol, move, inst):
+        if plan.route_index is not None:
+            old = sol.routes[plan.route_index]
+            attr = old.attr if getattr(old, "attr", None) is not None else route_attr(old, inst)
+            d, v1, v2, v3, clo = route_contributions(attr, old.depart, old.arrive, consts, inst)
+            delta.D -= d
+            delta.V1 -= v1
+            delta.V2 -= v2
+            delta.V3 -= v3
+            closure_delta -= clo
+            changes[old.depart] = changes.get(old.depart, 0) - 1
+        if plan.customers:
+            d, v1, v2, v3, clo = route_contributions(route_attr(Route(plan.depart, plan.arrive, plan.customers), inst),
+                                                     plan.depart, plan.arrive, consts, inst)
+            delta.D += d
+            delta.V1 += v1
+            delta.V2 += v2
+            delta.V3 += v3
+            closure_delta += clo
+            changes[plan.depart] = changes.get(plan.depart, 0) + 1
+    fleet_delta = 0
+    if inst.fleet_per_depot != INF and changes:
+        counts = depot_counts(sol, inst)
+        nv = inst.fleet_per_depot
+        for dep, chg in changes.items():
+            fleet_delta += max(counts[dep] + chg - nv, 0) - max(counts[dep] - nv, 0)
+    delta.V4 = consts.theta * (closure_delta + fleet_delta)
+    lam = penalties.lam
+    delta.F = delta.D + lam[0] * delta.V1 + lam[1] * delta.V2 + lam[2] * delta.V3 + lam[3] * delta.V4
+    return delta
