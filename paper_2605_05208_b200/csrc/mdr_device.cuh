@@ -19,6 +19,18 @@
 #include <cuda_runtime.h>
 
 #define MDR_CHUNK 256
+
+// k_eval_c shapes (DevPop::ct selects one per population): small populations /
+// instances -- 8 warps, 8 items per CTA task, 2 CTAs per SM (more, smaller tasks
+// for an under-filled GPU); large -- 16 warps, 32 items per task (2 per warp),
+// 1 CTA per SM (the route staging amortised over twice the items).  Measured:
+// C2 7.9 vs 7.3 G/s, C3 8.4 vs 6.6 (small wins); C4 22.8 vs 22.3, C5 25.2 vs 23.8
+// (large wins).
+#define MDR_SMALL_CU 8
+#define MDR_SMALL_CT 8
+#define MDR_LARGE_CU 16
+#define MDR_LARGE_CT 32
+
 #define MDR_EPS 1e-9
 
 namespace mdr {
@@ -49,6 +61,7 @@ struct LsState {
 struct DevPop {
   int Bcap, J, K, Kp, Fcap, FE;
   int staged;  // relocate/swap/2-opt* use the CTA-staged evaluators (mdr_staged.cuh)
+  int ct;      // items per CTA task of the staged evaluators (MDR_SMALL_CT / MDR_LARGE_CT)
   int N, ND;
   int *m;
   int4 *rmeta;

@@ -249,7 +249,7 @@ __global__ void __launch_bounds__(1024) k_plan(DevInst I, DevPop P, LsParams L) 
     }
     if (!st.done) {
       const int op = P.perms[((size_t)b * P.maxp + st.pass) * P.nops + st.pos];
-      const int t = (P.staged && op <= 2) ? op_tasks_c(op, P.m[b], I.NC) : op_tasks(op, P.m[b], I.NC, I.win);
+      const int t = (P.staged && op <= 2) ? op_tasks_c(op, P.m[b], I.NC, P.ct) : op_tasks(op, P.m[b], I.NC, I.win);
       P.op_cur[b] = op;
       P.wsize[b] = t;
       if (t > 0) {
@@ -352,14 +352,14 @@ __global__ void __launch_bounds__(256, MDR_EVAL_MINB) k_eval(DevInst I, DevPop P
 #define MDR_TGC 1
 #endif
 // CTA-task evaluators (relocate, swap, 2-opt*) with staged route boundaries
-template <bool WIN, int OP>
-__global__ void __launch_bounds__(32 * MDR_CU, MDR_CMINB) k_eval_c(DevInst I, DevPop P, LsParams L) {
+template <bool WIN, int OP, int CU, int CT>
+__global__ void __launch_bounds__(32 * CU, 16 / CU) k_eval_c(DevInst I, DevPop P, LsParams L) {
   extern __shared__ __align__(16) unsigned char smx_c[];
   RB *R = reinterpret_cast<RB *>(smx_c);
   // per-warp depot-indexed precomputes (front-insertion prefixes, 2-opt* A sides)
   const int WS = I.ND <= MDR_WDMAX ? 18 * I.ND : 0;
   double *Wd = WS ? reinterpret_cast<double *>(smx_c + sizeof(RB) * P.J) + (threadIdx.x >> 5) * WS : nullptr;
-  __shared__ double s_u[MDR_CU][MDR_USLOT];
+  __shared__ double s_u[CU][MDR_USLOT];
   __shared__ int s_t, s_b, s_lo, s_hi, s_next, s_end;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   double *U = s_u[wid];
@@ -368,7 +368,7 @@ __global__ void __launch_bounds__(32 * MDR_CU, MDR_CMINB) k_eval_c(DevInst I, De
   const int *OFF = P.opoff + OP * (P.Bcap + 1);
   const int *OB = P.opb + OP * P.Bcap;
   const bool mm = L.multi_move != 0;
-  const int nch = (I.NC + MDR_CT - 1) / MDR_CT;
+  const int nch = (I.NC + CT - 1) / CT;
   __shared__ int s_item;
   int staged = -1;
   if (threadIdx.x == 0) { s_next = 0; s_end = 0; s_lo = 0; s_hi = 0; }
@@ -413,12 +413,12 @@ __global__ void __launch_bounds__(32 * MDR_CU, MDR_CMINB) k_eval_c(DevInst I, De
       int it = 0;
       if (lane == 0) it = atomicAdd(&s_item, 1);
       it = __shfl_sync(0xffffffffu, it, 0);
-      if (it >= MDR_CT) break;
+      if (it >= CT) break;
       if (OP == 2 && local >= nch) {
-        const int ra = (local - nch) * MDR_CT + it;
+        const int ra = (local - nch) * CT + it;
         if (ra < v.M) stos_r<WIN>(I, P, v, R, b, ra, lam, mm, acc);
       } else {
-        const int u = I.ND + local * MDR_CT + it;
+        const int u = I.ND + local * CT + it;
         if (u < I.N) {
           if (OP == 0) srelocate<WIN>(I, P, v, R, b, u, lam, mm, acc, U, Wd);
           else if (OP == 1) sswap<WIN>(I, P, v, R, b, u, lam, mm, acc, U);
@@ -1013,27 +1013,50 @@ static int grid_for(K kern) {
 
 int eval_grid_size(bool win) { return win ? grid_for(k_eval<true, 0>) : grid_for(k_eval<false, 0>); }
 
-// Drain generic-queue region A (2-opt, depot operators) concurrently with the
-// staged evaluators only when those leave the GPU under-filled (few CTA tasks
-// per round: small populations / instances); otherwise it would just compete
-// with them, and both regions are drained in one pass after the join.
-bool generic_overlap(const DevInst &I, const DevPop &P) {
-  static int slots = 0;
-  if (!slots) {
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    slots = sms * MDR_CMINB;
-  }
-  const long long tasks = (long long)P.Bcap * ((I.NC + MDR_CT - 1) / MDR_CT) / 5;  // per operator kernel
-  return P.staged && tasks < 8LL * slots;
-}
-
 template <bool WIN>
 static void launch_eval_g_region(const DevInst &I, const DevPop &P, const LsParams &L, cudaStream_t s, int region) {
   static int g = 0;  // full occupancy of the (latency-bound) generic evaluator
   if (!g) g = grid_for(k_eval_g<WIN>);
   k_eval_g<WIN><<<g, 256, 0, s>>>(I, P, L, region);
+}
+
+// the three staged evaluators of one (CU, CT) shape on the side streams
+template <bool WIN, int CU, int CT>
+static void launch_staged(const DevInst &I, const DevPop &P, const LsParams &L, const cudaStream_t *side) {
+  static int gc[3] = {0, 0, 0};
+  static size_t sm_set = 0;
+  const size_t sm = sizeof(RB) * (size_t)P.J + (I.ND <= MDR_WDMAX ? sizeof(double) * 18 * (size_t)I.ND * CU : 0);
+  if (sm_set < sm) {
+    cudaFuncSetAttribute(k_eval_c<WIN, 0, CU, CT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    cudaFuncSetAttribute(k_eval_c<WIN, 1, CU, CT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    cudaFuncSetAttribute(k_eval_c<WIN, 2, CU, CT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    // shared-memory carveout just large enough for the resident CTAs (16 / CU):
+    // the rest of the 228 KB stays L1 for the gathers (+2 % on C4 vs the default)
+    int pct = (int)(((16 / CU) * (sm + 3 * 1024) * 100 + 228 * 1024 - 1) / (228 * 1024));
+    if (getenv("MDR_CARVEOUT")) pct = atoi(getenv("MDR_CARVEOUT"));
+    if (pct > 100) pct = 100;
+    cudaFuncSetAttribute(k_eval_c<WIN, 0, CU, CT>, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+    cudaFuncSetAttribute(k_eval_c<WIN, 1, CU, CT>, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+    cudaFuncSetAttribute(k_eval_c<WIN, 2, CU, CT>, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+    cudaFuncSetAttribute(k_eval_g<WIN>, cudaFuncAttributePreferredSharedMemoryCarveout, 0);
+    sm_set = sm;
+    gc[0] = 0;
+  }
+  if (!gc[0]) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    int per = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_eval_c<WIN, 0, CU, CT>, 32 * CU, sm);
+    gc[0] = sms * (per < 1 ? 1 : per);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_eval_c<WIN, 1, CU, CT>, 32 * CU, sm);
+    gc[1] = sms * (per < 1 ? 1 : per);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_eval_c<WIN, 2, CU, CT>, 32 * CU, sm);
+    gc[2] = sms * (per < 1 ? 1 : per);
+  }
+  k_eval_c<WIN, 0, CU, CT><<<gc[0], 32 * CU, sm, side[0]>>>(I, P, L);
+  k_eval_c<WIN, 1, CU, CT><<<gc[1], 32 * CU, sm, side[1]>>>(I, P, L);
+  k_eval_c<WIN, 2, CU, CT><<<gc[2], 32 * CU, sm, side[2]>>>(I, P, L);
 }
 
 template <bool WIN>
@@ -1045,53 +1068,18 @@ static void launch_eval_t(const DevInst &I, const DevPop &P, const LsParams &L, 
     g[3] = grid_for(k_eval<WIN, 3>); g[4] = grid_for(k_eval<WIN, 4>); g[5] = grid_for(k_eval<WIN, 5>);
   }
   if (P.staged) {
-    static int gc[3] = {0, 0, 0};
-    const size_t sm = sizeof(RB) * (size_t)P.J +
-                      (I.ND <= MDR_WDMAX ? sizeof(double) * 18 * (size_t)I.ND * MDR_CU : 0);
-    static size_t sm_set = 0;
-    if (sm_set < sm) {
-      cudaFuncSetAttribute(k_eval_c<WIN, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-      cudaFuncSetAttribute(k_eval_c<WIN, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-      cudaFuncSetAttribute(k_eval_c<WIN, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-      {
-        // shared-memory carveout just large enough for MDR_CMINB resident CTAs: the
-        // rest of the 228 KB stays L1 for the gathers (+2 % on C4 vs the default)
-        int pct = (int)((MDR_CMINB * (sm + 3 * 1024) * 100 + 228 * 1024 - 1) / (228 * 1024));
-        if (getenv("MDR_CARVEOUT")) pct = atoi(getenv("MDR_CARVEOUT"));
-        if (pct > 100) pct = 100;
-        cudaFuncSetAttribute(k_eval_c<WIN, 0>, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
-        cudaFuncSetAttribute(k_eval_c<WIN, 1>, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
-        cudaFuncSetAttribute(k_eval_c<WIN, 2>, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
-        cudaFuncSetAttribute(k_eval_g<WIN>, cudaFuncAttributePreferredSharedMemoryCarveout, 0);
-      }
-      sm_set = sm;
-      gc[0] = 0;
-    }
-    if (!gc[0]) {
-      int dev = 0, sms = 148;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-      int per = 1;
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_eval_c<WIN, 0>, 32 * MDR_CU, sm);
-      gc[0] = sms * (per < 1 ? 1 : per);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_eval_c<WIN, 1>, 32 * MDR_CU, sm);
-      gc[1] = sms * (per < 1 ? 1 : per);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_eval_c<WIN, 2>, 32 * MDR_CU, sm);
-      gc[2] = sms * (per < 1 ? 1 : per);
-    }
     // relocate / swap / 2-opt* as parallel branches (fork/join): their
     // persistent grids back-fill each other's tails
     cudaEventRecord(ev[0], s);
     for (int q = 0; q < 3; q++) cudaStreamWaitEvent(side[q], ev[0], 0);
-    k_eval_c<WIN, 0><<<gc[0], 32 * MDR_CU, sm, side[0]>>>(I, P, L);
-    k_eval_c<WIN, 1><<<gc[1], 32 * MDR_CU, sm, side[1]>>>(I, P, L);
-    k_eval_c<WIN, 2><<<gc[2], 32 * MDR_CU, sm, side[2]>>>(I, P, L);
+    if (P.ct == MDR_LARGE_CT) launch_staged<WIN, MDR_LARGE_CU, MDR_LARGE_CT>(I, P, L, side);
+    else launch_staged<WIN, MDR_SMALL_CU, MDR_SMALL_CT>(I, P, L, side);
     const bool ov0 = P.gbase[1] > 0;
     if (ov0) {  // each producer's intra-route queue drained right behind it, on its branch
       launch_eval_g_region<WIN>(I, P, L, side[0], 1);
       launch_eval_g_region<WIN>(I, P, L, side[1], 2);
     }
-    const bool ov = P.gbase[1] > 0;  // decided at mdr_pop_create (generic_overlap)
+    const bool ov = P.gbase[1] > 0;  // per-producer regions (mdr_pop_create; MDR_NO_OVERLAP: single queue)
     if (ov) {  // meanwhile on s: 2-opt / depot enumeration and their generic-path evaluation (region A)
       if (!WIN) k_eval<WIN, 3><<<g[3], 256, 0, s>>>(I, P, L);
       k_eval<WIN, 4><<<g[4], 256, 0, s>>>(I, P, L);

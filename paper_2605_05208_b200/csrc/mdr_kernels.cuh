@@ -22,7 +22,7 @@ void launch_repair(const DevInst &I, const DevPop &P, int B, int op, const int *
 size_t repair_attr_bytes();
 void launch_breakdown(const DevInst &I, const DevPop &P, int B, const double *lam, double *rt, double *out,
                       cudaStream_t s);
-bool generic_overlap(const DevInst &I, const DevPop &P);
+
 void launch_plan(const DevInst &I, const DevPop &P, const LsParams &L, cudaStream_t s);
 void launch_eval(const DevInst &I, const DevPop &P, const LsParams &L, int grid, bool win, cudaStream_t s,
                  const cudaStream_t *side, cudaEvent_t *ev);

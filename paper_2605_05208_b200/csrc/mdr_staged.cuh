@@ -553,19 +553,9 @@ __device__ void stos_r(const DevInst &I, const DevPop &P, const IV &v, const RB 
   }
 }
 
-#ifndef MDR_CU
-#define MDR_CU 8  // warps per CTA of k_eval_c
-#endif
-#ifndef MDR_CT
-#define MDR_CT 8  // customers (or 2-opt* routes) per CTA task, taken by the warps dynamically
-#endif
-#ifndef MDR_CMINB
-#define MDR_CMINB 2
-#endif
-
-__host__ __device__ __forceinline__ int op_tasks_c(int op, int M, int NC) {
-  int nch = (NC + MDR_CT - 1) / MDR_CT;
-  if (op == 2) return M < 2 ? 0 : nch + (M + MDR_CT - 1) / MDR_CT;
+__host__ __device__ __forceinline__ int op_tasks_c(int op, int M, int NC, int ct) {
+  int nch = (NC + ct - 1) / ct;
+  if (op == 2) return M < 2 ? 0 : nch + (M + ct - 1) / ct;
   return nch;
 }
 

@@ -1,0 +1,16 @@
+run() { MDR_LIB=$PWD/paper_2605_05208_b200/$1 timeout 600 env $2 python bench.py --config $3 --pop $4 --steps 1 --warmup 1 --no-cpu-baseline --no-e2e --no-repair 2>&1 | python -c "
+import sys,json
+for l in sys.stdin:
+    if l.startswith('{'):
+        d=json.loads(l); p=d['profile']
+        print('$1 $2 $3 value %.4g  ms/step %.0f  eval %.0f geval %.0f select %.0f'%(d['value'],d['ms_per_step'],p['eval_ms'],p.get('geval_ms',0),p['select_ms']))
+"; }
+for L in libmdr_sm100.so libmdr_sm100_g3.so libmdr_sm100_g2.so libmdr_sm100_g4.so; do
+  run $L MDR_FORCE_OVERLAP=1 C4 256
+done
+for L in libmdr_sm100.so libmdr_sm100_g3.so; do
+  run $L MDR_X=1 C5 64
+  run $L MDR_FORCE_OVERLAP=1 C5 64
+  run $L MDR_X=1 C2 64
+  run $L MDR_X=1 C3 128
+done
