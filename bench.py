@@ -388,8 +388,10 @@ def main():
         dist.barrier()
     clocks = clk.stop()
     rounds = pop.timing()["rounds"] - rounds0
-    n_eval = 5 if inst.has_windows else 6  # per-operator fused kernels (2-opt only without windows)
-    launches = rounds * (3 + n_eval) + 2 * args.steps  # plan, evals, generic, select per round + unpack/rebuild
+    # per round: plan, 3 staged evaluators, the depot (+ 2-opt without windows) enumerators,
+    # 3 generic-path drains (one per queue region), select; per step: unpack + rebuild
+    n_enum = 2 if inst.has_windows else 3
+    launches = rounds * (1 + 3 + n_enum + 3 + 1) + 2 * args.steps
 
     # profiled pass (untimed): eval-kernel share, avg launch duration, per-op candidates
     tm0 = pop.timing()
