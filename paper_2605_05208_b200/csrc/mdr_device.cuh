@@ -26,10 +26,18 @@
 // 1 CTA per SM (the route staging amortised over twice the items).  Measured:
 // C2 7.9 vs 7.3 G/s, C3 8.4 vs 6.6 (small wins); C4 22.8 vs 22.3, C5 25.2 vs 23.8
 // (large wins).
+#ifndef MDR_SMALL_CU
 #define MDR_SMALL_CU 8
+#endif
+#ifndef MDR_SMALL_CT
 #define MDR_SMALL_CT 8
+#endif
+#ifndef MDR_LARGE_CU
 #define MDR_LARGE_CU 16
+#endif
+#ifndef MDR_LARGE_CT
 #define MDR_LARGE_CT 32
+#endif
 
 #define MDR_EPS 1e-9
 
