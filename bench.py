@@ -513,7 +513,11 @@ def main():
             "clocks": clocks,
             "profile": {"rounds_per_step": rounds / args.steps, "plan_ms": tm["plan_ms"], "eval_ms": tm["eval_ms"],
                         "geval_ms": tm["geval_ms"],
-                        "select_ms": tm["select_ms"], "total_ms": tm["total_ms"]},
+                        "select_ms": tm["select_ms"], "total_ms": tm["total_ms"],
+                        # per-operator candidate counts of the profiled step (the
+                        # GPU tests assert them equal to the reference's / the oracle's)
+                        "cands_per_op": {n: int(op_c[o]) for o, n in enumerate(
+                            ("relocate", "swap", "two_opt_star", "two_opt", "depot_insert", "depot_replace"))}},
             # SURVEY.md 8(d) flavour 1: candidates scored per second of evaluation
             # phase only (enumerate + evaluate + leader/follower reduction), beside
             # the oracle's evaluate-all-operators on the start states on all host threads
