@@ -365,3 +365,25 @@ def test_download_range_matches_full_download():
         assert pop.download_range(b0, nb) == full[b0:b0 + nb]
     with pytest.raises(ValueError):
         pop.download_range(5, 3)
+
+
+@pytest.mark.gpu
+def test_abi_argument_errors_raise():
+    """Bad arguments fail loudly at the C-ABI (ValueError like the reference), never silently."""
+    from paper_2605_05208_b200.model import Route, Solution
+    inst, consts, nbr, sols = _synthetic_states("mdvrp", 20, 2, 5, 2)
+    dinst = DeviceInstance(inst, consts, nbr)
+    pop = Population(dinst, 2, 40, 32)
+    with pytest.raises(ValueError):  # route endpoint is not a depot
+        pop.upload([Solution([Route(5, 0, [6, 7])])], [[1.0] * 4])
+    with pytest.raises(ValueError):  # a depot listed as a customer
+        pop.upload([Solution([Route(0, 0, [1, 6])])], [[1.0] * 4])
+    pop.upload(sols[:1], [[1.0] * 4])
+    with pytest.raises(ValueError):  # unknown insertion operator
+        pop.repair(7, [[]])
+    with pytest.raises(ValueError):
+        pop.download_range(0, 2)
+    from paper_2605_05208_b200 import _lib
+    with pytest.raises(ValueError):  # theta must be >= 1, buffers non-null
+        _lib.check(_lib.lib().mdr_neighbor_build(0, inst.n_nodes, inst.n_depots, None, None, None, None, None,
+                                                 1.0, 1.0, 10.0, 0, None, None, None), "mdr_neighbor_build")
