@@ -351,6 +351,9 @@ __global__ void __launch_bounds__(256, MDR_EVAL_MINB) k_eval(DevInst I, DevPop P
 #ifndef MDR_TGC
 #define MDR_TGC 1
 #endif
+#ifndef MDR_SWAP_WARP
+#define MDR_SWAP_WARP 0  // 1: per-customer warp sweep (sswap) instead of the flattened chunks
+#endif
 // CTA-task evaluators (relocate, swap, 2-opt*) with staged route boundaries
 template <bool WIN, int OP, int CU, int CT>
 __global__ void __launch_bounds__(32 * CU, 16 / CU) k_eval_c(DevInst I, DevPop P, LsParams L) {
@@ -360,6 +363,9 @@ __global__ void __launch_bounds__(32 * CU, 16 / CU) k_eval_c(DevInst I, DevPop P
   const int WS = I.ND <= MDR_WDMAX ? 18 * I.ND : 0;
   double *Wd = WS ? reinterpret_cast<double *>(smx_c + sizeof(RB) * P.J) + (threadIdx.x >> 5) * WS : nullptr;
   __shared__ double s_u[CU][MDR_USLOT];
+  constexpr bool FLAT = OP == 1 && !MDR_SWAP_WARP;
+  __shared__ __align__(16) double s_swd[FLAT ? CT * MDR_SWD : 1];
+  __shared__ SWU s_sw[FLAT ? CT : 1];
   __shared__ int s_t, s_b, s_lo, s_hi, s_next, s_end;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   double *U = s_u[wid];
@@ -405,16 +411,24 @@ __global__ void __launch_bounds__(32 * CU, 16 / CU) k_eval_c(DevInst I, DevPop P
       staged = b;
     }
     __syncthreads();
+    if (FLAT) {
+      for (int j = threadIdx.x; j < CT; j += blockDim.x)
+        sswap_stage<WIN>(I, v, R, I.ND + local * CT + j, s_sw[j], s_swd + j * MDR_SWD);
+      __syncthreads();
+    }
     double lam[4];
 #pragma unroll
     for (int i = 0; i < 4; i++) lam[i] = P.lam[b * 4 + i];
     Acc acc{~0ull, ~0ull, 0};
+    const int nit = FLAT ? (CT * I.W + 31) / 32 : CT;
     for (;;) {  // warps take the task's items dynamically
       int it = 0;
       if (lane == 0) it = atomicAdd(&s_item, 1);
       it = __shfl_sync(0xffffffffu, it, 0);
-      if (it >= CT) break;
-      if (OP == 2 && local >= nch) {
+      if (it >= nit) break;
+      if (FLAT) {
+        sswap_chunk<WIN, CT>(I, P, v, R, b, it, s_sw, s_swd, lam, mm, acc);
+      } else if (OP == 2 && local >= nch) {
         const int ra = (local - nch) * CT + it;
         if (ra < v.M) stos_r<WIN>(I, P, v, R, b, ra, lam, mm, acc);
       } else {

@@ -374,6 +374,139 @@ __device__ void sswap(const DevInst &I, const DevPop &P, const IV &v, const RB *
 }
 
 // ---------------------------------------------------------------------------
+// SWAP, flattened form (the default; MDR_SWAP_WARP=1 selects sswap above).
+// The u-side pieces of all CT customers of the CTA task are staged once, one
+// thread per customer, before the warps start; the warps then sweep the
+// task's (customer, granular slot) items 32 at a time.  Every lane is busy
+// (θ = 50 left 14 of every 64 slots of the per-customer sweep idle) and no
+// warp waits on a serial lane-0 staging chain per customer.  Same candidates,
+// same deltas, same keys as sswap.
+// ---------------------------------------------------------------------------
+struct SWU {
+  int u, ru, pu, nxtu, lastP1, lastS1, s1f1, s1f2;  // u < 0: out of range or not routed
+};
+#define MDR_SWD 30  // doubles per staged customer: seg l=1, seg l=2, P[ru][pu], S[ru][pu+2], S[ru][pu+3]
+
+template <bool WIN>
+__device__ __forceinline__ void sswap_stage(const DevInst &I, const IV &v, const RB *R, int u, SWU &c, double *U) {
+  c.u = -1;
+  if (u >= I.N) return;
+  const int lu = __ldg(v.loc + u);
+  if (lu < 0) return;
+  const int ru = loc_r(lu), pu = loc_p(lu);
+  const int k1 = R[ru].k, n1 = R[ru].n;
+  const int *sq1 = v.seq + ru * v.Kp;
+  const int nxtu = pu + 2 <= k1 ? __ldg(sq1 + pu + 2) : u;
+  c.u = u; c.ru = ru; c.pu = pu; c.nxtu = nxtu;
+  c.lastP1 = __ldg(sq1 + pu);
+  c.lastS1 = __ldg(sq1 + n1 - 1);
+  c.s1f1 = pu + 2 <= n1 - 1 ? __ldg(sq1 + pu + 2) : -1;
+  c.s1f2 = pu + 3 <= n1 - 1 ? __ldg(sq1 + pu + 3) : -1;
+  At<WIN> s1 = a_node<WIN>(I, u);
+  st_at<WIN>(U, s1);
+  if (pu + 2 <= k1) st_at<WIN>(U + 6, a_cat_ne<WIN>(I, s1, a_node<WIN>(I, nxtu)));
+  st_at<WIN>(U + 12, pre<WIN>(v, ru, pu));
+  if (c.s1f1 >= 0) st_at<WIN>(U + 18, suf<WIN>(v, ru, pu + 2, n1));
+  if (c.s1f2 >= 0) st_at<WIN>(U + 24, suf<WIN>(v, ru, pu + 3, n1));
+}
+
+// one 32-item chunk of the task's (customer, slot) space; full-warp call
+template <bool WIN, int CT>
+__device__ void sswap_chunk(const DevInst &I, const DevPop &P, const IV &v, const RB *R, int b, int chunk,
+                            const SWU *C, const double *UD, const double lam[4], bool mm, Acc &acc) {
+  const int lane = threadIdx.x & 31;
+  const int W = I.W;
+  const int item = chunk * 32 + lane;
+  const int j = item / W, t = item - j * W;
+  int u = -1;
+  if (j < CT) u = C[j].u;
+  int vv = -1;
+  if (u >= 0) vv = __ldg(I.lists + (size_t)(u - I.ND) * W + t);
+  int ru = -1, pu = 0, nxtu = 0, lastP1 = 0, lastS1 = 0, s1f1 = -1, s1f2 = -1;
+  const double *U = UD;
+  if (u >= 0) {
+    const SWU &c = C[j];
+    ru = c.ru; pu = c.pu; nxtu = c.nxtu; lastP1 = c.lastP1; lastS1 = c.lastS1; s1f1 = c.s1f1; s1f2 = c.s1f2;
+    U = UD + j * MDR_SWD;
+  }
+  int rv = -1, pv = -1;
+  if (vv >= 0 && vv != u) {
+    int lv = __ldg(v.loc + vv);
+    if (lv >= 0) { rv = loc_r(lv); pv = loc_p(lv); }
+  }
+  const RB &X1 = R[ru < 0 ? 0 : ru];
+  const int k1 = X1.k;
+  const bool same = rv == ru;
+  const bool inter = rv >= 0 && !same;
+  constexpr int NV = WIN ? 2 : 3;  // segment variants (len, rev): (1,0), (2,0), (2,1)
+  int k2 = 0, n2 = 0, nxtv = vv;
+  At<WIN> P2;
+  At<WIN> Y[NV];
+  if (inter) {
+    k2 = R[rv].k;
+    n2 = R[rv].n;
+    P2 = pre<WIN>(v, rv, pv);
+    if (pv + 2 <= k2) nxtv = __ldg(v.seq + rv * v.Kp + pv + 2);
+#pragma unroll
+    for (int yi = 0; yi < NV; yi++) {
+      const int lu_ = yi == 0 ? 1 : 2, au = yi == 2;
+      if (pu + lu_ <= k1) {
+        const int ua = lu_ == 1 ? u : nxtu;
+        At<WIN> sA = ld_at<WIN>(U + (lu_ == 1 ? 0 : 6), au ? ua : u, au ? u : ua);
+        Y[yi] = a_cat_l<WIN>(P2, sA, link_to_u(I, P2.last, sA.first));
+      }
+    }
+  }
+#pragma unroll
+  for (int xi = 0; xi < NV; xi++) {
+    const int lv_ = xi == 0 ? 1 : 2, av = xi == 2;
+    const bool xok = inter && pv + lv_ <= k2;
+    At<WIN> X, S2;
+    if (xok) {
+      At<WIN> sB = a_node<WIN>(I, vv);
+      if (lv_ == 2) sB = a_cat_ne<WIN>(I, sB, a_node<WIN>(I, nxtv));
+      if (av) swap_ends(sB);
+      X = a_cat_l<WIN>(ld_at<WIN>(U + 12, X1.dep, lastP1), sB, link_of(I, lastP1, sB.first));
+      S2 = suf<WIN>(v, rv, pv + lv_ + 1, n2);
+    }
+#pragma unroll
+    for (int yi = 0; yi < NV; yi++) {
+      const int lu_ = yi == 0 ? 1 : 2, au = yi == 2;
+      bool fol = false, gqf = false;
+      unsigned long long o = 0, key = 0;
+      if (rv >= 0) {
+        if (same) {
+          int flip = pu > pv;
+          Cand c;
+          c.r1 = ru; c.r2 = rv;
+          c.p1 = flip ? pv : pu; c.p2 = flip ? pu : pv;
+          c.l1 = flip ? lv_ : lu_; c.l2 = flip ? lu_ : lv_;
+          c.rev1 = flip ? av : au; c.rev2 = flip ? au : av;
+          c.depot = -1; c.mode = -1;
+          gqf = (c.p1 + c.l1 <= k1) && (c.p2 + c.l2 <= k1) && (c.p2 >= c.p1 + c.l1);
+          key = pack_key(c);
+        } else if (xok && pu + lu_ <= k1) {
+          const int sf = lu_ == 1 ? s1f1 : s1f2;
+          At<WIN> A = X;
+          if (sf >= 0) A = a_cat_l<WIN>(X, ld_at<WIN>(U + (lu_ == 1 ? 18 : 24), sf, lastS1), link_to_u(I, X.last, sf));
+          At<WIN> B = Y[yi];
+          if (S2.first >= 0) B = a_cat_l<WIN>(B, S2, link_of(I, B.last, S2.first));
+          double cA[5], cB[5];
+          contrib_fast<WIN>(I, A, X1.dep, X1.arr, k1 - lu_ + lv_, cA);
+          const RB &X2 = R[rv];
+          contrib_fast<WIN>(I, B, X2.dep, X2.arr, k2 - lv_ + lu_, cB);
+          fol = two_route_delta<WIN>(I, cA, cB, X1.rc, X2.rc, X1.clo, X2.clo, 0.0, 1, lam, acc,
+                                     [&] { return key_of(ru, pu, rv, pv, lu_, lv_, au, av, -1, -1); }, key, mm,
+                                     P.nanflag + b, o);
+        }
+      }
+      append_fol(P, b, fol, o, key);
+      enqueue_g(P, b, 1, gqf, key);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // TWO_OPT_STAR (moves.py:375-405, batch.py:475-494)
 // ---------------------------------------------------------------------------
 // A = PA (+) SB, B = PB (+) SA for the cut (r1, p1, r2, p2); SA/SB may be empty
