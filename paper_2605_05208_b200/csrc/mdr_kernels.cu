@@ -351,6 +351,9 @@ __global__ void __launch_bounds__(256, MDR_EVAL_MINB) k_eval(DevInst I, DevPop P
 #ifndef MDR_TGC
 #define MDR_TGC 1
 #endif
+#ifndef MDR_REL_WARP
+#define MDR_REL_WARP 0  // 1: per-customer warp sweep (srelocate) instead of the flattened chunks
+#endif
 #ifndef MDR_SWAP_WARP
 #define MDR_SWAP_WARP 0  // 1: per-customer warp sweep (sswap) instead of the flattened chunks
 #endif
@@ -366,6 +369,9 @@ __global__ void __launch_bounds__(32 * CU, 16 / CU) k_eval_c(DevInst I, DevPop P
   constexpr bool FLAT = OP == 1 && !MDR_SWAP_WARP;
   __shared__ __align__(16) double s_swd[FLAT ? CT * MDR_SWD : 1];
   __shared__ SWU s_sw[FLAT ? CT : 1];
+  constexpr bool FLATR = OP == 0 && !MDR_REL_WARP;
+  __shared__ __align__(16) double s_rld[FLATR ? CT * MDR_RLD : 1];
+  __shared__ RLU s_rl[FLATR ? CT : 1];
   __shared__ int s_t, s_b, s_lo, s_hi, s_next, s_end;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   double *U = s_u[wid];
@@ -416,17 +422,25 @@ __global__ void __launch_bounds__(32 * CU, 16 / CU) k_eval_c(DevInst I, DevPop P
         sswap_stage<WIN>(I, v, R, I.ND + local * CT + j, s_sw[j], s_swd + j * MDR_SWD);
       __syncthreads();
     }
+    if (FLATR) {
+      for (int j = threadIdx.x; j < CT; j += blockDim.x)
+        srel_stage<WIN>(I, v, R, I.ND + local * CT + j, s_rl[j], s_rld + j * MDR_RLD);
+      __syncthreads();
+    }
     double lam[4];
 #pragma unroll
     for (int i = 0; i < 4; i++) lam[i] = P.lam[b * 4 + i];
     Acc acc{~0ull, ~0ull, 0};
-    const int nit = FLAT ? (CT * I.W + 31) / 32 : CT;
+    const int ngc = (CT * I.W + 31) / 32;
+    const int nit = FLAT ? ngc : FLATR ? ngc + (CT * v.M + 31) / 32 : CT;
     for (;;) {  // warps take the task's items dynamically
       int it = 0;
       if (lane == 0) it = atomicAdd(&s_item, 1);
       it = __shfl_sync(0xffffffffu, it, 0);
       if (it >= nit) break;
-      if (FLAT) {
+      if (FLATR) {
+        srel_chunk<WIN, CT>(I, P, v, R, b, it < ngc ? it : it - ngc, it >= ngc, s_rl, s_rld, lam, mm, acc);
+      } else if (FLAT) {
         sswap_chunk<WIN, CT>(I, P, v, R, b, it, s_sw, s_swd, lam, mm, acc);
       } else if (OP == 2 && local >= nch) {
         const int ra = (local - nch) * CT + it;
@@ -1038,22 +1052,30 @@ static void launch_eval_g_region(const DevInst &I, const DevPop &P, const LsPara
 template <bool WIN, int CU, int CT>
 static void launch_staged(const DevInst &I, const DevPop &P, const LsParams &L, const cudaStream_t *side) {
   static int gc[3] = {0, 0, 0};
-  static size_t sm_set = 0;
-  const size_t sm = sizeof(RB) * (size_t)P.J + (I.ND <= MDR_WDMAX ? sizeof(double) * 18 * (size_t)I.ND * CU : 0);
-  if (sm_set < sm) {
-    cudaFuncSetAttribute(k_eval_c<WIN, 0, CU, CT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    cudaFuncSetAttribute(k_eval_c<WIN, 1, CU, CT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    cudaFuncSetAttribute(k_eval_c<WIN, 2, CU, CT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    // shared-memory carveout just large enough for the resident CTAs (16 / CU):
-    // the rest of the 228 KB stays L1 for the gathers (+2 % on C4 vs the default)
-    int pct = (int)(((16 / CU) * (sm + 3 * 1024) * 100 + 228 * 1024 - 1) / (228 * 1024));
-    if (getenv("MDR_CARVEOUT")) pct = atoi(getenv("MDR_CARVEOUT"));
-    if (pct > 100) pct = 100;
-    cudaFuncSetAttribute(k_eval_c<WIN, 0, CU, CT>, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
-    cudaFuncSetAttribute(k_eval_c<WIN, 1, CU, CT>, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
-    cudaFuncSetAttribute(k_eval_c<WIN, 2, CU, CT>, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+  static size_t sm_set[3] = {0, 0, 0};  // per evaluator: the sizes vary independently with J and ND
+  // dynamic shared memory: staged route boundaries, plus the per-warp depot-indexed
+  // precomputes for the evaluators that use them (2-opt*; relocate in its warp form)
+  const size_t smr = sizeof(RB) * (size_t)P.J;
+  const size_t smw = smr + (I.ND <= MDR_WDMAX ? sizeof(double) * 18 * (size_t)I.ND * CU : 0);
+  const size_t smo[3] = {MDR_REL_WARP ? smw : smr, smr, smw};
+  if (sm_set[0] < smo[0] || sm_set[1] < smo[1] || sm_set[2] < smo[2]) {
+    void *fn[3] = {(void *)k_eval_c<WIN, 0, CU, CT>, (void *)k_eval_c<WIN, 1, CU, CT>,
+                   (void *)k_eval_c<WIN, 2, CU, CT>};
+    for (int q = 0; q < 3; q++) {
+      if (sm_set[q] >= smo[q]) continue;
+      sm_set[q] = smo[q];
+      cudaFuncSetAttribute(fn[q], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smo[q]);
+      // shared-memory carveout just large enough for the resident CTAs (16 / CU):
+      // the rest of the 228 KB stays L1 for the gathers (+2 % on C4 vs the default)
+      cudaFuncAttributes fa;
+      size_t st = 3 * 1024;
+      if (cudaFuncGetAttributes(&fa, fn[q]) == cudaSuccess) st = fa.sharedSizeBytes + 1024;
+      int pct = (int)(((16 / CU) * (smo[q] + st) * 100 + 228 * 1024 - 1) / (228 * 1024));
+      if (getenv("MDR_CARVEOUT")) pct = atoi(getenv("MDR_CARVEOUT"));
+      if (pct > 100) pct = 100;
+      cudaFuncSetAttribute(fn[q], cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+    }
     cudaFuncSetAttribute(k_eval_g<WIN>, cudaFuncAttributePreferredSharedMemoryCarveout, 0);
-    sm_set = sm;
     gc[0] = 0;
   }
   if (!gc[0]) {
@@ -1061,16 +1083,16 @@ static void launch_staged(const DevInst &I, const DevPop &P, const LsParams &L, 
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     int per = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_eval_c<WIN, 0, CU, CT>, 32 * CU, sm);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_eval_c<WIN, 0, CU, CT>, 32 * CU, smo[0]);
     gc[0] = sms * (per < 1 ? 1 : per);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_eval_c<WIN, 1, CU, CT>, 32 * CU, sm);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_eval_c<WIN, 1, CU, CT>, 32 * CU, smo[1]);
     gc[1] = sms * (per < 1 ? 1 : per);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_eval_c<WIN, 2, CU, CT>, 32 * CU, sm);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_eval_c<WIN, 2, CU, CT>, 32 * CU, smo[2]);
     gc[2] = sms * (per < 1 ? 1 : per);
   }
-  k_eval_c<WIN, 0, CU, CT><<<gc[0], 32 * CU, sm, side[0]>>>(I, P, L);
-  k_eval_c<WIN, 1, CU, CT><<<gc[1], 32 * CU, sm, side[1]>>>(I, P, L);
-  k_eval_c<WIN, 2, CU, CT><<<gc[2], 32 * CU, sm, side[2]>>>(I, P, L);
+  k_eval_c<WIN, 0, CU, CT><<<gc[0], 32 * CU, smo[0], side[0]>>>(I, P, L);
+  k_eval_c<WIN, 1, CU, CT><<<gc[1], 32 * CU, smo[1], side[1]>>>(I, P, L);
+  k_eval_c<WIN, 2, CU, CT><<<gc[2], 32 * CU, smo[2], side[2]>>>(I, P, L);
 }
 
 template <bool WIN>

@@ -262,6 +262,169 @@ __device__ void srelocate(const DevInst &I, const DevPop &P, const IV &v, const 
 }
 
 // ---------------------------------------------------------------------------
+// RELOCATE, flattened form (the default; MDR_REL_WARP=1 selects srelocate).
+// The u-side pieces of the task's CT customers are staged once (one thread per
+// customer); the warps then sweep first the (customer, granular slot) items,
+// then the (customer, route) boundary items, 32 per chunk, so no lane idles on
+// a list or route-count tail and no warp waits on a per-customer staging
+// chain.  The front-insertion concat node(d) (+) seg is formed per candidate
+// (the warp form's per-depot Wd table is per customer, which the chunks mix).
+// Same candidates, deltas and keys as srelocate.
+// ---------------------------------------------------------------------------
+struct RLU {
+  int u, ru, pu, nxt;  // u < 0: out of range or not routed
+};
+#define MDR_RLD 24  // doubles per staged customer: removal terms l=1,2 [10], seg l=1 [6], seg l=2 [6], fleet_dec [1]
+
+template <bool WIN>
+__device__ __forceinline__ void srel_stage(const DevInst &I, const IV &v, const RB *R, int u, RLU &c, double *U) {
+  c.u = -1;
+  if (u >= I.N) return;
+  const int lu = __ldg(v.loc + u);
+  if (lu < 0) return;
+  const int ru = loc_r(lu), pu = loc_p(lu);
+  const RB &X1 = R[ru];
+  const int k1 = X1.k, n1 = X1.n;
+  const int nxt = pu + 2 <= k1 ? __ldg(v.seq + ru * v.Kp + pu + 2) : u;
+  c.u = u; c.ru = ru; c.pu = pu; c.nxt = nxt;
+  At<WIN> P1 = pre<WIN>(v, ru, pu);
+  for (int l = 1; l <= 2; l++) {
+    if (pu + l <= k1) {
+      At<WIN> A = P1;
+      if (pu + l + 1 <= n1 - 1) A = a_cat_ne<WIN>(I, P1, suf<WIN>(v, ru, pu + l + 1, n1));
+      contrib_fast<WIN>(I, A, X1.dep, X1.arr, k1 - l, U + 5 * (l - 1));
+    }
+  }
+  At<WIN> s1 = a_node<WIN>(I, u);
+  st_at<WIN>(U + 10, s1);
+  if (pu + 2 <= k1) st_at<WIN>(U + 16, a_cat_ne<WIN>(I, s1, a_node<WIN>(I, nxt)));
+  U[22] = I.nv_on ? __ldg(v.fl + X1.dep).y : 0.0;
+}
+
+// one 32-item chunk: granular items [0, CT*W) when bnd == false, else (customer, route) items [0, CT*M)
+template <bool WIN, int CT>
+__device__ void srel_chunk(const DevInst &I, const DevPop &P, const IV &v, const RB *R, int b, int chunk, bool bnd,
+                           const RLU *C, const double *UD, const double lam[4], bool mm, Acc &acc) {
+  const int lane = threadIdx.x & 31;
+  const int per = bnd ? v.M : I.W;
+  const int item = chunk * 32 + lane;
+  const int j = item / per, s = item - j * per;
+  int u = -1, ru = 0, pu = 0, nxt = 0;
+  const double *U = UD;
+  if (j < CT) {
+    const RLU c = C[j];
+    u = c.u; ru = c.ru; pu = c.pu; nxt = c.nxt;
+    U = UD + j * MDR_RLD;
+  }
+  const bool uok = u >= 0;
+  const RB &X1 = R[uok ? ru : 0];
+  const int k1 = X1.k;
+  const double fdec1 = U[22];
+  constexpr int nvar = WIN ? 2 : 3;
+  auto eval_links = [&](int len, int rev, int r2, int tgt, const At<WIN> &P2, const At<WIN> &S2, Link Lp, Link Ls,
+                        const RB &X2, unsigned long long &o, unsigned long long &key) -> bool {
+    At<WIN> seg = ld_at<WIN>(U + (len == 1 ? 10 : 16), rev ? (len == 1 ? u : nxt) : u, rev ? u : (len == 1 ? u : nxt));
+    At<WIN> B = a_cat_l<WIN>(P2, seg, Lp);
+    if (S2.first >= 0) B = a_cat_l<WIN>(B, S2, Ls);
+    double cB[5];
+    contrib_fast<WIN>(I, B, X2.dep, X2.arr, X2.k + len, cB);
+    double fleet_delta = 0.0;
+    int fn = 1;
+    if (I.nv_on && k1 - len == 0) { fleet_delta = 0.0 + fdec1; fn = 0; }
+    return two_route_delta<WIN>(I, U + 5 * (len - 1), cB, X1.rc, X2.rc, X1.clo, X2.clo, fleet_delta, fn, lam, acc,
+                                [&] { return key_of(ru, pu, r2, tgt, len, 0, rev, 0, -1, -1); }, key, mm,
+                                P.nanflag + b, o);
+  };
+  if (!bnd) {
+    const bool has2 = pu + 2 <= k1;
+    int vv = -1, lv = -1, sv = -1;
+    if (uok) vv = __ldg(I.lists + (size_t)(u - I.ND) * I.W + s);
+    Link Lvu{0.0, 0.0}, Lvn{0.0, 0.0}, Lus{0.0, 0.0}, Lns{0.0, 0.0};
+    if (vv >= 0) {
+      lv = __ldg(v.loc + vv);
+      sv = __ldg(v.nxs + vv);
+      Lvu = link_to_u(I, vv, u);
+      if (nvar == 3 && has2) Lvn = link_to_u(I, vv, nxt);
+      if (sv >= 0) {
+        Lus = link_of(I, u, sv);
+        if (has2) Lns = link_of(I, nxt, sv);
+      }
+    }
+    int rv = -1, tgt = -1;
+    if (lv >= 0) { rv = loc_r(lv); tgt = loc_p(lv) + 1; }
+    const bool same = rv == ru;
+    At<WIN> P2, S2;
+    if (rv >= 0 && !same) {
+      P2 = ld_tab<WIN>(v.tP, rv * v.Kp + tgt);
+      P2.first = vv;
+      P2.last = vv;
+      if (sv >= 0) {
+        S2 = ld_tab<WIN>(v.tS, rv * v.Kp + tgt + 1);
+        S2.first = sv;
+        S2.last = sv;
+      } else {
+        S2 = a_empty<WIN>();
+      }
+    }
+#pragma unroll
+    for (int vi = 0; vi < nvar; vi++) {
+      const int len = vi == 0 ? 1 : 2, rev = vi == 2;
+      bool ok = rv >= 0 && pu + len <= k1 && !(same && tgt > pu && tgt <= pu + len);
+      if (!rev) ok = ok && !(same && tgt == pu);
+      bool fol = false, gqf = false;
+      unsigned long long o = 0, key = 0;
+      if (ok) {
+        if (same) { gqf = true; key = key_of(ru, pu, rv, tgt, len, 0, rev, 0, -1, -1); }
+        else fol = eval_links(len, rev, rv, tgt, P2, S2, (len == 2 && rev) ? Lvn : Lvu,
+                              (len == 1 || rev) ? Lus : Lns, R[rv], o, key);
+      }
+      append_fol(P, b, fol, o, key);
+      enqueue_g(P, b, 0, gqf, key);
+    }
+    return;
+  }
+  const int rb = s;
+  const bool in = uok;
+  const bool same = rb == ru;
+#pragma unroll
+  for (int side = 0; side < 2; side++) {
+    int tgt = 0;
+    At<WIN> P2, S2;
+    if (in) {
+      const RB &X2 = R[rb];
+      if (side == 0) {
+        tgt = 0;
+        P2 = a_node<WIN>(I, X2.dep);
+        S2 = X2.sf_first >= 0 ? rb_sf<WIN>(X2) : a_empty<WIN>();
+      } else {
+        tgt = X2.k;
+        P2 = rb_pb<WIN>(X2);
+        S2 = I.open ? a_empty<WIN>() : a_node<WIN>(I, X2.arr);
+      }
+    }
+#pragma unroll
+    for (int vi = 0; vi < nvar; vi++) {
+      const int len = vi == 0 ? 1 : 2, rev = vi == 2;
+      bool ok = in && pu + len <= k1 && !(same && tgt == pu + len);
+      if (!rev) ok = ok && !(same && tgt == pu);
+      bool fol = false, gqf = false;
+      unsigned long long o = 0, key = 0;
+      if (ok) {
+        if (same) { gqf = true; key = key_of(ru, pu, rb, tgt, len, 0, rev, 0, -1, -1); }
+        else {
+          const int sf = rev ? (len == 1 ? u : nxt) : u, sl = rev ? u : (len == 1 ? u : nxt);
+          Link Ls{0.0, 0.0};
+          if (S2.first >= 0) Ls = link_of(I, sl, S2.first);
+          fol = eval_links(len, rev, rb, tgt, P2, S2, link_to_u(I, P2.last, sf), Ls, R[rb], o, key);
+        }
+      }
+      append_fol(P, b, fol, o, key);
+      enqueue_g(P, b, 0, gqf, key);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // SWAP (moves.py:314-358, batch.py:430-463), warp task = customer u
 // A = (P1 + segB) + S1, B = (P2 + segA) + S2: X = P1 + segB depends only on v's
 // segment (lv, av) and Y = P2 + segA only on u's (lu, au), so each is built
