@@ -241,7 +241,7 @@ def cpu_baseline(name, inst, consts, nbr, sols, depth, seconds=20.0):
     # one individual per thread: a population smaller than the host uses that many cores
     return {"value": cands / dt, "unit": "move-evals/s", "cores": min(k, threads), "kind": "port",
             "sample": f"{k} complete {name} descents (individuals 0..{k-1}, depth {depth}, multi-move) "
-                      f"on {threads} host threads, {dt:.1f} s, {cands} candidates",
+                      f"on {min(k, threads)} host threads, {dt:.1f} s, {cands} candidates",
             "descents_per_s": k / dt}
 
 
