@@ -15,6 +15,7 @@ from __future__ import annotations
 
 import ctypes as C
 import time
+import weakref
 from dataclasses import dataclass
 from typing import Optional
 
@@ -127,9 +128,12 @@ class DeviceSearch:
 
     def __init__(self, inst, consts, nbr, device: int = 0):
         self.session = session_for(inst, consts, nbr, device)
-        self.inst = inst
         self.pop: Optional[Population] = None
         self.last_stats = None
+
+    @property
+    def inst(self):
+        return self.session.inst
 
     def _ensure(self, sols, need=None):
         J, K = Population.caps_for(sols, self.inst)
@@ -208,6 +212,10 @@ def _searcher(inst, consts, nbr, device: int = 0) -> DeviceSearch:
     s = _SEARCHERS.get(key)
     if s is None or s.inst is not inst or s.session.nbr is not nbr:
         s = _SEARCHERS[key] = DeviceSearch(inst, consts, nbr, device)
+        try:  # the entry (and its device population) goes with the instance
+            weakref.finalize(inst, _SEARCHERS.pop, key, None)
+        except TypeError:
+            pass
     return s
 
 

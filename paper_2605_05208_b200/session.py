@@ -11,15 +11,28 @@ from .evaluation import ScalingConstants
 _SESSIONS: dict = {}
 
 
+def _ref(obj):
+    """Weak reference where the type allows one: a cache entry must not keep its
+    instance alive, or its finalizer (which frees the device copies) never runs."""
+    try:
+        return weakref.ref(obj)
+    except TypeError:
+        return lambda: obj
+
+
 class Session:
     def __init__(self, inst, consts, nbr, device: int):
-        self.inst = inst
+        self._inst = _ref(inst)
         self.consts = consts
         self.nbr = nbr
         self.device = device
         self.dinst = DeviceInstance(inst, consts, nbr, device)
         self._single = None
         self._single_sig = None
+
+    @property
+    def inst(self):
+        return self._inst()
 
     def single(self, sol, lam):
         """A B=1 population holding `sol` (re-uploaded only when it changed)."""
