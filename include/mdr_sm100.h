@@ -162,6 +162,10 @@ int mdr_get_timing(mdr_pop *pop, mdr_timing *out);
  * Replaces the rng.shuffle calls of localsearch.py:112-113. */
 int mdr_shuffle_stream(uint32_t *state, int32_t n_items, const uint8_t *items, int32_t n_passes, uint8_t *out);
 int mdr_set_profiling(mdr_pop *pop, int32_t on);
+/* evaluator shape the population's local search launches (diagnostic, lets the
+ * parity tests assert they ran the kernels the benchmark times):
+ * out = {staged evaluators on, items per CTA task, warps per CTA, B_cap} */
+int mdr_pop_info(mdr_pop *pop, int32_t out[4]);
 
 /* Repair insertion (genetic.repair_insert, genetic.py:174-244) on the device
  * for individuals 0..B-1 of the last upload: op FBI=0, IBI=1, FRI=2, IRI=3 (RI

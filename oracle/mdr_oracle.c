@@ -1087,6 +1087,7 @@ typedef struct {
   double *lam;
   const orc_ls_cfg *cfgs;
   orc_ls_stats *stats;
+  orc_sol_out *outs; /* optional: final routes per individual */
   int next;
   pthread_mutex_t mu;
   /* eval-only mode */
@@ -1124,6 +1125,24 @@ static void *pool_worker(void *arg) {
       pthread_mutex_unlock(&P->mu);
     } else {
       ls_core(P->I, &s, P->lam + 4 * b, &P->cfgs[b], &P->stats[b], NULL);
+      if (P->outs) {
+        orc_sol_out *o = &P->outs[b];
+        int64_t tot = 0;
+        for (int r = 0; r < s.m; r++) tot += s.r[r].k;
+        o->m = s.m;
+        if (s.m > o->cap_routes || tot > o->cap_cust) {
+          o->status = 3;
+        } else {
+          o->status = 0;
+          o->off[0] = 0;
+          for (int r = 0; r < s.m; r++) {
+            o->depart[r] = s.r[r].dep;
+            o->arrive[r] = s.r[r].arr;
+            memcpy(o->cust + o->off[r], s.r[r].c, sizeof(int32_t) * (size_t)s.r[r].k);
+            o->off[r + 1] = o->off[r] + s.r[r].k;
+          }
+        }
+      }
     }
     sol_free(&s);
   }
@@ -1147,6 +1166,17 @@ int orc_local_search_many(const orc_instance_desc *inst, int32_t B, const orc_fl
   memset(&P, 0, sizeof(P));
   P.I = inst; P.B = B; P.sols = sols; P.lam = lam; P.cfgs = cfgs; P.stats = stats;
   pool_run(&P, nthreads);
+  return 0;
+}
+
+int orc_local_search_many_out(const orc_instance_desc *inst, int32_t B, const orc_flat_sol *sols, double *lam,
+                              const orc_ls_cfg *cfgs, int32_t nthreads, orc_ls_stats *stats, orc_sol_out *outs) {
+  pool_t P;
+  memset(&P, 0, sizeof(P));
+  P.I = inst; P.B = B; P.sols = sols; P.lam = lam; P.cfgs = cfgs; P.stats = stats; P.outs = outs;
+  pool_run(&P, nthreads);
+  for (int b = 0; b < B; b++)
+    if (outs[b].status) return 3;
   return 0;
 }
 

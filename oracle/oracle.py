@@ -80,6 +80,7 @@ def lib():
         L.orc_leader_followers.restype = C.c_int64
         L.orc_local_search.restype = C.c_int
         L.orc_local_search_many.restype = C.c_int
+        L.orc_local_search_many_out.restype = C.c_int
         L.orc_eval_all_many.restype = C.c_int64
         L.orc_repair.restype = C.c_int
         L.orc_repair_many.restype = C.c_int
@@ -313,6 +314,50 @@ def local_search_many(oi: OracleInstance, sols, lams, depth, multi_move, kappa, 
                             C.c_int32(nthreads), ST)
     return [dict(passes=s.passes, accepted=s.accepted, op_evals=s.op_evals, cands=list(s.cands),
                  status=s.status) for s in ST]
+
+
+class SolOut(C.Structure):
+    _fields_ = [("cap_routes", C.c_int32), ("cap_cust", C.c_int32), ("m", C.c_int32), ("status", C.c_int32),
+                ("off", _i32p), ("cust", _i32p), ("depart", _i32p), ("arrive", _i32p)]
+
+
+def local_search_many_routes(oi: OracleInstance, sols, lams, depth, multi_move, kappa, lam_min, lam_max,
+                             perms_list, nthreads):
+    """local_search_many that also returns each individual's final routes and
+    penalties: [(routes, lam, stats)] in input order."""
+    L = lib()
+    B = len(sols)
+    flats = [_Flat(s) for s in sols]
+    FS = (FlatSol * B)(*[f.s for f in flats])
+    cfgs_keep = [_cfg(depth, multi_move, kappa, lam_min, lam_max, p) for p in perms_list]
+    CF = (LsCfg * B)(*[c for c, _ in cfgs_keep])
+    lam_a = np.ascontiguousarray(np.asarray(lams, np.float64).reshape(B, 4)).copy()
+    ST = (LsStats * B)()
+    OUT = (SolOut * B)()
+    keep = []
+    for b, s in enumerate(sols):
+        nc = sum(len(r.customers) for r in s.routes) + 1
+        cap_r = len(s.routes) * 4 + 64 + nc
+        bufs = (np.zeros(cap_r + 1, np.int32), np.zeros(nc, np.int32), np.zeros(cap_r, np.int32),
+                np.zeros(cap_r, np.int32))
+        keep.append(bufs)
+        o = OUT[b]
+        o.cap_routes, o.cap_cust = cap_r, nc
+        o.off, o.cust, o.depart, o.arrive = (_p(a, _i32p) for a in bufs)
+    rc = L.orc_local_search_many_out(C.byref(oi.desc), C.c_int32(B), FS, _p(lam_a, _f64p), CF,
+                                     C.c_int32(nthreads), ST, OUT)
+    if rc:
+        raise RuntimeError(f"oracle local_search_many_out status {rc}")
+    res = []
+    for b in range(B):
+        off, cust, dep, arr = keep[b]
+        m = OUT[b].m
+        routes = [(int(dep[r]), int(arr[r]), [int(c) for c in cust[off[r]:off[r + 1]]]) for r in range(m)]
+        s = ST[b]
+        res.append((routes, [float(x) for x in lam_a[b]],
+                    dict(passes=s.passes, accepted=s.accepted, op_evals=s.op_evals, cands=list(s.cands),
+                         status=s.status)))
+    return res
 
 
 def eval_all_many(oi: OracleInstance, sols, lams, nthreads):

@@ -105,6 +105,7 @@ def lib():
         L.mdr_local_search.argtypes = [vp, C.POINTER(LsCfg), C.POINTER(LsStats), vp]
         L.mdr_get_timing.argtypes = [vp, C.POINTER(Timing)]
         L.mdr_set_profiling.argtypes = [vp, C.c_int32]
+        L.mdr_pop_info.argtypes = [vp, i32p]
         L.mdr_shuffle_stream.argtypes = [C.POINTER(C.c_uint32), C.c_int32, u8p, C.c_int32, u8p]
         L.mdr_probe_l2_gbs.argtypes = [C.c_int32, C.c_int64, C.c_int32, f64p]
         L.mdr_probe_fp64_gops.argtypes = [C.c_int32, C.c_int32, f64p]
@@ -148,4 +149,4 @@ EXPORTED = ("mdr_last_error", "mdr_device_count", "mdr_build_info", "mdr_instanc
             "mdr_leader_followers", "mdr_totals", "mdr_local_search", "mdr_get_timing",
             "mdr_set_profiling", "mdr_shuffle_stream", "mdr_probe_l2_gbs",
             "mdr_probe_fp64_gops", "mdr_neighbor_build", "mdr_repair", "mdr_pop_download_range",
-            "mdr_pop_breakdown")
+            "mdr_pop_breakdown", "mdr_pop_info")

@@ -130,17 +130,27 @@ int mdr_instance_create(const mdr_instance_desc *d, int32_t device, mdr_instance
   CK(cudaSetDevice(device));
   mdr_instance *I = new mdr_instance();
   I->device = device;
+  auto bail = [&](int code, const std::string &msg) {
+    for (void *q : I->allocs) cudaFree(q);
+    delete I;
+    return fail(code, msg);
+  };
+#define CKI(call)                                                                              \
+  do {                                                                                         \
+    cudaError_t e__ = (call);                                                                  \
+    if (e__ != cudaSuccess) return bail(MDR_ERR_CUDA, std::string(#call ": ") + cudaGetErrorString(e__)); \
+  } while (0)
   DevInst &D = I->I;
   D.N = N; D.ND = ND; D.NC = N - ND; D.W = d->width;
   size_t nn = (size_t)N * N;
   double *dist = nullptr, *time = nullptr;
   int rc;
-  if ((rc = dalloc(I->allocs, &dist, nn))) { delete I; return rc; }
-  cudaMemcpy(dist, d->dist, nn * sizeof(double), cudaMemcpyHostToDevice);
+  if ((rc = dalloc(I->allocs, &dist, nn))) return bail(rc, g_err);
+  CKI(cudaMemcpy(dist, d->dist, nn * sizeof(double), cudaMemcpyHostToDevice));
   D.talias = (d->time == nullptr || d->time == d->dist);
   if (!D.talias) {
-    if ((rc = dalloc(I->allocs, &time, nn))) { delete I; return rc; }
-    cudaMemcpy(time, d->time, nn * sizeof(double), cudaMemcpyHostToDevice);
+    if ((rc = dalloc(I->allocs, &time, nn))) return bail(rc, g_err);
+    CKI(cudaMemcpy(time, d->time, nn * sizeof(double), cudaMemcpyHostToDevice));
   } else {
     time = dist;
   }
@@ -148,13 +158,13 @@ int mdr_instance_create(const mdr_instance_desc *d, int32_t device, mdr_instance
   std::vector<double4> node(N);
   for (int v = 0; v < N; v++) node[v] = make_double4(d->demand[v], d->service[v], d->tw_early[v], d->tw_late[v]);
   double4 *dnode = nullptr;
-  if ((rc = dalloc(I->allocs, &dnode, N))) { delete I; return rc; }
-  cudaMemcpy(dnode, node.data(), N * sizeof(double4), cudaMemcpyHostToDevice);
+  if ((rc = dalloc(I->allocs, &dnode, N))) return bail(rc, g_err);
+  CKI(cudaMemcpy(dnode, node.data(), N * sizeof(double4), cudaMemcpyHostToDevice));
   D.node = dnode;
   int *lists = nullptr;
   size_t nl = (size_t)(N - ND) * d->width;
-  if ((rc = dalloc(I->allocs, &lists, nl))) { delete I; return rc; }
-  cudaMemcpy(lists, d->lists + (size_t)ND * d->width, nl * sizeof(int), cudaMemcpyHostToDevice);
+  if ((rc = dalloc(I->allocs, &lists, nl))) return bail(rc, g_err);
+  CKI(cudaMemcpy(lists, d->lists + (size_t)ND * d->width, nl * sizeof(int), cudaMemcpyHostToDevice));
   D.lists = lists;
   D.Q = d->capacity; D.Dmax = d->max_duration; D.NV = d->fleet_per_depot;
   D.d_on = !std::isinf(d->max_duration);
@@ -177,12 +187,8 @@ int mdr_instance_create(const mdr_instance_desc *d, int32_t device, mdr_instance
     D.sym = getenv("MDR_NO_SYM") ? 0 : sym;
   }
   D.rD = 1.0 / d->max_duration;
-  cudaError_t e = cudaDeviceSynchronize();
-  if (e != cudaSuccess) {
-    for (void *p : I->allocs) cudaFree(p);
-    delete I;
-    return fail(MDR_ERR_CUDA, std::string("instance upload: ") + cudaGetErrorString(e));
-  }
+  CKI(cudaDeviceSynchronize());
+#undef CKI
   *out = I;
   return MDR_OK;
 }
@@ -194,15 +200,29 @@ void mdr_instance_destroy(mdr_instance *I) {
   delete I;
 }
 
+static int pop_build(mdr_pop *p, mdr_instance *inst, int32_t Bcap, int32_t J, int32_t K, int32_t Fcap);
+
 int mdr_pop_create(mdr_instance *inst, int32_t Bcap, int32_t J, int32_t K, int32_t Fcap, mdr_pop **out) {
   if (!inst || !out) return fail(MDR_ERR_ARG, "null argument");
   if (Bcap < 1 || J < 1 || K < 1 || Fcap < 1) return fail(MDR_ERR_ARG, "capacities must be >= 1");
   if (J > 4094) return fail(MDR_ERR_ARG, "J_cap must be <= 4094 (12-bit route field of the packed key)");
   if (K > 500) return fail(MDR_ERR_ARG, "K_cap must be <= 500 (9-bit position field of the packed key)");
   CK(cudaSetDevice(inst->device));
-  mdr_pop *p = new mdr_pop();
-  memset(&p->tm, 0, sizeof(p->tm));
+  mdr_pop *p = new mdr_pop();  // value-initialised: every handle starts null
   p->inst = inst;
+  const int rc = pop_build(p, inst, Bcap, J, K, Fcap);
+  if (rc != MDR_OK) {
+    const std::string msg = g_err;
+    mdr_pop_destroy(p);  // frees whatever was allocated before the failure
+    return fail(rc, msg);
+  }
+  *out = p;
+  return MDR_OK;
+}
+
+// every failure returns straight out; mdr_pop_create then releases the partial pop
+static int pop_build(mdr_pop *p, mdr_instance *inst, int32_t Bcap, int32_t J, int32_t K, int32_t Fcap) {
+  memset(&p->tm, 0, sizeof(p->tm));
   p->B = 0;
   DevPop &P = p->P;
   const DevInst &I = inst->I;
@@ -292,7 +312,6 @@ int mdr_pop_create(mdr_instance *inst, int32_t Bcap, int32_t J, int32_t K, int32
   CK(cudaEventCreateWithFlags(&p->join[1], cudaEventDisableTiming));
   for (int q = 0; q < 3; q++) CK(cudaStreamCreateWithFlags(&p->side[q], cudaStreamNonBlocking));
   for (int q = 0; q < 4; q++) CK(cudaEventCreateWithFlags(&p->fev[q], cudaEventDisableTiming));
-  *out = p;
   return MDR_OK;
 }
 
@@ -303,13 +322,16 @@ void mdr_pop_destroy(mdr_pop *p) {
   if (p->d_perms) cudaFree(p->d_perms);
   if (p->d_xfer) cudaFree(p->d_xfer);
   if (p->h_hdr) cudaFreeHost(p->h_hdr);
-  for (int i = 0; i < 8; i++) cudaEventDestroy(p->ev[i]);
+  for (int i = 0; i < 8; i++)
+    if (p->ev[i]) cudaEventDestroy(p->ev[i]);
   for (cudaEvent_t e : p->rev) cudaEventDestroy(e);
-  cudaStreamDestroy(p->ls);
-  cudaEventDestroy(p->join[0]);
-  cudaEventDestroy(p->join[1]);
-  for (int q = 0; q < 3; q++) cudaStreamDestroy(p->side[q]);
-  for (int q = 0; q < 4; q++) cudaEventDestroy(p->fev[q]);
+  if (p->ls) cudaStreamDestroy(p->ls);
+  for (int q = 0; q < 2; q++)
+    if (p->join[q]) cudaEventDestroy(p->join[q]);
+  for (int q = 0; q < 3; q++)
+    if (p->side[q]) cudaStreamDestroy(p->side[q]);
+  for (int q = 0; q < 4; q++)
+    if (p->fev[q]) cudaEventDestroy(p->fev[q]);
   for (void *q : {(void *)p->rp_pre, (void *)p->rp_suf, (void *)p->rp_c1, (void *)p->rp_c2, (void *)p->rp_p1, (void *)p->rp_pend,
                   (void *)p->rp_status, (void *)p->rp_stats, (void *)p->rp_fold, (void *)p->rp_foldi,
                   (void *)p->bd_rt, (void *)p->bd_io})
@@ -878,6 +900,15 @@ int mdr_pop_breakdown(mdr_pop *p, const double *lam, double *out, void *stream) 
   CK(cudaGetLastError());
   CK(cudaMemcpyAsync(out, d_out, sizeof(double) * 6 * B, cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
+  return MDR_OK;
+}
+
+int mdr_pop_info(mdr_pop *p, int32_t out[4]) {
+  if (!p || !out) return fail(MDR_ERR_ARG, "null argument");
+  out[0] = p->P.staged;
+  out[1] = p->P.ct;
+  out[2] = p->P.ct == MDR_LARGE_CT ? MDR_LARGE_CU : MDR_SMALL_CU;
+  out[3] = p->P.Bcap;
   return MDR_OK;
 }
 

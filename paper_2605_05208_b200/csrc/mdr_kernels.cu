@@ -1029,6 +1029,15 @@ void launch_plan(const DevInst &I, const DevPop &P, const LsParams &L, cudaStrea
   k_plan<<<1, 1024, 0, s>>>(I, P, L);
 }
 
+// launch-configuration caches are per device: attributes set with
+// cudaFuncSetAttribute and SM-count grids apply to the device current when set
+#define MDR_MAXDEV 16
+static int cur_dev() {
+  int d = 0;
+  cudaGetDevice(&d);
+  return (d < 0 || d >= MDR_MAXDEV) ? 0 : d;
+}
+
 template <typename K>
 static int grid_for(K kern) {
   int dev = 0, sms = 148, per = 1;
@@ -1043,7 +1052,8 @@ int eval_grid_size(bool win) { return win ? grid_for(k_eval<true, 0>) : grid_for
 
 template <bool WIN>
 static void launch_eval_g_region(const DevInst &I, const DevPop &P, const LsParams &L, cudaStream_t s, int region) {
-  static int g = 0;  // full occupancy of the (latency-bound) generic evaluator
+  static int gd[MDR_MAXDEV] = {0};  // full occupancy of the (latency-bound) generic evaluator
+  int &g = gd[cur_dev()];
   if (!g) g = grid_for(k_eval_g<WIN>);
   k_eval_g<WIN><<<g, 256, 0, s>>>(I, P, L, region);
 }
@@ -1051,8 +1061,11 @@ static void launch_eval_g_region(const DevInst &I, const DevPop &P, const LsPara
 // the three staged evaluators of one (CU, CT) shape on the side streams
 template <bool WIN, int CU, int CT>
 static void launch_staged(const DevInst &I, const DevPop &P, const LsParams &L, const cudaStream_t *side) {
-  static int gc[3] = {0, 0, 0};
-  static size_t sm_set[3] = {0, 0, 0};  // per evaluator: the sizes vary independently with J and ND
+  static int gcd[MDR_MAXDEV][3];
+  static size_t sm_setd[MDR_MAXDEV][3];  // per evaluator: the sizes vary independently with J and ND
+  const int dv = cur_dev();
+  int *gc = gcd[dv];
+  size_t *sm_set = sm_setd[dv];
   // dynamic shared memory: staged route boundaries, plus the per-warp depot-indexed
   // precomputes for the evaluators that use them (2-opt*; relocate in its warp form)
   const size_t smr = sizeof(RB) * (size_t)P.J;
@@ -1098,7 +1111,8 @@ static void launch_staged(const DevInst &I, const DevPop &P, const LsParams &L, 
 template <bool WIN>
 static void launch_eval_t(const DevInst &I, const DevPop &P, const LsParams &L, cudaStream_t s, const cudaStream_t *side,
                           cudaEvent_t *ev) {
-  static int g[6] = {0, 0, 0, 0, 0, 0};
+  static int gd[MDR_MAXDEV][6];
+  int *g = gd[cur_dev()];
   if (!g[0]) {
     g[0] = grid_for(k_eval<WIN, 0>); g[1] = grid_for(k_eval<WIN, 1>); g[2] = grid_for(k_eval<WIN, 2>);
     g[3] = grid_for(k_eval<WIN, 3>); g[4] = grid_for(k_eval<WIN, 4>); g[5] = grid_for(k_eval<WIN, 5>);
@@ -1157,7 +1171,9 @@ void launch_eval_g(const DevInst &I, const DevPop &P, const LsParams &L, int gri
 
 void launch_select(const DevInst &I, const DevPop &P, const LsParams &L, bool win, cudaStream_t s) {
   size_t sm = select_smem(P);
-  static size_t set_t = 0, set_f = 0;  // attribute set once per size (not during graph capture)
+  static size_t set_td[MDR_MAXDEV], set_fd[MDR_MAXDEV];  // attribute set once per size (not during graph capture)
+  const int dv = cur_dev();
+  size_t &set_t = set_td[dv], &set_f = set_fd[dv];
   if (win) {
     if (sm > 48 * 1024 && sm > set_t) {
       cudaFuncSetAttribute(k_select<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);

@@ -238,6 +238,12 @@ class Population:
         self.h2d_bytes_repair = int(off.nbytes + pend.nbytes)
         return stats
 
+    def info(self) -> dict:
+        """Evaluator shape of this population (mdr_pop_info)."""
+        out = np.zeros(4, np.int32)
+        check(_lib.lib().mdr_pop_info(self.handle, ptr(out, i32p)), "mdr_pop_info")
+        return dict(staged=int(out[0]), items_per_task=int(out[1]), warps_per_cta=int(out[2]), B_cap=int(out[3]))
+
     def set_profiling(self, on: bool):
         check(_lib.lib().mdr_set_profiling(self.handle, int(on)))
 

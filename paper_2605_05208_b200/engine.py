@@ -264,6 +264,10 @@ def run_islands(inst, cfg: SolverConfig, batch: int = 64, exchange_every: int = 
     import torch.distributed as dist
     from . import distributed as DS
     from dataclasses import replace
+    if int(exchange_every) < 1:  # checked before the first collective: no rank may fail mid-loop
+        raise ValueError("exchange_every must be >= 1")
+    if int(batch) < 1:
+        raise ValueError("batch must be >= 1")
     rank, world = dist.get_rank(group), dist.get_world_size(group)
     R = _Run(inst, replace(cfg, seed=cfg.seed + rank), nbr)
     cap = inst.n_customers  # routes with customers never exceed the customer count

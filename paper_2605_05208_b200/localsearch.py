@@ -25,7 +25,7 @@ from ._lib import CapacityError
 from .batch import SolutionCache, evaluate_candidates, leader_and_followers
 from .device import Population
 from .moves import ALL_OPS, Op, move_plan
-from .session import session_for
+from .session import same_consts, session_for
 
 VIOLATION_TOL = 1e-9
 
@@ -208,9 +208,14 @@ _SEARCHERS: dict = {}
 
 
 def _searcher(inst, consts, nbr, device: int = 0) -> DeviceSearch:
-    key = (id(inst), id(nbr), device)
+    """The reusable device search of (instance, device).  Other lists or other
+    scaling constants (baked into the device instance) replace the entry and
+    free the old device population."""
+    key = (id(inst), device)
     s = _SEARCHERS.get(key)
-    if s is None or s.inst is not inst or s.session.nbr is not nbr:
+    if (s is None or s.inst is not inst or s.session.nbr is not nbr
+            or (consts is not None and not same_consts(consts, s.session.consts))):
+        _SEARCHERS.pop(key, None)
         s = _SEARCHERS[key] = DeviceSearch(inst, consts, nbr, device)
         try:  # the entry (and its device population) goes with the instance
             weakref.finalize(inst, _SEARCHERS.pop, key, None)
@@ -225,12 +230,19 @@ def local_search_population(sols, penalties, cfg: SearchConfig, nbr, consts, ins
     are updated in place.  Returns the per-individual stats.  on_feasible(D, sol),
     if given, is called per individual (in order) with its lowest-D feasible
     state passed through, as `local_search` does."""
+    if not (len(sols) == len(penalties) == len(rngs)):
+        raise ValueError("sols, penalties and rngs must have the same length")
+    if not sols:
+        return []
+    p0 = penalties[0]
+    for p in penalties[1:]:  # one device launch carries one (kappa, lam_min, lam_max)
+        if (p.kappa, p.lam_min, p.lam_max) != (p0.kappa, p0.lam_min, p0.lam_max):
+            raise ValueError("local_search_population: all penalty states must share kappa, lam_min and lam_max")
     search = _searcher(inst, consts, nbr, device)
     ops = enabled_operators(inst)
     perms = np.stack([draw_permutations(r, ops, cfg.depth + 1) for r in rngs])
     lams = [p.lam for p in penalties]
     dl = -1.0 if deadline is None else max(0.0, deadline - time.monotonic())
-    p0 = penalties[0]
     routes, lam, stats = search.run(sols, lams, perms, cfg, p0.kappa, p0.lam_min, p0.lam_max, dl,
                                     snapshot_best=on_feasible is not None)
     best = search.pop.download_best() if on_feasible is not None else None

@@ -51,15 +51,26 @@ class Session:
         self._single_sig = None
 
 
+def same_consts(a, b) -> bool:
+    return (a.gamma, a.theta) == (b.gamma, b.theta)
+
+
 def session_for(inst, consts=None, nbr=None, device: int = 0) -> Session:
-    """Session keyed by the identity of the instance and neighbour lists."""
-    key = (id(inst), id(nbr) if nbr is not None else None, device)
+    """The device session of an instance on a device.
+
+    One entry per (instance, device, with/without lists): a call with other
+    neighbour lists or other scaling constants (baked into the device
+    instance) replaces the entry, which frees the old device instance and its
+    populations -- repeated runs that build fresh lists do not accumulate
+    device memory.  The entry goes with the instance (weak reference)."""
+    key = (id(inst), device, nbr is None)
     s = _SESSIONS.get(key)
     if s is not None and s.inst is inst and s.nbr is nbr:
-        if consts is None or (consts.gamma, consts.theta) == (s.consts.gamma, s.consts.theta):
+        if consts is None or same_consts(consts, s.consts):
             return s
     if consts is None:
         consts = ScalingConstants.from_instance(inst)
+    _SESSIONS.pop(key, None)  # drop the stale entry before allocating the new one
     s = Session(inst, consts, nbr, device)
     _SESSIONS[key] = s
     try:

@@ -42,3 +42,36 @@ def test_caches_release_instances():
         del inst, consts, nbr, sol
         gc.collect()
         assert len(S._SESSIONS) == n0 and len(LS._SEARCHERS) == m0
+
+
+class _FakeDev:
+    """Stand-in for the device instance (no GPU): records what it was built with."""
+
+    def __init__(self, inst, consts, nbr=None, device=0):
+        self.consts, self.nbr = consts, nbr
+
+
+def test_searcher_rebuilt_when_scaling_constants_change(monkeypatch):
+    monkeypatch.setattr(S, "DeviceInstance", _FakeDev)
+    inst = W.make_instance(random.Random(4), "mdvrp", n_customers=12, n_depots=2)
+    nbr = build(inst, NeighborConfig(5), ScalingConstants.from_instance(inst))
+    a = LS._searcher(inst, ScalingConstants(1.0, 19.0), nbr)
+    assert LS._searcher(inst, ScalingConstants(1.0, 19.0), nbr) is a
+    b = LS._searcher(inst, ScalingConstants(2.0, 19.0), nbr)
+    assert b is not a and b.session.dinst.consts.gamma == 2.0
+    c = LS._searcher(inst, ScalingConstants(2.0, 7.0), nbr)
+    assert c is not b and c.session.dinst.consts.theta == 7.0
+
+
+def test_fresh_lists_per_run_do_not_accumulate_sessions(monkeypatch):
+    """engine runs build new NeighborLists each time: one entry per instance stays."""
+    monkeypatch.setattr(S, "DeviceInstance", _FakeDev)
+    inst = W.make_instance(random.Random(5), "mdvrp", n_customers=12, n_depots=2)
+    consts = ScalingConstants.from_instance(inst)
+    n0, m0 = len(S._SESSIONS), len(LS._SEARCHERS)
+    for _ in range(5):
+        nbr = build(inst, NeighborConfig(5), consts)
+        LS._searcher(inst, consts, nbr)
+        S.session_for(inst, consts, None)
+    assert len(S._SESSIONS) == n0 + 2  # with and without lists
+    assert len(LS._SEARCHERS) == m0 + 1
