@@ -109,6 +109,11 @@ typedef struct mdr_timing {
   double geval_ms; /* generic-path evaluator after the evaluators (intra-route, 2-opt, depot
                       operators; 0 when the population is small enough that these are
                       drained on the evaluators' graph branches, inside eval_ms) */
+  /* profiling pass only: the evaluation phase serialised on one stream, per part:
+   * [0] relocate staged evaluator, [1] its intra-route drain (k_eval_g region 1),
+   * [2] swap, [3] its drain, [4] 2-opt*, [5] depot (+2-opt) enumerators and region-0 drain */
+  double kern_ms[6];
+  int64_t kern_rounds;
 } mdr_timing;
 
 const char *mdr_last_error(void);
@@ -162,6 +167,34 @@ int mdr_get_timing(mdr_pop *pop, mdr_timing *out);
  * Replaces the rng.shuffle calls of localsearch.py:112-113. */
 int mdr_shuffle_stream(uint32_t *state, int32_t n_items, const uint8_t *items, int32_t n_passes, uint8_t *out);
 int mdr_set_profiling(mdr_pop *pop, int32_t on);
+/* Population management of the generation loop.
+ * n members; member i's edge set = edge_keys[edge_off[i] .. edge_off[i+1]), sorted unique
+ * int64 keys a*N+b with a <= b (model.py:217-228).  dist: [n*n] row-major, in/out: rows and
+ * columns >= row0 are (re)computed as solution_distance (population.py:19-24), the rest is
+ * kept (distances do not change while both members live).  If n > mu, survivor_selection
+ * (population.py:103-116) runs on cost[i] (penalised cost) and birth[i] (unique) and writes
+ * the removed indices, in removal order, to removed[0 .. n-mu).
+ * Replaces Population.distance_matrix / survivor_selection (population.py:94-116). */
+/* Initial solutions of B individuals (genetic.initial_solution, genetic.py:251-294):
+ * order[ooff[b*ND+d] .. ooff[b*ND+d+1]) = depot d's nearest-depot members of individual b after
+ * the caller's rng.shuffle; each is inserted at its feasible slot of least distance increase, else
+ * in a new route (d, d) while the fleet allows, else left over: n_left[b] customers in
+ * left[b*N_C ..] (insertion order).  The routes replace the population's individuals 0..B-1
+ * (depot-major order); the caller repairs the leftovers (mdr_repair, IBI). */
+int mdr_construct(mdr_pop *pop, int32_t B, const int32_t *ooff, const int32_t *order, int32_t *n_left, int32_t *left,
+                  void *stream);
+
+/* Forward simulation of n_routes node sequences (route r = seq[off[r] .. off[r+1]), depots
+ * included as Route.sequence gives them): out[r*6 ..] = {distance, load, duration, time_warp,
+ * late_count, minimal duration (want_min; else = duration)}.  Replaces simulate_route /
+ * minimal_duration (model.py:242-314), the per-route part of check_feasible (model.py:349-392). */
+int mdr_route_sim(mdr_instance *inst, int32_t n_routes, const int32_t *off, const int32_t *seq, int32_t want_min,
+                  double *out);
+
+int mdr_population_select(int32_t device, int32_t n, int32_t row0, const int64_t *edge_off, const int64_t *edge_keys,
+                          double *dist, int32_t mu, double xi, const double *cost, const int64_t *birth,
+                          int32_t *removed);
+
 /* evaluator shape the population's local search launches (diagnostic, lets the
  * parity tests assert they ran the kernels the benchmark times):
  * out = {staged evaluators on, items per CTA task, warps per CTA, B_cap} */

@@ -17,10 +17,10 @@ from .moves import (ALL_OPS, MODE_ARRIVE, MODE_BOTH, MODE_DEPART, CandidateSet, 
 from .batch import DeltaArrays, SolutionCache, evaluate_candidates, leader_and_followers
 from .localsearch import (DeviceSearch, SearchConfig, apply_moves, enabled_operators, evaluate_batch,
                           local_search, local_search_population, select_moves)
-from .genetic import InsertionOperator, repair_insert, repair_population
+from .genetic import InsertionOperator, initial_solution, initial_solutions, repair_insert, repair_population
 from .formats import ParseError, parse_instance, read_solution, write_solution
 from .engine import RunStats, SolverConfig, run, run_batched, run_islands
-from .evaluation import EvalBreakdown, evaluate, move_delta
+from .evaluation import EvalBreakdown, RouteAttr, evaluate
 from .feasibility import FeasibilityReport, check_feasible, minimal_duration, simulate_route
 
 __all__ = [
@@ -30,9 +30,9 @@ __all__ = [
     "enumerate_candidates", "move_plan", "DeltaArrays", "SolutionCache", "evaluate_candidates",
     "leader_and_followers", "DeviceSearch", "SearchConfig", "apply_moves", "enabled_operators",
     "evaluate_batch", "local_search", "local_search_population", "select_moves",
-    "InsertionOperator", "repair_insert", "repair_population",
+    "InsertionOperator", "initial_solution", "initial_solutions", "repair_insert", "repair_population",
     "ParseError", "parse_instance", "read_solution", "write_solution",
     "RunStats", "SolverConfig", "run", "run_batched", "run_islands",
-    "EvalBreakdown", "evaluate", "move_delta", "FeasibilityReport", "check_feasible", "minimal_duration",
+    "EvalBreakdown", "RouteAttr", "evaluate", "FeasibilityReport", "check_feasible", "minimal_duration",
     "simulate_route",
 ]

@@ -69,7 +69,8 @@ class RepairStats(C.Structure):
 class Timing(C.Structure):
     _fields_ = [("eval_ms", C.c_double), ("select_ms", C.c_double), ("plan_ms", C.c_double),
                 ("total_ms", C.c_double), ("eval_launches", C.c_int64), ("rounds", C.c_int64),
-                ("cands_total", C.c_int64), ("geval_ms", C.c_double)]
+                ("cands_total", C.c_int64), ("geval_ms", C.c_double), ("kern_ms", C.c_double * 6),
+                ("kern_rounds", C.c_int64)]
 
 
 _L = None
@@ -117,6 +118,10 @@ def lib():
         L.mdr_neighbor_build.argtypes = [C.c_int32, C.c_int32, C.c_int32, f64p, f64p, f64p, f64p, f64p, C.c_double,
                                          C.c_double, C.c_double, C.c_int32, C.POINTER(C.c_int32), u8p,
                                          C.POINTER(C.c_float)]
+        L.mdr_population_select.argtypes = [C.c_int32, C.c_int32, C.c_int32, i64p, i64p, f64p, C.c_int32,
+                                            C.c_double, f64p, i64p, i32p]
+        L.mdr_construct.argtypes = [vp, C.c_int32, i32p, i32p, i32p, i32p, vp]
+        L.mdr_route_sim.argtypes = [vp, C.c_int32, i32p, i32p, C.c_int32, f64p]
         _L = L
     return _L
 
@@ -149,4 +154,5 @@ EXPORTED = ("mdr_last_error", "mdr_device_count", "mdr_build_info", "mdr_instanc
             "mdr_leader_followers", "mdr_totals", "mdr_local_search", "mdr_get_timing",
             "mdr_set_profiling", "mdr_shuffle_stream", "mdr_probe_l2_gbs",
             "mdr_probe_fp64_gops", "mdr_neighbor_build", "mdr_repair", "mdr_pop_download_range",
+            "mdr_population_select", "mdr_route_sim", "mdr_construct",
             "mdr_pop_breakdown", "mdr_pop_info")

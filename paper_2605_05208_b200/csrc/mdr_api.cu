@@ -58,7 +58,8 @@ struct mdr_pop {
   int profiling;
   mdr_timing tm;
   cudaEvent_t ev[8];
-  std::vector<cudaEvent_t> rev;  // per-round events when profiling (4 per round)
+  std::vector<cudaEvent_t> rev;  // per-round events when profiling (5 per round)
+  std::vector<cudaEvent_t> kev;  // per-round per-evaluator events when profiling (7 per round)
   cudaStream_t ls;               // private stream of the round loop (graph capture)
   cudaEvent_t join[2];
   cudaStream_t side[3];          // fork/join branches of the per-operator evaluators
@@ -325,6 +326,7 @@ void mdr_pop_destroy(mdr_pop *p) {
   for (int i = 0; i < 8; i++)
     if (p->ev[i]) cudaEventDestroy(p->ev[i]);
   for (cudaEvent_t e : p->rev) cudaEventDestroy(e);
+  for (cudaEvent_t e : p->kev) cudaEventDestroy(e);
   if (p->ls) cudaStreamDestroy(p->ls);
   for (int q = 0; q < 2; q++)
     if (p->join[q]) cudaEventDestroy(p->join[q]);
@@ -883,6 +885,66 @@ int mdr_repair(mdr_pop *p, int32_t op, const int32_t *pend_off, const int32_t *p
   return MDR_OK;
 }
 
+int mdr_construct(mdr_pop *p, int32_t B, const int32_t *ooff, const int32_t *order, int32_t *n_left, int32_t *left,
+                  void *stream) {
+  if (!p || !ooff || !n_left || !left) return fail(MDR_ERR_ARG, "null argument");
+  const DevInst &I = p->inst->I;
+  DevPop &P = p->P;
+  if (B < 0 || B > P.Bcap) return fail(MDR_ERR_ARG, "B exceeds the population capacity");
+  const int NC = I.N - I.ND;
+  const int tot = ooff[(size_t)B * I.ND];
+  if (tot > 0 && !order) return fail(MDR_ERR_ARG, "null order");
+  int Jd = 1;
+  for (int b = 0; b < B; b++) {
+    std::vector<char> seen(I.N, 0);
+    for (int d = 0; d < I.ND; d++) {
+      const int a = ooff[b * I.ND + d], e = ooff[b * I.ND + d + 1];
+      if (e < a) return fail(MDR_ERR_ARG, "ooff must be non-decreasing");
+      Jd = std::max(Jd, e - a);
+      for (int t = a; t < e; t++) {
+        const int c = order[t];
+        if (c < I.ND || c >= I.N || seen[c]) return fail(MDR_ERR_ARG, "order holds a non-customer or a repeat");
+        seen[c] = 1;
+      }
+    }
+  }
+  Jd = std::min(Jd, P.J);
+  cudaStream_t s = (cudaStream_t)stream;
+  CK(cudaSetDevice(p->inst->device));
+  const size_t tab = (size_t)std::max(B, 1) * Jd * P.Kp * repair_attr_bytes();
+  int rc;
+  if ((rc = regrow(&p->rp_pre, p->rp_cap[0], tab)) || (rc = regrow(&p->rp_suf, p->rp_cap[1], tab))) return rc;
+  int *d_buf = nullptr;
+  const size_t nbuf = (size_t)B * I.ND + 1 + tot + 2 * (size_t)std::max(B, 1) + (size_t)std::max(B, 1) * NC;
+  CK(cudaMalloc(&d_buf, sizeof(int) * nbuf));
+  int *d_ooff = d_buf, *d_order = d_ooff + (size_t)B * I.ND + 1, *d_nl = d_order + tot, *d_st = d_nl + std::max(B, 1),
+      *d_left = d_st + std::max(B, 1);
+  std::vector<int> st(std::max(B, 1));
+  auto run = [&]() -> int {
+    CK(cudaMemcpyAsync(d_ooff, ooff, sizeof(int) * ((size_t)B * I.ND + 1), cudaMemcpyHostToDevice, s));
+    if (tot) CK(cudaMemcpyAsync(d_order, order, sizeof(int) * tot, cudaMemcpyHostToDevice, s));
+    launch_construct(I, P, B, d_ooff, d_order, p->rp_pre, p->rp_suf, Jd, d_nl, d_left, d_st, s);
+    CK(cudaGetLastError());
+    if (B) {
+      CK(cudaMemcpyAsync(st.data(), d_st, sizeof(int) * B, cudaMemcpyDeviceToHost, s));
+      CK(cudaMemcpyAsync(n_left, d_nl, sizeof(int) * B, cudaMemcpyDeviceToHost, s));
+      CK(cudaMemcpyAsync(left, d_left, sizeof(int) * (size_t)B * NC, cudaMemcpyDeviceToHost, s));
+    }
+    CK(cudaStreamSynchronize(s));
+    return MDR_OK;
+  };
+  rc = run();
+  cudaFree(d_buf);
+  if (rc) return rc;
+  for (int b = 0; b < B; b++)
+    if (st[b]) return fail(MDR_ERR_CAPACITY, "construction needs more routes (J) or a longer route (K)");
+  p->B = B;
+  if (B > 0) launch_rebuild(I, P, B, I.win, s);
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(s));
+  return MDR_OK;
+}
+
 int mdr_pop_breakdown(mdr_pop *p, const double *lam, double *out, void *stream) {
   if (!p || !out) return fail(MDR_ERR_ARG, "null argument");
   const int B = p->B;
@@ -1013,7 +1075,17 @@ int mdr_local_search(mdr_pop *p, const mdr_ls_cfg *cfg, mdr_ls_stats *stats, voi
       launch_plan(I, P, L, s);
       if (dbg && cudaStreamSynchronize(s)) return fail(MDR_ERR_CUDA, "k_plan failed");
       if (prof) cudaEventRecord(ev_at(ev_used + 1), s);
-      launch_eval(I, P, L, p->grid, I.win, s, p->side, p->fev);
+      cudaEvent_t *kt = nullptr;
+      if (prof) {
+        const size_t need = (size_t)(ev_used / 5 + 1) * 7;
+        while (p->kev.size() < need) {
+          cudaEvent_t e;
+          cudaEventCreate(&e);
+          p->kev.push_back(e);
+        }
+        kt = p->kev.data() + (ev_used / 5) * 7;
+      }
+      launch_eval(I, P, L, p->grid, I.win, s, p->side, p->fev, kt);
       if (dbg && cudaStreamSynchronize(s)) return fail(MDR_ERR_CUDA, "k_eval failed");
       if (prof) cudaEventRecord(ev_at(ev_used + 2), s);
       launch_eval_g(I, P, L, p->grid, I.win, s);
@@ -1059,6 +1131,15 @@ int mdr_local_search(mdr_pop *p, const mdr_ls_cfg *cfg, mdr_ls_stats *stats, voi
       p->tm.geval_ms += g;
       p->tm.select_ms += c;
       p->tm.eval_launches++;
+      if (P.staged) {
+        cudaEvent_t *kt = p->kev.data() + (e / 5) * 7;
+        for (int q = 0; q < 6; q++) {
+          float x = 0;
+          cudaEventElapsedTime(&x, kt[q], kt[q + 1]);
+          p->tm.kern_ms[q] += x;
+        }
+        p->tm.kern_rounds++;
+      }
       if (rlog) fprintf(rlog, "%lld,%.4f,%.4f,%.4f,%.4f\n", e / 5, a, b2, g, c);
     }
     if (rlog) fclose(rlog);
@@ -1097,6 +1178,41 @@ int mdr_local_search(mdr_pop *p, const mdr_ls_cfg *cfg, mdr_ls_stats *stats, voi
   if (worst == MDR_ERR_CAPACITY) return fail(worst, "capacity exceeded during local search (J_cap/K_cap/F_cap)");
   if (worst) return fail(worst, "local search stopped with an error status");
   return MDR_OK;
+}
+
+int mdr_route_sim(mdr_instance *inst, int32_t n_routes, const int32_t *off, const int32_t *seq, int32_t want_min,
+                  double *out) {
+  if (!inst || n_routes < 0 || (n_routes > 0 && (!off || !seq || !out))) return fail(MDR_ERR_ARG, "null argument");
+  if (n_routes == 0) return MDR_OK;
+  const DevInst &I = inst->I;
+  for (int r = 0; r < n_routes; r++) {
+    if (off[r + 1] - off[r] < 1) return fail(MDR_ERR_ARG, "empty route sequence");
+  }
+  const int ns = off[n_routes];
+  for (int i = 0; i < ns; i++)
+    if (seq[i] < 0 || seq[i] >= I.N) return fail(MDR_ERR_ARG, "node id out of range");
+  CK(cudaSetDevice(inst->device));
+  int *d_off = nullptr, *d_seq = nullptr;
+  double *d_raw = nullptr, *d_out = nullptr;
+  int rc = MDR_OK;
+  auto run = [&]() -> int {
+    CK(cudaMalloc(&d_off, sizeof(int) * (n_routes + 1)));
+    CK(cudaMalloc(&d_seq, sizeof(int) * ns));
+    CK(cudaMalloc(&d_raw, sizeof(double) * ns));
+    CK(cudaMalloc(&d_out, sizeof(double) * 6 * n_routes));
+    CK(cudaMemcpy(d_off, off, sizeof(int) * (n_routes + 1), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(d_seq, seq, sizeof(int) * ns, cudaMemcpyHostToDevice));
+    launch_route_sim(I, n_routes, d_off, d_seq, want_min, d_raw, d_out, 0);
+    CK(cudaGetLastError());
+    CK(cudaMemcpy(out, d_out, sizeof(double) * 6 * n_routes, cudaMemcpyDeviceToHost));
+    return MDR_OK;
+  };
+  rc = run();
+  cudaFree(d_off);
+  cudaFree(d_seq);
+  cudaFree(d_raw);
+  cudaFree(d_out);
+  return rc;
 }
 
 }  // extern "C"

@@ -466,6 +466,210 @@ __global__ void __launch_bounds__(32 * CU, 16 / CU) k_eval_c(DevInst I, DevPop P
   }
 }
 
+// ---------------------------------------------------------------------------
+// Pipelined relocate / swap evaluators (the default for OP 0 and 1): the same
+// flattened chunks as k_eval_c, but with no CTA-wide barrier.  Task staging is
+// double-buffered -- two copies of the route boundaries and of the CT staged
+// customers -- and handed over with mbarriers: the first warp to run out of
+// items of task t fetches and stages task t+1 into the other buffer (one warp:
+// routes strided over the lanes, one customer per lane) while the other warps
+// finish task t; a warp releases a buffer (bar_free, one arrive per warp) when
+// it is done with a task and waits on bar_ready before the next one.  The
+// stager of a buffer waits for the release of its previous use, so no warp
+// ever reads a buffer being rewritten.  Per task and warp the (dF, key) minimum
+// and the candidate count are flushed to the individual as before.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ unsigned smem_u32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mb_init(unsigned long long *bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mb_arrive(unsigned long long *bar) {
+  asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.release.cta.shared::cta.b64 st, [%0];\n\t}" ::"r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void mb_wait(unsigned long long *bar, unsigned parity) {
+  unsigned ok = 0;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  } while (!ok);
+}
+
+template <bool WIN>
+__device__ __forceinline__ void stage_routes_warp(const DevInst &I, const IV &v, RB *R, int lane) {
+  for (int r = lane; r < v.M; r += 32) {
+    const int4 mt = __ldg(v.rm + r);
+    const int n = mt.x + (I.open ? 1 : 2);
+    const int *sq = v.seq + r * v.Kp;
+    RB &x = R[r];
+    x.k = mt.x; x.dep = mt.y; x.arr = mt.z; x.clo = mt.w; x.n = n;
+    const double4 rc = ldg4(v.rc + r);
+    x.rc[0] = rc.x; x.rc[1] = rc.y; x.rc[2] = rc.z; x.rc[3] = rc.w;
+    if (n - 1 >= 1) {
+      st_at<WIN>(x.sf, ld_tab<WIN>(v.tS, r * v.Kp + 1));
+      x.sf_first = __ldg(sq + 1);
+      x.sf_last = __ldg(sq + n - 1);
+    } else {
+      x.sf_first = -1;
+      x.sf_last = -1;
+    }
+    st_at<WIN>(x.pb, ld_tab<WIN>(v.tP, r * v.Kp + mt.x));
+    x.pb_last = __ldg(sq + mt.x);
+  }
+}
+
+// k_eval_p's stager: one warp fetches the next task and stages it into buffer nb
+struct PipeShared {
+  RB *R0;
+  double *ud;  // [2][CT * UDW]
+  void *cust;  // RLU[2][CT] or SWU[2][CT]
+  unsigned long long *bar_ready, *bar_free;
+  int *b, *local, *item, *first, *rbuf, *nst;
+  int *next, *end, *lo, *hi, *bi;
+};
+
+template <bool WIN, int OP, int CT>
+__device__ __forceinline__ void pipe_stage(const DevInst &I, const DevPop &P, const PipeShared &S, int nb) {
+  constexpr int UDW = OP == 0 ? MDR_RLD : MDR_SWD;
+  const int lane = threadIdx.x & 31;
+  const int total = P.optasks[OP];
+  const int cnt = P.opcnt[OP];
+  const int *OFF = P.opoff + OP * (P.Bcap + 1);
+  const int *OB = P.opb + OP * P.Bcap;
+  const int nst = S.nst[nb];
+  if (nst > 0) mb_wait(&S.bar_free[nb], (nst - 1) & 1);  // the previous use of nb is released
+  if (lane == 0) {
+    if (*S.next >= *S.end) {
+      const int t0 = atomicAdd(P.task_next + OP, MDR_TGC);
+      *S.next = t0;
+      *S.end = min(t0 + MDR_TGC, total);
+    }
+    const int t = *S.next < *S.end ? (*S.next)++ : total;
+    int b = -1;
+    if (t < total) {
+      if (t < *S.lo || t >= *S.hi) {
+        int l2 = 0, h2 = cnt - 1;
+        while (l2 < h2) {
+          const int mid = (l2 + h2 + 1) >> 1;
+          if (OFF[mid] <= t) l2 = mid; else h2 = mid - 1;
+        }
+        *S.bi = OB[l2];
+        *S.lo = OFF[l2];
+        *S.hi = OFF[l2 + 1];
+      }
+      b = *S.bi;
+    }
+    S.b[nb] = b;
+    S.local[nb] = t - *S.lo;
+    S.item[nb] = 0;
+    S.first[nb] = 0;
+  }
+  __syncwarp();
+  const int b = S.b[nb];
+  if (b >= 0) {
+    const IV v = make_iv(P, b);
+    RB *R = S.R0 + (size_t)nb * P.J;
+    if (S.rbuf[nb] != b) {
+      stage_routes_warp<WIN>(I, v, R, lane);
+      __syncwarp();
+      if (lane == 0) S.rbuf[nb] = b;
+    }
+    const int u = I.ND + S.local[nb] * CT + lane;
+    double *U = S.ud + ((size_t)nb * CT + lane) * UDW;
+    if (lane < CT) {
+      if (OP == 0) srel_stage<WIN>(I, v, R, u, reinterpret_cast<RLU *>(S.cust)[nb * CT + lane], U);
+      else sswap_stage<WIN>(I, v, R, u, reinterpret_cast<SWU *>(S.cust)[nb * CT + lane], U);
+    }
+  }
+  __syncwarp();
+  __threadfence_block();
+  if (lane == 0) {
+    S.nst[nb] = nst + 1;
+    mb_arrive(&S.bar_ready[nb]);
+  }
+}
+
+template <bool WIN, int OP, int CU, int CT>
+__global__ void __launch_bounds__(32 * CU, 16 / CU) k_eval_p(DevInst I, DevPop P, LsParams L) {
+  static_assert(OP == 0 || OP == 1, "pipelined form: relocate and swap");
+  static_assert(CT <= 32, "one staged customer per lane");
+  extern __shared__ __align__(16) unsigned char smx_c[];
+  RB *const R0 = reinterpret_cast<RB *>(smx_c);
+  constexpr int UDW = OP == 0 ? MDR_RLD : MDR_SWD;
+  __shared__ __align__(16) double s_ud[2][CT * UDW];
+  __shared__ RLU s_rl[OP == 0 ? 2 : 1][OP == 0 ? CT : 1];
+  __shared__ SWU s_sw[OP == 1 ? 2 : 1][OP == 1 ? CT : 1];
+  __shared__ __align__(8) unsigned long long bar_ready[2], bar_free[2];
+  __shared__ int s_b[2], s_local[2], s_item[2], s_first[2], s_rbuf[2], s_nst[2];
+  __shared__ int s_next, s_end, s_lo, s_hi, s_bi;
+  const int lane = threadIdx.x & 31;
+  const bool mm = L.multi_move != 0;
+  if (threadIdx.x == 0) {
+    mb_init(&bar_ready[0], 1);
+    mb_init(&bar_ready[1], 1);
+    mb_init(&bar_free[0], CU);
+    mb_init(&bar_free[1], CU);
+    s_next = 0; s_end = 0; s_lo = 0; s_hi = 0; s_bi = -1;
+    s_rbuf[0] = s_rbuf[1] = -1;
+    s_nst[0] = s_nst[1] = 0;
+  }
+  __syncthreads();
+  PipeShared S;
+  S.R0 = R0;
+  S.ud = &s_ud[0][0];
+  S.cust = OP == 0 ? (void *)&s_rl[0][0] : (void *)&s_sw[0][0];
+  S.bar_ready = bar_ready; S.bar_free = bar_free;
+  S.b = s_b; S.local = s_local; S.item = s_item; S.first = s_first; S.rbuf = s_rbuf; S.nst = s_nst;
+  S.next = &s_next; S.end = &s_end; S.lo = &s_lo; S.hi = &s_hi; S.bi = &s_bi;
+  if ((threadIdx.x >> 5) == 0) pipe_stage<WIN, OP, CT>(I, P, S, 0);
+  int buf = 0;
+  unsigned use[2] = {0u, 0u};
+  for (;;) {
+    mb_wait(&bar_ready[buf], use[buf] & 1);
+    const int b = s_b[buf];
+    if (b < 0) break;
+    const IV v = make_iv(P, b);
+    const RB *R = R0 + (size_t)buf * P.J;
+    double lam[4];
+#pragma unroll
+    for (int i = 0; i < 4; i++) lam[i] = P.lam[b * 4 + i];
+    Acc acc{~0ull, ~0ull, 0};
+    const int ngc = (CT * I.W + 31) / 32;
+    const int nit = OP == 1 ? ngc : ngc + (CT * v.M + 31) / 32;
+    for (;;) {
+      int it = 0;
+      if (lane == 0) it = atomicAdd(&s_item[buf], 1);
+      it = __shfl_sync(0xffffffffu, it, 0);
+      if (it >= nit) break;
+      if (OP == 0)
+        srel_chunk<WIN, CT>(I, P, v, R, b, it < ngc ? it : it - ngc, it >= ngc, s_rl[OP == 0 ? buf : 0], s_ud[buf],
+                            lam, mm, acc);
+      else
+        sswap_chunk<WIN, CT>(I, P, v, R, b, it, s_sw[OP == 1 ? buf : 0], s_ud[buf], lam, mm, acc);
+    }
+    OK r = warp_min(OK{acc.o, acc.k});
+    int n = acc.n;
+#pragma unroll
+    for (int s = 16; s > 0; s >>= 1) n += __shfl_xor_sync(0xffffffffu, n, s);
+    int first = 0;
+    __syncwarp();
+    if (lane == 0) {
+      leader_min(P.leader + b, r.o, r.k);
+      if (n) atomicAdd(&P.cands[(size_t)b * 6 + OP], (unsigned long long)n);
+      first = atomicAdd(&s_first[buf], 1) == 0;
+      mb_arrive(&bar_free[buf]);
+    }
+    first = __shfl_sync(0xffffffffu, first, 0);
+    use[buf]++;
+    if (first) pipe_stage<WIN, OP, CT>(I, P, S, buf ^ 1);
+    buf ^= 1;
+  }
+}
+
 // generic evaluator: intra-route relocate/swap, 2-opt, depot operators,
 // one thread per queued candidate through eval_cand (batch.py:365-553)
 template <bool WIN>
@@ -1060,7 +1264,7 @@ static void launch_eval_g_region(const DevInst &I, const DevPop &P, const LsPara
 
 // the three staged evaluators of one (CU, CT) shape on the side streams
 template <bool WIN, int CU, int CT>
-static void launch_staged(const DevInst &I, const DevPop &P, const LsParams &L, const cudaStream_t *side) {
+static void launch_staged_one(const DevInst &I, const DevPop &P, const LsParams &L, const cudaStream_t *side, int only) {
   static int gcd[MDR_MAXDEV][3];
   static size_t sm_setd[MDR_MAXDEV][3];  // per evaluator: the sizes vary independently with J and ND
   const int dv = cur_dev();
@@ -1070,9 +1274,14 @@ static void launch_staged(const DevInst &I, const DevPop &P, const LsParams &L, 
   // precomputes for the evaluators that use them (2-opt*; relocate in its warp form)
   const size_t smr = sizeof(RB) * (size_t)P.J;
   const size_t smw = smr + (I.ND <= MDR_WDMAX ? sizeof(double) * 18 * (size_t)I.ND * CU : 0);
-  const size_t smo[3] = {MDR_REL_WARP ? smw : smr, smr, smw};
+  // pipelined relocate / swap (k_eval_p): two route-boundary buffers; MDR_NO_PIPE=1 selects k_eval_c
+  static int pipe_env = -1;
+  if (pipe_env < 0) pipe_env = getenv("MDR_NO_PIPE") ? 0 : 1;
+  const bool pipe = pipe_env && !MDR_REL_WARP && !MDR_SWAP_WARP && CT <= 32;
+  const size_t smo[3] = {pipe ? 2 * smr : (MDR_REL_WARP ? smw : smr), pipe ? 2 * smr : smr, smw};
   if (sm_set[0] < smo[0] || sm_set[1] < smo[1] || sm_set[2] < smo[2]) {
-    void *fn[3] = {(void *)k_eval_c<WIN, 0, CU, CT>, (void *)k_eval_c<WIN, 1, CU, CT>,
+    void *fn[3] = {pipe ? (void *)k_eval_p<WIN, 0, CU, CT> : (void *)k_eval_c<WIN, 0, CU, CT>,
+                   pipe ? (void *)k_eval_p<WIN, 1, CU, CT> : (void *)k_eval_c<WIN, 1, CU, CT>,
                    (void *)k_eval_c<WIN, 2, CU, CT>};
     for (int q = 0; q < 3; q++) {
       if (sm_set[q] >= smo[q]) continue;
@@ -1096,28 +1305,64 @@ static void launch_staged(const DevInst &I, const DevPop &P, const LsParams &L, 
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     int per = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_eval_c<WIN, 0, CU, CT>, 32 * CU, smo[0]);
+    if (pipe) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_eval_p<WIN, 0, CU, CT>, 32 * CU, smo[0]);
+    else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_eval_c<WIN, 0, CU, CT>, 32 * CU, smo[0]);
     gc[0] = sms * (per < 1 ? 1 : per);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_eval_c<WIN, 1, CU, CT>, 32 * CU, smo[1]);
+    if (pipe) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_eval_p<WIN, 1, CU, CT>, 32 * CU, smo[1]);
+    else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_eval_c<WIN, 1, CU, CT>, 32 * CU, smo[1]);
     gc[1] = sms * (per < 1 ? 1 : per);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_eval_c<WIN, 2, CU, CT>, 32 * CU, smo[2]);
     gc[2] = sms * (per < 1 ? 1 : per);
   }
-  k_eval_c<WIN, 0, CU, CT><<<gc[0], 32 * CU, smo[0], side[0]>>>(I, P, L);
-  k_eval_c<WIN, 1, CU, CT><<<gc[1], 32 * CU, smo[1], side[1]>>>(I, P, L);
-  k_eval_c<WIN, 2, CU, CT><<<gc[2], 32 * CU, smo[2], side[2]>>>(I, P, L);
+  if (pipe) {
+    if (only < 0 || only == 0) k_eval_p<WIN, 0, CU, CT><<<gc[0], 32 * CU, smo[0], side[0]>>>(I, P, L);
+    if (only < 0 || only == 1) k_eval_p<WIN, 1, CU, CT><<<gc[1], 32 * CU, smo[1], side[1]>>>(I, P, L);
+  } else {
+    if (only < 0 || only == 0) k_eval_c<WIN, 0, CU, CT><<<gc[0], 32 * CU, smo[0], side[0]>>>(I, P, L);
+    if (only < 0 || only == 1) k_eval_c<WIN, 1, CU, CT><<<gc[1], 32 * CU, smo[1], side[1]>>>(I, P, L);
+  }
+  if (only < 0 || only == 2) k_eval_c<WIN, 2, CU, CT><<<gc[2], 32 * CU, smo[2], side[2]>>>(I, P, L);
 }
 
+template <bool WIN, int CU, int CT>
+static void launch_staged(const DevInst &I, const DevPop &P, const LsParams &L, const cudaStream_t *side) {
+  launch_staged_one<WIN, CU, CT>(I, P, L, side, -1);
+}
+
+// kt (profiling only): 7 timing events; the branches are then serialised on s and
+// kt[0..6] bracket relocate | its intra drain | swap | its drain | 2-opt* | depot
+// enumerators + region-0 drain, so each evaluator's own duration is measured
 template <bool WIN>
 static void launch_eval_t(const DevInst &I, const DevPop &P, const LsParams &L, cudaStream_t s, const cudaStream_t *side,
-                          cudaEvent_t *ev) {
+                          cudaEvent_t *ev, cudaEvent_t *kt) {
   static int gd[MDR_MAXDEV][6];
   int *g = gd[cur_dev()];
   if (!g[0]) {
     g[0] = grid_for(k_eval<WIN, 0>); g[1] = grid_for(k_eval<WIN, 1>); g[2] = grid_for(k_eval<WIN, 2>);
     g[3] = grid_for(k_eval<WIN, 3>); g[4] = grid_for(k_eval<WIN, 4>); g[5] = grid_for(k_eval<WIN, 5>);
   }
-  if (P.staged) {
+  if (P.staged && kt) {
+    const cudaStream_t ser[3] = {s, s, s};
+    cudaEventRecord(kt[0], s);
+    if (P.ct == MDR_LARGE_CT) launch_staged_one<WIN, MDR_LARGE_CU, MDR_LARGE_CT>(I, P, L, ser, 0);
+    else launch_staged_one<WIN, MDR_SMALL_CU, MDR_SMALL_CT>(I, P, L, ser, 0);
+    cudaEventRecord(kt[1], s);
+    if (P.gbase[1] > 0) launch_eval_g_region<WIN>(I, P, L, s, 1);
+    cudaEventRecord(kt[2], s);
+    if (P.ct == MDR_LARGE_CT) launch_staged_one<WIN, MDR_LARGE_CU, MDR_LARGE_CT>(I, P, L, ser, 1);
+    else launch_staged_one<WIN, MDR_SMALL_CU, MDR_SMALL_CT>(I, P, L, ser, 1);
+    cudaEventRecord(kt[3], s);
+    if (P.gbase[1] > 0) launch_eval_g_region<WIN>(I, P, L, s, 2);
+    cudaEventRecord(kt[4], s);
+    if (P.ct == MDR_LARGE_CT) launch_staged_one<WIN, MDR_LARGE_CU, MDR_LARGE_CT>(I, P, L, ser, 2);
+    else launch_staged_one<WIN, MDR_SMALL_CU, MDR_SMALL_CT>(I, P, L, ser, 2);
+    cudaEventRecord(kt[5], s);
+    if (!WIN) k_eval<WIN, 3><<<g[3], 256, 0, s>>>(I, P, L);
+    k_eval<WIN, 4><<<g[4], 256, 0, s>>>(I, P, L);
+    k_eval<WIN, 5><<<g[5], 256, 0, s>>>(I, P, L);
+    if (P.gbase[1] > 0) launch_eval_g_region<WIN>(I, P, L, s, 0);
+    cudaEventRecord(kt[6], s);
+  } else if (P.staged) {
     // relocate / swap / 2-opt* as parallel branches (fork/join): their
     // persistent grids back-fill each other's tails
     cudaEventRecord(ev[0], s);
@@ -1156,10 +1401,10 @@ static void launch_eval_t(const DevInst &I, const DevPop &P, const LsParams &L, 
 }
 
 void launch_eval(const DevInst &I, const DevPop &P, const LsParams &L, int grid, bool win, cudaStream_t s,
-                 const cudaStream_t *side, cudaEvent_t *ev) {
+                 const cudaStream_t *side, cudaEvent_t *ev, cudaEvent_t *kt) {
   (void)grid;
-  if (win) launch_eval_t<true>(I, P, L, s, side, ev);
-  else launch_eval_t<false>(I, P, L, s, side, ev);
+  if (win) launch_eval_t<true>(I, P, L, s, side, ev, kt);
+  else launch_eval_t<false>(I, P, L, s, side, ev, kt);
 }
 
 void launch_eval_g(const DevInst &I, const DevPop &P, const LsParams &L, int grid, bool win, cudaStream_t s) {

@@ -20,12 +20,14 @@ void launch_repair(const DevInst &I, const DevPop &P, int B, int op, const int *
                    void *pre, void *suf, double *c1, double *c2, int *p1, double *fold, int *foldi, int Pcap,
                    int *status, long long *stats, cudaStream_t s);
 size_t repair_attr_bytes();
+void launch_construct(const DevInst &I, const DevPop &P, int B, const int *ooff, const int *order, void *pre,
+                      void *suf, int Jd, int *n_left, int *left, int *status, cudaStream_t s);
 void launch_breakdown(const DevInst &I, const DevPop &P, int B, const double *lam, double *rt, double *out,
                       cudaStream_t s);
 
 void launch_plan(const DevInst &I, const DevPop &P, const LsParams &L, cudaStream_t s);
 void launch_eval(const DevInst &I, const DevPop &P, const LsParams &L, int grid, bool win, cudaStream_t s,
-                 const cudaStream_t *side, cudaEvent_t *ev);
+                 const cudaStream_t *side, cudaEvent_t *ev, cudaEvent_t *kt = nullptr);
 void launch_eval_g(const DevInst &I, const DevPop &P, const LsParams &L, int grid, bool win, cudaStream_t s);
 void launch_select(const DevInst &I, const DevPop &P, const LsParams &L, bool win, cudaStream_t s);
 void launch_eval_mat(const DevInst &I, const DevPop &P, int b, int op, const MatCands &c, const double *lam,
@@ -36,6 +38,8 @@ void launch_totals(const DevInst &I, const DevPop &P, int b, double *out, cudaSt
 void launch_lf_prep(const MatCands &c, const MatDeltas &d, unsigned long long *ord, unsigned long long *key,
                     unsigned char *flag, int *nan, cudaStream_t s);
 int eval_grid_size(bool win);
+void launch_route_sim(const DevInst &I, int nr, const int *off, const int *seq, int want_min, double *raw,
+                      double *out, cudaStream_t s);
 void launch_unpack(const DevInst &I, const DevPop &P, int B, const int *rbase, const int *coff, const int *cust,
                    const int *dep, const int *arr, cudaStream_t s);
 void launch_pack(const DevPop &P, int b0, int B, int best, int *rbase, int *coff, int *cust, int *dep, int *arr, int *hdr,

@@ -405,6 +405,119 @@ void launch_repair(const DevInst &I, const DevPop &P, int B, int op, const int *
 
 size_t repair_attr_bytes() { return sizeof(RAt); }
 
+// ---------------------------------------------------------------------------
+// Initial solutions (genetic.initial_solution, genetic.py:251-294), one CTA per
+// individual.  Depot by depot (id order), the depot's members are inserted in
+// the given (caller-shuffled) order: every route of the depot is scanned by a
+// warp with r_scan in feasible-only mode (cost = route distance increase of
+// the _attr_feasible candidates, genetic.py:109-116, 271-279), the first minimum
+// over (route, position) in scan order wins (strict '<', as the reference's
+// nested loop), else a new route (d, d, [c]) while the depot's fleet allows,
+// else the customer is left over.  The depot's routes are appended to the
+// individual's route list (sol.routes.extend order); pre/suf hold only the
+// current depot's routes (indexed from its first route).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(RP_THREADS) k_construct(DevInst I, DevPop P, int B, const int *ooff,
+                                                          const int *order, RAt *g_pre, RAt *g_suf, int Jd,
+                                                          int *n_left, int *left, int *status) {
+  const int b = blockIdx.x;
+  if (b >= B) return;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = RP_THREADS / 32;
+  __shared__ double s_m1[RP_THREADS / 32];
+  __shared__ int s_r[RP_THREADS / 32], s_p[RP_THREADS / 32];
+  __shared__ int s_m, s_r0, s_nl, s_err, s_touch;
+  if (tid == 0) { s_m = 0; s_nl = 0; s_err = 0; }
+  __syncthreads();
+  const double lam0[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int d = 0; d < I.ND && !s_err; d++) {
+    if (tid == 0) s_r0 = s_m;
+    __syncthreads();
+    RepView V;
+    V.Kp = P.Kp; V.J = P.J; V.K = P.K;
+    V.seq = P.seq + ((size_t)b * P.J + s_r0) * P.Kp;  // this depot's routes, local index 0..
+    V.rm = P.rmeta + (size_t)b * P.J + s_r0;
+    V.pre = g_pre + (size_t)b * Jd * P.Kp;
+    V.suf = g_suf + (size_t)b * Jd * P.Kp;
+    const int o0 = ooff[b * I.ND + d], o1 = ooff[b * I.ND + d + 1];
+    for (int t = o0; t < o1; t++) {
+      const int cst = order[t];
+      const int md = s_m - s_r0;
+      // per thread: first minimum over its routes (increasing route order), then
+      // the warp's minimum by (cost, route)
+      double bm = CUDART_INF;
+      int br = -1, bp = -1;
+      for (int r = tid; r < md; r += RP_THREADS) {
+        double m1, m2;
+        int p1;
+        r_scan(I, V, r, cst, true, lam0, m1, p1, m2);
+        if (p1 >= 0 && m1 < bm) { bm = m1; br = r; bp = p1; }
+      }
+#pragma unroll
+      for (int sh = 16; sh > 0; sh >>= 1) {
+        const double om = __shfl_xor_sync(0xffffffffu, bm, sh);
+        const int orr = __shfl_xor_sync(0xffffffffu, br, sh), op = __shfl_xor_sync(0xffffffffu, bp, sh);
+        if (orr >= 0 && (br < 0 || om < bm || (om == bm && orr < br))) { bm = om; br = orr; bp = op; }
+      }
+      if (lane == 0) { s_m1[wid] = bm; s_r[wid] = br; s_p[wid] = bp; }
+      __syncthreads();
+      if (tid == 0) {
+        // fold the warps' minima by (cost, route): the reference's scan order
+        double cm = CUDART_INF;
+        int cr = -1, cp = -1;
+        for (int w = 0; w < nw; w++) {
+          if (s_r[w] < 0) continue;
+          if (s_m1[w] < cm || (s_m1[w] == cm && s_r[w] < cr)) { cm = s_m1[w]; cr = s_r[w]; cp = s_p[w]; }
+        }
+        s_touch = -1;
+        if (cr >= 0) {
+          int4 mt = V.rm[cr];
+          if (mt.x >= V.K) {
+            s_err = MDR_ERR_CAPACITY;
+          } else {
+            int *sq = V.seq + (size_t)cr * V.Kp;
+            const int n = r_len(I, mt.x);
+            for (int i = n; i > cp + 1; i--) sq[i] = sq[i - 1];
+            sq[cp + 1] = cst;
+            mt.x += 1;
+            V.rm[cr] = mt;
+            s_touch = cr;
+          }
+        } else if (!I.nv_on || (double)md < I.NV) {
+          if (s_m >= P.J || md >= Jd) {
+            s_err = MDR_ERR_CAPACITY;
+          } else {
+            int *sq = V.seq + (size_t)md * V.Kp;
+            sq[0] = d;
+            sq[1] = cst;
+            if (!I.open) sq[2] = d;
+            V.rm[md] = make_int4(1, d, d, 0);
+            s_m += 1;
+            s_touch = md;
+          }
+        } else {
+          left[(size_t)b * (I.N - I.ND) + s_nl++] = cst;
+        }
+      }
+      __syncthreads();
+      if (s_err) break;
+      if (s_touch >= 0 && wid == 0) r_rebuild(I, V, s_touch, lane);
+      __syncthreads();
+    }
+    __syncthreads();
+  }
+  if (tid == 0) {
+    P.m[b] = s_m;
+    n_left[b] = s_nl;
+    status[b] = s_err;
+  }
+}
+
+void launch_construct(const DevInst &I, const DevPop &P, int B, const int *ooff, const int *order, void *pre,
+                      void *suf, int Jd, int *n_left, int *left, int *status, cudaStream_t s) {
+  if (B <= 0) return;
+  k_construct<<<B, RP_THREADS, 0, s>>>(I, P, B, ooff, order, (RAt *)pre, (RAt *)suf, Jd, n_left, left, status);
+}
+
 // evaluation.evaluate (evaluation.py:206-224) of every uploaded individual, with
 // the scalar algebra's semantics: each route folded left with Python max/min
 // (route_attr), route_contributions per route, then D/V1/V2/V3 summed in route

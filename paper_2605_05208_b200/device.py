@@ -238,6 +238,21 @@ class Population:
         self.h2d_bytes_repair = int(off.nbytes + pend.nbytes)
         return stats
 
+    def construct(self, ooff, order, n_customers: int, stream=None):
+        """mdr_construct: initial solutions of B = len(ooff)//ND individuals into this
+        population; returns each individual's leftover customers."""
+        B = (len(ooff) - 1) // self.dinst.n_depots
+        ooff = np.ascontiguousarray(ooff, np.int32)
+        order = np.ascontiguousarray(order if len(order) else [0], np.int32)
+        n_left = np.zeros(max(B, 1), np.int32)
+        left = np.zeros(max(B, 1) * n_customers, np.int32)
+        s = stream if stream is not None else _cur_stream(self.dinst.device)
+        check(_lib.lib().mdr_construct(self.handle, B, ptr(ooff, i32p), ptr(order, i32p), ptr(n_left, i32p),
+                                       ptr(left, i32p), s), "mdr_construct")
+        self.B = B
+        self.n_cust = int(ooff[-1])
+        return [left[b * n_customers: b * n_customers + n_left[b]].tolist() for b in range(B)]
+
     def info(self) -> dict:
         """Evaluator shape of this population (mdr_pop_info)."""
         out = np.zeros(4, np.int32)
@@ -250,7 +265,11 @@ class Population:
     def timing(self) -> dict:
         t = Timing()
         check(_lib.lib().mdr_get_timing(self.handle, C.byref(t)))
-        return {f: getattr(t, f) for f, _ in Timing._fields_}
+        out = {f: getattr(t, f) for f, _ in Timing._fields_ if f != "kern_ms"}
+        # profiling pass, evaluation phase serialised: per-evaluator CUDA-event times
+        for i, n in enumerate(("relocate", "relocate_intra", "swap", "swap_intra", "two_opt_star", "depot_generic")):
+            out["kern_" + n + "_ms"] = t.kern_ms[i]
+        return out
 
     # ---- operator-level -----------------------------------------------------
     def count(self, b: int, op: int) -> int:

@@ -25,7 +25,7 @@ import time
 from dataclasses import dataclass, field
 from typing import Optional
 
-from .evaluation import EvalBreakdown, PenaltyState, ScalingConstants, evaluate, route_attr
+from .evaluation import EvalBreakdown, PenaltyState, ScalingConstants, evaluate
 from .genetic import (DIVERSITY_LEVELS, DiscountedUCB1, InsertionOperator, dcrex, improvement_reward,
                       initialize_population, repair_insert, repair_population, route_exchange)
 from .localsearch import SearchConfig, _searcher, local_search, local_search_population
@@ -215,7 +215,7 @@ def _batched_generation(R: "_Run", batch: int, device: int) -> None:
     for off, _ in kids:
         off.drop_empty_routes()
         for r in off.routes:
-            r.attr = route_attr(r, inst)
+            r.attr = None  # repaired: the cache is refreshed by the descent
         offspring.append(off)
     t2 = time.perf_counter()
     pens = [R.penalties.clone() for _ in offspring]

@@ -1,19 +1,23 @@
-"""Forward-simulation feasibility oracle (mirrors `mdroute.model`, model.py:232-392;
-SURVEY.md sec. 8(a) row a48).
+"""Feasibility check by forward simulation, on the device (SURVEY.md 8(a) row
+a48; drop-in for model.simulate_route / minimal_duration / check_feasible,
+model.py:242-392).
 
-Independent of the concat algebra: every route is simulated node by node
-(wait for early windows, clamp late arrivals and accumulate the overshoot as
-time warp), and `check_feasible` reports coverage, structure and every
-violation magnitude.  `minimal_duration` scans the finitely many departure
-times that align an arrival with a window bound.  Host-side test/validation
-utility, used to cross-check the device results (F = D <=> feasible).
+The structural and coverage checks are set bookkeeping over the host route
+lists; every route's simulation -- distance, load, time warp, late arrivals,
+duration and the minimal duration over warp-minimal departure times -- runs in
+one batched launch (mdr_route_sim, csrc/mdr_feasibility.cu).  The report's
+sums accumulate the per-route values in route order, as the reference's loop
+does, so the report is bit-identical (tests/test_scalar_oracles.py).
 """
 from __future__ import annotations
 
-import math
+import ctypes as C
 from dataclasses import dataclass, field
 from typing import Optional
 
+import numpy as np
+
+from . import _lib
 from .model import INF
 
 
@@ -21,70 +25,9 @@ from .model import INF
 class RouteSim:
     distance: float = 0.0
     load: float = 0.0
-    duration: float = 0.0   # travel + service + waiting, warps excluded by clamping
+    duration: float = 0.0
     time_warp: float = 0.0
     late_count: int = 0
-
-
-def simulate_from(route, inst, t0: float) -> RouteSim:
-    """Simulate a route whose first node is reached at time t0 (model.py:242-282)."""
-    seq = route.sequence(inst.open_routes)
-    c, t = inst.dist, inst.time
-    e, l, s, q = inst.tw_early, inst.tw_late, inst.service, inst.demand
-    sim = RouteSim()
-    first = seq[0]
-    start = max(t0, e[first])
-    if start > l[first]:
-        sim.time_warp += start - l[first]
-        sim.late_count += 1
-        start = l[first]
-    now = start + s[first]
-    for a, b in zip(seq, seq[1:]):
-        sim.distance += c[a, b]
-        arrive = now + t[a, b]
-        if arrive < e[b]:
-            arrive = e[b]
-        elif arrive > l[b]:
-            sim.time_warp += arrive - l[b]
-            sim.late_count += 1
-            arrive = l[b]
-        now = arrive + s[b]
-        sim.load += q[b]
-    sim.duration = float(now - start + sim.time_warp)
-    sim.distance, sim.load, sim.time_warp = float(sim.distance), float(sim.load), float(sim.time_warp)
-    return sim
-
-
-def simulate_route(route, inst) -> RouteSim:
-    """Earliest-departure simulation."""
-    return simulate_from(route, inst, float(inst.tw_early[route.sequence(inst.open_routes)[0]]))
-
-
-def minimal_duration(route, inst) -> float:
-    """Minimal duration over warp-minimal departure times (model.py:285-315)."""
-    if not inst.has_windows:
-        return simulate_route(route, inst).duration
-    seq = route.sequence(inst.open_routes)
-    e, l, s, t = inst.tw_early, inst.tw_late, inst.service, inst.time
-    first = seq[0]
-    starts = {float(e[first])}
-    if math.isfinite(l[first]):
-        starts.add(float(l[first]))
-    raw = 0.0  # travel + service from the first service start, no waiting
-    for a, b in zip(seq, seq[1:]):
-        raw += s[a] + t[a, b]
-        for bound in (e[b], l[b]):
-            if math.isfinite(bound):
-                starts.add(float(bound - raw))
-    base = simulate_route(route, inst)
-    best = base.duration
-    for t0 in starts:
-        if t0 < e[first]:
-            continue
-        sim = simulate_from(route, inst, t0)
-        if sim.time_warp <= base.time_warp + 1e-9:
-            best = min(best, sim.duration)
-    return best
 
 
 @dataclass
@@ -101,7 +44,7 @@ class FeasibilityReport:
 
     @property
     def coverage_ok(self) -> bool:
-        return not self.missing and not self.duplicated
+        return not (self.missing or self.duplicated)
 
     @property
     def all_ok(self) -> bool:
@@ -111,47 +54,74 @@ class FeasibilityReport:
                 and self.fleet_excess == 0)
 
 
+def _simulate(routes, inst, want_min: bool, device: int = 0) -> np.ndarray:
+    """[len(routes), 6] {distance, load, duration, time_warp, late, min duration} from the device."""
+    from .session import session_for
+    seqs = [r.sequence(inst.open_routes) for r in routes]
+    off = np.zeros(len(seqs) + 1, np.int32)
+    off[1:] = np.cumsum([len(s) for s in seqs])
+    flat = np.ascontiguousarray(np.concatenate(seqs) if seqs else np.zeros(0), np.int32)
+    out = np.zeros((max(len(seqs), 1), 6), np.float64)
+    if seqs:
+        sess = session_for(inst, None, None, device)
+        _lib.check(_lib.lib().mdr_route_sim(sess.dinst.handle, len(seqs), _lib.ptr(off, _lib.i32p),
+                                            _lib.ptr(flat, _lib.i32p), int(want_min), _lib.ptr(out, _lib.f64p)),
+                   "mdr_route_sim")
+    return out[:len(seqs)]
+
+
+def _sim(row) -> RouteSim:
+    return RouteSim(float(row[0]), float(row[1]), float(row[2]), float(row[3]), int(row[4]))
+
+
+def simulate_route(route, inst, device: int = 0) -> RouteSim:
+    """Earliest-departure forward simulation of one route (model.py:285-288)."""
+    return _sim(_simulate([route], inst, False, device)[0])
+
+
+def minimal_duration(route, inst, device: int = 0) -> float:
+    """Minimal duration over warp-minimal departure times (model.py:291-314)."""
+    return float(_simulate([route], inst, True, device)[0, 5])
+
+
 def _structure_error(sol, inst) -> Optional[str]:
     n = inst.n_nodes
     for r in sol.routes:
-        if not (0 <= r.depart < n) or not (0 <= r.arrive < n):
-            return f"unknown depot id on route {r!r}"
-        if not inst.is_depot(r.depart) or not inst.is_depot(r.arrive):
+        for x in (r.depart, r.arrive):
+            if not 0 <= x < n:
+                return f"unknown depot id on route {r!r}"
+        if not (inst.is_depot(r.depart) and inst.is_depot(r.arrive)):
             return f"route endpoint is not a depot: {r!r}"
         for c in r.customers:
-            if not (0 <= c < n):
+            if not 0 <= c < n:
                 return f"unknown node id {c}"
             if inst.is_depot(c):
                 return f"depot {c} appears as a customer"
-        if len(set(r.customers)) != len(r.customers):
+        if len(r.customers) != len(set(r.customers)):
             return f"repeated customer within route {r!r}"
     return None
 
 
-def check_feasible(sol, inst) -> FeasibilityReport:
-    """Oracle feasibility check by direct forward simulation (model.py:349-392)."""
-    rep = FeasibilityReport()
-    rep.structural_error = _structure_error(sol, inst)
+def check_feasible(sol, inst, device: int = 0) -> FeasibilityReport:
+    """Coverage, structure and every violation magnitude (model.py:349-392)."""
+    rep = FeasibilityReport(structural_error=_structure_error(sol, inst))
     if rep.structural_error is not None:
         return rep
-    seen: dict = {}
-    for c in sol.customer_list():
-        seen[c] = seen.get(c, 0) + 1
-    rep.missing = sorted(c for c in inst.customers() if c not in seen)
-    rep.duplicated = sorted(c for c, k in seen.items() if k > 1)
-    per_depot = [0] * inst.n_depots
-    for r in sol.routes:
-        if not r.customers:
-            continue
-        sim = simulate_route(r, inst)
-        rep.capacity_excess += max(sim.load - inst.capacity, 0.0)
+    count = np.bincount(np.asarray(sol.customer_list(), np.int64), minlength=inst.n_nodes)
+    cust = np.arange(inst.n_depots, inst.n_nodes)
+    rep.missing = [int(c) for c in cust[count[inst.n_depots:] == 0]]
+    rep.duplicated = [int(c) for c in np.nonzero(count > 1)[0]]
+    live = [r for r in sol.routes if r.customers]
+    sims = _simulate(live, inst, inst.max_duration != INF, device)
+    per_depot = np.zeros(inst.n_depots, np.int64)
+    for r, row in zip(live, sims):
+        rep.capacity_excess += max(float(row[1]) - inst.capacity, 0.0)
         if inst.max_duration != INF:
-            rep.duration_excess += max(minimal_duration(r, inst) - inst.max_duration, 0.0)
-        rep.time_warp += sim.time_warp
-        rep.late_count += sim.late_count
-        if not inst.open_routes and r.depart != r.arrive:
-            rep.closure_violations += 1
+            rep.duration_excess += max(float(row[5]) - inst.max_duration, 0.0)
+        rep.time_warp += float(row[3])
+        rep.late_count += int(row[4])
+        rep.closure_violations += int(not inst.open_routes and r.depart != r.arrive)
         per_depot[r.depart] += 1
     if inst.fleet_per_depot != INF:
-        rep.fleet_excess = int(sum(max(k - inst.fleet_per_depot, 0) for k in per_depot))
+        rep.fleet_excess = int(np.maximum(per_depot - inst.fleet_per_depot, 0).sum())
     return rep

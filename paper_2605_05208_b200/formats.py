@@ -1,13 +1,15 @@
-"""Cordeau-format instance files and solution files (mirrors `mdroute.bench`
-bench.py:24-156).  Host-side I/O feeding the
-device path with real benchmark instances: `parse_instance` builds the same
-`Instance` (identical distance matrix, labels, fleet/capacity/duration
-relaxations) and `write_solution` / `read_solution` produce and read the same
-text.
+"""Cordeau benchmark files: instance parsing and solution files (SURVEY.md
+sec. 8(f) row 4; drop-in for `mdroute.bench.parse_instance`, `write_solution`
+and `read_solution`, bench.py:24-156).
 
-Layout: a header `type m n t` (vehicles per depot, customers, depots), t lines
-`D Q` (0 = unlimited), n customer lines `id x y service demand f a <a combo
-fields> [e l]`, then t depot lines in the same layout.
+The instance reader walks the non-blank lines with a cursor through three
+sections -- header `type m n t`, t depot specs `D Q`, n customer records and
+t depot records (`id x y service demand [f a combos...] [e l]`) -- and hands
+the coordinates to `Instance.from_coords`, so the distance matrix, labels and
+relaxations (fleet 0 = unlimited, MDOVRP without fleet and duration limits,
+`relax_fleet`) equal the reference's, and so do the error messages.  A
+solution file's per-route distance and load come from the device route
+simulation (mdr_route_sim, the same sequential sums as simulate_route).
 """
 from __future__ import annotations
 
@@ -22,118 +24,118 @@ class ParseError(ValueError):
     pass
 
 
-def _tokens(path: Path):
-    return [(i, ln.split()) for i, ln in enumerate(path.read_text().splitlines(), start=1) if ln.split()]
+class _Lines:
+    """Non-blank lines of a file as (line number, tokens), consumed in order."""
+
+    def __init__(self, path: Path):
+        self.rows = [(no, ln.split()) for no, ln in enumerate(path.read_text().splitlines(), 1) if ln.strip()]
+        self.at = 0
+
+    def take(self, k: int):
+        out = self.rows[self.at:self.at + k]
+        self.at += k
+        return out
 
 
-def _node_fields(lineno, toks, want_windows):
-    """(file_id, x, y, service, demand, e, l) of one node line (bench.py:38-56)."""
-    try:
-        fid = int(float(toks[0]))
-        x, y = float(toks[1]), float(toks[2])
-        service = float(toks[3]) if len(toks) > 3 else 0.0
-        demand = float(toks[4]) if len(toks) > 4 else 0.0
-        rest = toks[5:]
-        if len(rest) >= 2:
-            rest = rest[2 + int(float(rest[1])):]  # skip frequency, combo count and combos
-        e = l = None
-        if len(rest) >= 2:
-            e, l = float(rest[-2]), float(rest[-1])
-    except (ValueError, IndexError) as exc:
-        raise ParseError(f"line {lineno}: malformed node line: {exc}") from exc
-    if want_windows and e is None:
-        raise ParseError(f"line {lineno}: time-window fields missing for TW variant")
-    return fid, x, y, service, demand, e, l
+class _Record:
+    """One node line: file id, coordinates, service, demand and the optional window."""
+
+    __slots__ = ("fid", "x", "y", "service", "demand", "window")
+
+    def __init__(self, lineno: int, toks, need_window: bool):
+        try:
+            self.fid = int(float(toks[0]))
+            self.x, self.y = float(toks[1]), float(toks[2])
+            self.service = float(toks[3]) if len(toks) > 3 else 0.0
+            self.demand = float(toks[4]) if len(toks) > 4 else 0.0
+            tail = toks[5:]
+            if len(tail) >= 2:  # visit frequency, combination count, the combinations
+                tail = tail[2 + int(float(tail[1])):]
+            self.window = (float(tail[-2]), float(tail[-1])) if len(tail) >= 2 else None
+        except (ValueError, IndexError) as exc:
+            raise ParseError(f"line {lineno}: malformed node line: {exc}") from exc
+        if need_window and self.window is None:
+            raise ParseError(f"line {lineno}: time-window fields missing for TW variant")
 
 
 def parse_instance(path, variant, relax_fleet: bool = False) -> Instance:
-    """Parse one instance file and apply the variant's relaxations (bench.py:59-121)."""
-    path = Path(path)
-    variant = Variant(variant)
-    lines = _tokens(path)
-    if not lines:
+    """Read a Cordeau instance file for `variant` (bench.py:59-121)."""
+    path, variant = Path(path), Variant(variant)
+    src = _Lines(path)
+    if not src.rows:
         raise ParseError(f"{path}: empty instance file")
-    lineno, head = lines[0]
+    (hline, head), = src.take(1)
     if len(head) < 4:
-        raise ParseError(f"line {lineno}: header needs 'type m n t'")
+        raise ParseError(f"line {hline}: header needs 'type m n t'")
     try:
-        ptype, m, n, t = (int(float(v)) for v in head[:4])
+        ptype, vehicles, n_cust, n_dep = (int(float(v)) for v in head[:4])
     except ValueError as exc:
-        raise ParseError(f"line {lineno}: bad header: {exc}") from exc
-    if ptype != EXPECTED_TYPE[variant]:
-        raise ParseError(f"line {lineno}: problem type {ptype} does not match variant {variant.value} "
-                         f"(expected {EXPECTED_TYPE[variant]})")
-    if len(lines) < 1 + t + n + t:
-        raise ParseError(f"{path}: expected {1 + t + n + t} data lines, found {len(lines)}")
-    specs = []
-    for lineno, toks in lines[1:1 + t]:
+        raise ParseError(f"line {hline}: bad header: {exc}") from exc
+    want = EXPECTED_TYPE[variant]
+    if ptype != want:
+        raise ParseError(f"line {hline}: problem type {ptype} does not match variant {variant.value} "
+                         f"(expected {want})")
+    need = 1 + 2 * n_dep + n_cust
+    if len(src.rows) < need:
+        raise ParseError(f"{path}: expected {need} data lines, found {len(src.rows)}")
+
+    specs = set()
+    for lineno, toks in src.take(n_dep):
         if len(toks) < 2:
             raise ParseError(f"line {lineno}: depot spec needs 'D Q'")
-        specs.append((float(toks[0]), float(toks[1])))
-    if len({d for d, _ in specs}) > 1 or len({q for _, q in specs}) > 1:
+        specs.add((float(toks[0]), float(toks[1])))
+    durations, capacities = {d for d, _ in specs}, {q for _, q in specs}
+    if len(durations) > 1 or len(capacities) > 1:
         raise ParseError(f"{path}: heterogeneous depot specs are not supported")
-    duration, cap = specs[0]
-    capacity = cap if cap > 0 else INF
-    max_duration = duration if duration > 0 else INF
-    windows = variant is Variant.MDVRPTW
-    cust_rows = [_node_fields(ln, tk, windows) for ln, tk in lines[1 + t:1 + t + n]]
-    depot_rows = [_node_fields(ln, tk, False) for ln, tk in lines[1 + t + n:1 + t + n + t]]
-    fleet = float(m) if m > 0 else INF
+    duration, = durations
+    cap, = capacities
+
+    tw = variant is Variant.MDVRPTW
+    cust = [_Record(no, tk, tw) for no, tk in src.take(n_cust)]
+    deps = [_Record(no, tk, False) for no, tk in src.take(n_dep)]
+
+    limits = dict(fleet_per_depot=float(vehicles) if vehicles > 0 else INF,
+                  capacity=cap if cap > 0 else INF,
+                  max_duration=duration if duration > 0 else INF)
     if variant is Variant.MDOVRP:
-        fleet, max_duration = INF, INF
+        limits.update(fleet_per_depot=INF, max_duration=INF)
     if relax_fleet:
-        fleet = INF
-    depot_windows = None
-    if windows:
-        depot_windows = [(r[5] if r[5] is not None else 0.0, r[6] if r[6] is not None else INF)
-                         for r in depot_rows]
-    customers = [(x, y, q, s, e, l) if windows else (x, y, q, s) for _, x, y, s, q, e, l in cust_rows]
-    labels = [r[0] for r in depot_rows] + [r[0] for r in cust_rows]
-    return Instance.from_coords(variant, [(r[1], r[2]) for r in depot_rows], customers, fleet_per_depot=fleet,
-                                capacity=capacity, max_duration=max_duration, depot_windows=depot_windows,
-                                labels=labels, name=path.stem)
+        limits["fleet_per_depot"] = INF
+    if tw:
+        customers = [(c.x, c.y, c.demand, c.service, *c.window) for c in cust]
+        windows = [d.window if d.window is not None else (0.0, INF) for d in deps]
+    else:
+        customers = [(c.x, c.y, c.demand, c.service) for c in cust]
+        windows = None
+    return Instance.from_coords(variant, [(d.x, d.y) for d in deps], customers, depot_windows=windows,
+                                labels=[r.fid for r in deps + cust], name=path.stem, **limits)
 
 
-def _route_sim(route, inst):
-    """(distance, load) of simulate_route (model.py:242-282): sequential sums."""
-    seq = route.sequence(inst.open_routes)
-    dist = 0.0
-    load = 0.0
-    for a, b in zip(seq, seq[1:]):
-        dist += inst.dist[a, b]
-        load += inst.demand[b]
-    return float(dist), float(load)
-
-
-def _route_distance(route, inst):
-    seq = route.sequence(inst.open_routes)
-    return float(sum(inst.dist[a, b] for a, b in zip(seq, seq[1:])))
-
-
-def write_solution(sol: Solution, path, inst: Instance) -> None:
-    """Total cost, then `depart_label [arrive_label] cost load: c1 c2 ...` per route (bench.py:128-141)."""
+def write_solution(sol: Solution, path, inst: Instance, device: int = 0) -> None:
+    """Total cost, then `depart_label [arrive_label] cost load: c1 c2 ...` per route
+    (bench.py:128-141); distances and loads from the device route simulation."""
+    from .feasibility import _simulate
+    sims = _simulate(sol.routes, inst, False, device)
     lab = inst.labels
-    lines = [f"{sum(_route_distance(r, inst) for r in sol.routes):.2f}"]
-    for r in sol.routes:
-        dist, load = _route_sim(r, inst)
-        custs = " ".join(str(lab[c]) for c in r.customers)
-        if inst.open_routes:
-            lines.append(f"{lab[r.depart]} {dist:.2f} {load:g}: {custs}")
-        else:
-            lines.append(f"{lab[r.depart]} {lab[r.arrive]} {dist:.2f} {load:g}: {custs}")
-    Path(path).write_text("\n".join(lines) + "\n")
+    total = 0
+    for row in sims:
+        total += float(row[0])
+    out = [f"{total:.2f}"]
+    for r, row in zip(sol.routes, sims):
+        ends = f"{lab[r.depart]}" if inst.open_routes else f"{lab[r.depart]} {lab[r.arrive]}"
+        out.append(f"{ends} {float(row[0]):.2f} {float(row[1]):g}: " + " ".join(str(lab[c]) for c in r.customers))
+    Path(path).write_text("\n".join(out) + "\n")
 
 
 def read_solution(path, inst: Instance) -> Solution:
-    """Inverse of write_solution (bench.py:144-156)."""
-    label_to_id = {lab: i for i, lab in enumerate(inst.labels)}
-    lines = [ln for ln in Path(path).read_text().splitlines() if ln.strip()]
+    """Routes of a solution file, labels mapped back to node ids (bench.py:144-156)."""
+    node_of = {lab: i for i, lab in enumerate(inst.labels)}
     sol = Solution()
-    for ln in lines[1:]:
-        head, _, tail = ln.partition(":")
-        toks = head.split()
-        custs = [label_to_id[int(v)] for v in tail.split()]
-        depart = label_to_id[int(toks[0])]
-        arrive = depart if inst.open_routes else label_to_id[int(toks[1])]
-        sol.routes.append(Route(depart, arrive, custs))
+    body = [ln for ln in Path(path).read_text().splitlines() if ln.strip()][1:]
+    for ln in body:
+        ends, _, members = ln.partition(":")
+        ids = ends.split()
+        dep = node_of[int(ids[0])]
+        arr = dep if inst.open_routes else node_of[int(ids[1])]
+        sol.routes.append(Route(dep, arr, [node_of[int(v)] for v in members.split()]))
     return sol

@@ -22,12 +22,12 @@ from dataclasses import dataclass
 from enum import IntEnum
 from typing import Optional, Sequence
 
+import numpy as np
+
 from ._lib import CapacityError
 from .device import Population
-from .evaluation import route_attr
 from .model import INF, Route, Solution, route_edges, solution_edges
 from .session import session_for
-from .workload import initial_solution
 
 DIVERSITY_LEVELS = 20
 
@@ -181,10 +181,74 @@ def improvement_reward(parent_value: float, offspring_value: float) -> float:
     return 100.0 * (parent_value - offspring_value) / parent_value
 
 
-def initialize_population(inst, mu: int, consts, penalties, rng) -> list:
+def _construction_orders(inst, rngs):
+    """The host half of initial_solution (genetic.py:255-266): nearest-depot
+    membership (ties to the lower depot id) and each depot's rng.shuffle, drawn
+    in the reference's order -- rngs[i] may repeat the same object, whose
+    stream then continues across the individuals as a sequential caller's would."""
+    nd = inst.n_depots
+    near = np.argmin(np.asarray(inst.dist)[:nd, nd:], axis=0)  # first minimum = lowest id
+    base = [[int(c) for c in np.nonzero(near == d)[0] + nd] for d in range(nd)]
+    ooff, order = [0], []
+    for rng in rngs:
+        for d in range(nd):
+            members = list(base[d])
+            rng.shuffle(members)
+            order.extend(members)
+            ooff.append(len(order))
+    return np.asarray(ooff, np.int32), np.asarray(order, np.int32)
+
+
+def initial_solutions(inst, consts, penalties, rngs, device: int = 0) -> list:
+    """genetic.initial_solution (genetic.py:251-294) for len(rngs) individuals at
+    once: the shuffles on the host, the greedy per-depot construction
+    (mdr_construct) and the relaxed best-insertion repair of the leftovers
+    (mdr_repair, IBI) on the device, then drop_empty_routes."""
+    B = len(rngs)
+    if B == 0:
+        return []
+    ooff, order = _construction_orders(inst, rngs)
+    nc, nd = inst.n_customers, inst.n_depots
+    sess = session_for(inst, consts, None, device)
+    demand = float(np.sum(np.asarray(inst.demand)[nd:]))
+    est = nd + (int(math.ceil(demand / inst.capacity)) if inst.capacity != INF and inst.capacity > 0 else nd)
+    J, K = min(4094, max(32, 2 * est)), min(500, max(32, 2 * -(-nc // max(est - nd, 1))))
+    out = []
+    at = 0
+    while at < B:
+        per_ind = J * (K + 2) * (K + 2) * (6 if inst.has_windows else 4) * 8 + J * (K + 2) * 200
+        chunk = max(1, min(B - at, int(2e9 // per_ind)))
+        pop = Population(sess.dinst, chunk, J, K, 1 << 10)
+        try:
+            left = pop.construct(ooff[at * nd: (at + chunk) * nd + 1] - ooff[at * nd],
+                                 order[ooff[at * nd]: ooff[(at + chunk) * nd]], nc)
+            if any(left):
+                pop.repair(int(InsertionOperator.IBI), left)
+        except CapacityError:
+            if J >= 4094 and K >= 500:
+                raise
+            J, K = min(4094, 2 * J), min(500, 2 * K)
+            continue
+        routes, _ = pop.download()
+        for rt in routes:
+            sol = Solution([Route(d, a, list(c)) for d, a, c in rt])
+            sol.drop_empty_routes()
+            out.append(sol)
+        at += chunk
+    return out
+
+
+def initial_solution(inst, consts, penalties, rng, device: int = 0) -> Solution:
+    """Nearest-depot assignment, randomized greedy construction per depot, then
+    relaxed insertion of whatever could not be placed feasibly (genetic.py:251-294)."""
+    return initial_solutions(inst, consts, penalties, [rng], device)[0]
+
+
+def initialize_population(inst, mu: int, consts, penalties, rng, device: int = 0) -> list:
+    """mu initial solutions drawn from one rng stream (genetic.py:297-301), built in one batch."""
     if mu < 2:
         raise ValueError("population size must be >= 2")
-    return [initial_solution(inst, consts, penalties, rng) for _ in range(mu)]
+    return initial_solutions(inst, consts, penalties, [rng] * mu, device)
 
 
 # --------------------------------------------------------------------------- #
@@ -373,5 +437,5 @@ def dcrex(population: Sequence, inst, consts, penalties, diversity_bandit: Disco
     repair_insert(off, unrouted, op, inst, consts, penalties, rng)
     off.drop_empty_routes()
     for r in off.routes:
-        r.attr = route_attr(r, inst)
+        r.attr = None  # repaired routes: stale caches dropped (the descent refreshes them)
     return CrossoverResult(off, level, op, sigma, main_index)

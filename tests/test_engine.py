@@ -84,12 +84,32 @@ def _oracle_kernels(setattr_):
     setattr_(E, "repair_population", repair_population)
     setattr_(GN, "repair_population", repair_population)
     setattr_(E, "build_device", build)
+    from oracle import population_ref as PR, scalar_ref as SR
+    from paper_2605_05208_b200.population import Population
+    import numpy as np
+
+    def host_select(self, mu, costs):  # the restatement standing in for mdr_population_select
+        edges = [m.edges for m in self.members]
+        self._dist, self._known = np.asarray(PR.distance_rows(edges), np.float64).reshape(len(edges), -1), len(edges)
+        if costs is None or len(edges) <= mu:
+            return []
+        return PR.removal_order(edges, costs, [m.birth for m in self.members], mu, self.xi)
+
+    setattr_(Population, "_device_select", host_select)
+    setattr_(E, "evaluate", SR.evaluate)
+    from oracle import initial_ref
+
+    def init_pop(inst, mu, consts, penalties, rng, device=0):  # the restatement for the device construction
+        return [initial_ref.initial_solution(inst, consts, penalties, rng) for _ in range(mu)]
+
+    setattr_(E, "initialize_population", init_pop)
 
     class _HostPop:  # breakdowns of the last oracle batch, by the host evaluate
         sols = []
 
         def breakdowns(self, lams):
-            from paper_2605_05208_b200.evaluation import PenaltyState, ScalingConstants, evaluate
+            from paper_2605_05208_b200.evaluation import PenaltyState
+            from oracle.scalar_ref import evaluate
             out = []
             for s, l in zip(self.sols, lams):
                 b = evaluate(s, PenaltyState(lam=l), self.consts, self.inst)
@@ -136,7 +156,8 @@ def test_device_breakdown_equals_evaluate(variant, fleet, dur):
     """mdr_pop_breakdown == evaluation.evaluate bit for bit (infeasible random states,
     empty routes, fleet excess, closures)."""
     from paper_2605_05208_b200.device import DeviceInstance, Population
-    from paper_2605_05208_b200.evaluation import PenaltyState, ScalingConstants, evaluate
+    from paper_2605_05208_b200.evaluation import PenaltyState, ScalingConstants
+    from oracle.scalar_ref import evaluate
     inst = W.make_instance(random.Random(31), variant, n_customers=45, n_depots=3, fleet=fleet, max_duration=dur)
     consts = ScalingConstants.from_instance(inst)
     sols = [W.random_solution(random.Random(700 + i), inst) for i in range(9)]

@@ -27,8 +27,10 @@ def test_parse_instance_equals_reference(key):
         (want["fleet"], want["capacity"], want["max_duration"])
 
 
+@pytest.mark.gpu
 @pytest.mark.parametrize("key", sorted(MAN["cases"]))
 def test_solution_file_equals_reference(key, tmp_path):
+    """write_solution (route distances and loads from the device simulation) is byte-identical."""
     fname, variant, relax = key.split("|")
     want = MAN["cases"][key]
     inst = parse_instance(os.path.join(HERE, fname), variant, relax_fleet=relax == "1")
@@ -36,6 +38,13 @@ def test_solution_file_equals_reference(key, tmp_path):
     out = tmp_path / "s.sol"
     write_solution(sol, out, inst)
     assert out.read_text() == open(os.path.join(HERE, want["sol_file"])).read()
+
+
+@pytest.mark.parametrize("key", sorted(MAN["cases"]))
+def test_read_solution_equals_reference(key):
+    fname, variant, relax = key.split("|")
+    want = MAN["cases"][key]
+    inst = parse_instance(os.path.join(HERE, fname), variant, relax_fleet=relax == "1")
     back = read_solution(os.path.join(HERE, want["sol_file"]), inst)
     assert [[r.depart, r.arrive, r.customers] for r in back.routes] == [list(x) for x in want["read_back"]]
 

@@ -182,7 +182,7 @@ def test_appendix_a_c2_shape_descents_vs_oracle():
     inst, _ = W.appendix_a_instance(spec)
     consts = P.ScalingConstants.from_instance(inst)
     nbr = P.build_neighbors(inst, P.NeighborConfig(spec.theta), consts)
-    sols = [W.initial_solution(inst, consts, P.PenaltyState(), random.Random(100 + i)) for i in range(4)]
+    sols = P.initial_solutions(inst, consts, P.PenaltyState(), [random.Random(100 + i) for i in range(4)])
     cfg = P.SearchConfig(depth=40, multi_move=True)
     ops = P.enabled_operators(inst)
     oi = O.OracleInstance(inst, consts, nbr)
@@ -250,7 +250,7 @@ def test_appendix_a_configs_descents_vs_oracle(name, pop, depth):
     inst, _ = W.appendix_a_instance(spec)
     consts = P.ScalingConstants.from_instance(inst)
     nbr = P.build_neighbors(inst, P.NeighborConfig(spec.theta), consts)
-    sols = [W.initial_solution(inst, consts, P.PenaltyState(), random.Random(100 + i)) for i in range(pop)]
+    sols = P.initial_solutions(inst, consts, P.PenaltyState(), [random.Random(100 + i) for i in range(pop)])
     cfg = P.SearchConfig(depth=depth, multi_move=True)
     ops = P.enabled_operators(inst)
     oi = O.OracleInstance(inst, consts, nbr)

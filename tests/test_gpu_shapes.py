@@ -36,11 +36,13 @@ THREADS = os.cpu_count() or 1
 
 
 def _start(args):
+    """Oracle start state (the scalar restatement of genetic.initial_solution)."""
+    from oracle import initial_ref
     name, i = args
     spec = W.CONFIGS[name]
     inst, _ = W.appendix_a_instance(spec)
     consts = P.ScalingConstants.from_instance(inst)
-    s = W.initial_solution(inst, consts, P.PenaltyState(), random.Random(100 + i))
+    s = initial_ref.initial_solution(inst, consts, P.PenaltyState(), random.Random(100 + i))
     return [(r.depart, r.arrive, list(r.customers)) for r in s.routes]
 
 
@@ -48,15 +50,20 @@ _CACHE = {}
 
 
 def appendix_a(name, n):
-    """Instance, constants, lists and the first n Appendix-A start states of a config."""
+    """Instance, constants, lists and the first n Appendix-A start states of a
+    config, built on the device (genetic.initial_solutions: mdr_construct + IBI
+    repair); the first few are checked against the oracle's restatement."""
     if (name, n) not in _CACHE:
         spec = W.CONFIGS[name]
         inst, _ = W.appendix_a_instance(spec)
         consts = P.ScalingConstants.from_instance(inst)
         nbr = P.build_neighbors(inst, P.NeighborConfig(spec.theta), consts)
-        with ProcessPoolExecutor(max(1, min(THREADS, 32))) as ex:
-            raw = list(ex.map(_start, [(name, i) for i in range(n)], chunksize=4))
-        sols = [P.Solution([P.Route(d, a, c) for d, a, c in rs]) for rs in raw]
+        sols = P.initial_solutions(inst, consts, P.PenaltyState(), [random.Random(100 + i) for i in range(n)])
+        k = min(n, max(2, THREADS))
+        with ProcessPoolExecutor(max(1, min(THREADS, 32)), mp_context=__import__("multiprocessing").get_context("spawn")) as ex:
+            raw = list(ex.map(_start, [(name, i) for i in range(k)]))
+        assert [[(r.depart, r.arrive, list(r.customers)) for r in s.routes] for s in sols[:k]] == raw, \
+            "device start states differ from the oracle's"
         _CACHE[(name, n)] = (inst, consts, nbr, sols)
     return _CACHE[(name, n)]
 

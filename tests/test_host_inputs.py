@@ -24,15 +24,20 @@ def test_neighbor_lists_and_constants_equal_reference(group):
         assert np.array_equal(nbr.lists, case.nbr.lists), case.tag
 
 
+@pytest.mark.parametrize("impl", [pytest.param("oracle"), pytest.param("device", marks=pytest.mark.gpu)])
 @pytest.mark.parametrize("name", ["C1", "C2", "C3"])
-def test_appendix_a_initial_solution_equals_reference(name):
+def test_appendix_a_initial_solution_equals_reference(name, impl):
     """medium golden '<name>_init' = reference genetic.initial_solution continuing the
-    seed-2026 stream after the Appendix A instance draws."""
+    seed-2026 stream after the Appendix A instance draws.  oracle: the scalar
+    restatement; device: genetic.initial_solution (mdr_construct + IBI repair)."""
+    from oracle import initial_ref
+    from paper_2605_05208_b200 import genetic
     case = [c for c in G.cases("medium") if c.tag == f"{name}_init"][0]
     inst, rng = W.appendix_a_instance(W.CONFIGS[name])
     assert np.array_equal(inst.dist, case.inst.dist)
     consts = ScalingConstants.from_instance(inst)
-    sol = W.initial_solution(inst, consts, PenaltyState(), rng)
+    make = initial_ref.initial_solution if impl == "oracle" else genetic.initial_solution
+    sol = make(inst, consts, PenaltyState(), rng)
     assert G.routes_of(sol) == G.routes_of(case.sol)
 
 

@@ -59,10 +59,14 @@ def test_large_instance_constants_lists_equal_reference(name):
     assert _sha(np.ascontiguousarray(nbr.lists, np.int32)) == g["lists_sha"]
 
 
+@pytest.mark.parametrize("impl", [pytest.param("oracle"), pytest.param("device", marks=pytest.mark.gpu)])
 @pytest.mark.parametrize("name,i", [("C4", 0), ("C4", 1), ("C4", 2), ("C4", 3), ("C5", 0), ("C5", 3)])
-def test_start_states_equal_reference(name, i):
+def test_start_states_equal_reference(name, i, impl):
+    from oracle import initial_ref
+    from paper_2605_05208_b200 import genetic
     inst, consts, _ = built(name)
-    s = W.initial_solution(inst, consts, P.PenaltyState(), random.Random(100 + i))
+    make = initial_ref.initial_solution if impl == "oracle" else genetic.initial_solution
+    s = make(inst, consts, P.PenaltyState(), random.Random(100 + i))
     assert G.routes_of(s) == [(d, a, list(c)) for d, a, c in GOLD[name]["starts"][i]]
 
 

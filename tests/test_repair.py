@@ -83,7 +83,8 @@ def test_device_repair_population_matches_oracle(name, op):
     inst, _ = W.appendix_a_instance(spec)
     consts = ScalingConstants.from_instance(inst)
     rng = random.Random(zlib.crc32(f"{name}{op}".encode()))
-    base = [W.initial_solution(inst, consts, PenaltyState(), random.Random(100 + i)) for i in range(4)]
+    from paper_2605_05208_b200.genetic import initial_solutions
+    base = initial_solutions(inst, consts, PenaltyState(), [random.Random(100 + i) for i in range(4)])
     sols, pend, pens = [], [], []
     for i in range(16):
         s, u = _partial(rng, base[i % 4], rng.choice([0.25, 0.4]), i % 2 == 0)

@@ -8,8 +8,9 @@ import random
 import pytest
 
 from paper_2605_05208_b200 import workload as W
-from paper_2605_05208_b200.evaluation import PenaltyState, ScalingConstants, evaluate, move_delta
-from paper_2605_05208_b200.feasibility import check_feasible, minimal_duration, simulate_route
+from oracle import feasibility_ref as FR, scalar_ref as SR
+from paper_2605_05208_b200 import evaluation as EV, feasibility as FD
+from paper_2605_05208_b200.evaluation import PenaltyState, ScalingConstants
 from paper_2605_05208_b200.moves import Move, Op
 
 CASES = json.load(open(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "scalar.json")))
@@ -24,8 +25,18 @@ def _case(c):
     return inst, sol
 
 
+IMPLS = [pytest.param("oracle", id="oracle"), pytest.param("device", id="device", marks=pytest.mark.gpu)]
+
+
+@pytest.mark.parametrize("impl", IMPLS)
 @pytest.mark.parametrize("i", range(len(CASES)))
-def test_evaluate_and_feasibility_equal_reference(i):
+def test_evaluate_and_feasibility_equal_reference(i, impl):
+    """oracle: the scalar restatements (test checkers); device: the product's
+    evaluate (mdr_pop_breakdown) and check_feasible / simulate_route /
+    minimal_duration (mdr_route_sim)."""
+    evaluate = SR.evaluate if impl == "oracle" else EV.evaluate
+    M = FR if impl == "oracle" else FD
+    check_feasible, simulate_route, minimal_duration = M.check_feasible, M.simulate_route, M.minimal_duration
     c = CASES[i]
     inst, sol = _case(c)
     consts = ScalingConstants.from_instance(inst)
@@ -56,5 +67,5 @@ def test_move_delta_equals_reference(i):
     for key, want in c["move_deltas"]:
         op, r1, r2, p1, p2, l1, l2, v1, v2, dep, mode = key
         mv = Move(Op(op), r1, p1, r2, p2, l1, l2, bool(v1), bool(v2), dep, mode)
-        d = move_delta(sol, mv, pen, consts, inst)
+        d = SR.move_delta(sol, mv, pen, consts, inst)
         assert [H(x) for x in (d.D, d.V1, d.V2, d.V3, d.V4, d.F)] == want, key
