@@ -89,6 +89,7 @@ typedef struct mdr_ls_cfg {
   int32_t rounds_per_sync;         /* device rounds per host poll (0 = default) */
   int32_t use_graph;               /* reserved (graphs are used unless MDR_NO_GRAPH is set) */
   int32_t snapshot_best;           /* keep the best feasible state for mdr_pop_download_best */
+  int32_t trace;                   /* record every accepted step (mdr_pop_trace) */
 } mdr_ls_cfg;
 
 typedef struct mdr_ls_stats {
@@ -160,6 +161,16 @@ int mdr_totals(mdr_pop *pop, int32_t b, double out[5]);
 /* B_active = individuals 0..B-1 of the last upload. stats: [B] */
 int mdr_local_search(mdr_pop *pop, const mdr_ls_cfg *cfg, mdr_ls_stats *stats, void *stream);
 int mdr_get_timing(mdr_pop *pop, mdr_timing *out);
+/* The accepted steps of individual b's last traced descent (cfg.trace): per step
+ * {op << 56 | feasible << 55 | n_moves, bits of the post-step distance D, n_moves packed move
+ * keys (Move.key order) in selection order}.  *n = words recorded; MDR_ERR_CAPACITY if the
+ * trace overflowed or out is shorter than *n.  Lets the host replay every post-step state
+ * for on_feasible (localsearch.py:133-134). */
+int mdr_pop_trace(mdr_pop *pop, int32_t b, uint64_t *out, int64_t cap, int64_t *n);
+/* route_attr (evaluation.py:97-106) of every route of individuals b0 .. b0+nb-1 (the Route.attr
+ * caches apply_moves refreshes, localsearch.py:73-80): out[((b-b0)*J_cap + r)*6 ..] =
+ * {dist, load, T, E, L, TW} of the left fold with Python max/min semantics. */
+int mdr_pop_route_attrs(mdr_pop *pop, int32_t b0, int32_t nb, double *out, void *stream);
 
 /* n_passes results of CPython random.Random.shuffle(list(items)) continuing the
  * MT19937 state of rng.getstate()[1] (624 words + index, advanced in place);

@@ -50,7 +50,8 @@ class LsCfg(C.Structure):
     _fields_ = [("depth", C.c_int32), ("multi_move", C.c_int32), ("kappa", C.c_double),
                 ("lam_min", C.c_double), ("lam_max", C.c_double), ("max_passes", C.c_int32),
                 ("n_ops", C.c_int32), ("perms", u8p), ("deadline_s", C.c_double),
-                ("rounds_per_sync", C.c_int32), ("use_graph", C.c_int32), ("snapshot_best", C.c_int32)]
+                ("rounds_per_sync", C.c_int32), ("use_graph", C.c_int32), ("snapshot_best", C.c_int32),
+                ("trace", C.c_int32)]
 
 
 class LsStats(C.Structure):
@@ -120,6 +121,8 @@ def lib():
                                          C.POINTER(C.c_float)]
         L.mdr_population_select.argtypes = [C.c_int32, C.c_int32, C.c_int32, i64p, i64p, f64p, C.c_int32,
                                             C.c_double, f64p, i64p, i32p]
+        L.mdr_pop_trace.argtypes = [vp, C.c_int32, C.POINTER(C.c_uint64), C.c_int64, C.POINTER(C.c_int64)]
+        L.mdr_pop_route_attrs.argtypes = [vp, C.c_int32, C.c_int32, f64p, vp]
         L.mdr_construct.argtypes = [vp, C.c_int32, i32p, i32p, i32p, i32p, vp]
         L.mdr_route_sim.argtypes = [vp, C.c_int32, i32p, i32p, C.c_int32, f64p]
         _L = L
@@ -154,5 +157,5 @@ EXPORTED = ("mdr_last_error", "mdr_device_count", "mdr_build_info", "mdr_instanc
             "mdr_leader_followers", "mdr_totals", "mdr_local_search", "mdr_get_timing",
             "mdr_set_profiling", "mdr_shuffle_stream", "mdr_probe_l2_gbs",
             "mdr_probe_fp64_gops", "mdr_neighbor_build", "mdr_repair", "mdr_pop_download_range",
-            "mdr_population_select", "mdr_route_sim", "mdr_construct",
+            "mdr_population_select", "mdr_route_sim", "mdr_construct", "mdr_pop_trace", "mdr_pop_route_attrs",
             "mdr_pop_breakdown", "mdr_pop_info")

@@ -72,6 +72,10 @@ struct mdr_pop {
   double *rp_fold = nullptr;
   int *rp_foldi = nullptr;
   double *bd_rt = nullptr, *bd_io = nullptr;  // mdr_pop_breakdown scratch
+  unsigned long long *tr_buf = nullptr;        // accepted-step trace (cfg.trace)
+  long long *tr_cnt = nullptr;
+  size_t tr_cap[2] = {0, 0};
+  long long tr_per = 0;                        // words per individual of the last traced run
   size_t rp_cap[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
 };
 
@@ -334,6 +338,8 @@ void mdr_pop_destroy(mdr_pop *p) {
     if (p->side[q]) cudaStreamDestroy(p->side[q]);
   for (int q = 0; q < 4; q++)
     if (p->fev[q]) cudaEventDestroy(p->fev[q]);
+  if (p->tr_buf) cudaFree(p->tr_buf);
+  if (p->tr_cnt) cudaFree(p->tr_cnt);
   for (void *q : {(void *)p->rp_pre, (void *)p->rp_suf, (void *)p->rp_c1, (void *)p->rp_c2, (void *)p->rp_p1, (void *)p->rp_pend,
                   (void *)p->rp_status, (void *)p->rp_stats, (void *)p->rp_fold, (void *)p->rp_foldi,
                   (void *)p->bd_rt, (void *)p->bd_io})
@@ -1028,6 +1034,21 @@ int mdr_local_search(mdr_pop *p, const mdr_ls_cfg *cfg, mdr_ls_stats *stats, voi
   L.lam_max = cfg->lam_max;
   L.B = B;
   L.snapshot = cfg->snapshot_best ? 1 : 0;
+  L.trace = cfg->trace ? 1 : 0;
+  P.trace = nullptr;
+  P.trcount = nullptr;
+  P.tcap = 0;
+  if (L.trace && B) {  // a step selects at most one move per route: depth * (2 + J) words bound it
+    const long long per = (long long)cfg->depth * (2 + P.J);
+    int rc;
+    if ((rc = regrow(&p->tr_buf, p->tr_cap[0], (size_t)B * per)) || (rc = regrow(&p->tr_cnt, p->tr_cap[1], (size_t)B)))
+      return rc;
+    CK(cudaMemsetAsync(p->tr_cnt, 0, sizeof(long long) * B, s));
+    P.trace = p->tr_buf;
+    P.trcount = p->tr_cnt;
+    P.tcap = per;
+    p->tr_per = per;
+  }
   const int rps = cfg->rounds_per_sync > 0 ? cfg->rounds_per_sync : 8;
   auto t0 = std::chrono::steady_clock::now();
   int prof = p->profiling;
@@ -1177,6 +1198,40 @@ int mdr_local_search(mdr_pop *p, const mdr_ls_cfg *cfg, mdr_ls_stats *stats, voi
   }
   if (worst == MDR_ERR_CAPACITY) return fail(worst, "capacity exceeded during local search (J_cap/K_cap/F_cap)");
   if (worst) return fail(worst, "local search stopped with an error status");
+  return MDR_OK;
+}
+
+int mdr_pop_route_attrs(mdr_pop *p, int32_t b0, int32_t nb, double *out, void *stream) {
+  if (!p || !out) return fail(MDR_ERR_ARG, "null argument");
+  if (b0 < 0 || nb < 0 || b0 + nb > p->B) return fail(MDR_ERR_ARG, "individual range out of bounds");
+  if (nb == 0) return MDR_OK;
+  cudaStream_t s = (cudaStream_t)stream;
+  CK(cudaSetDevice(p->inst->device));
+  const size_t n = (size_t)nb * p->P.J * 6;
+  double *d = nullptr;
+  CK(cudaMalloc(&d, sizeof(double) * n));
+  auto run = [&]() -> int {
+    launch_route_attrs(p->inst->I, p->P, b0, nb, d, s);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(out, d, sizeof(double) * n, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    return MDR_OK;
+  };
+  const int rc = run();
+  cudaFree(d);
+  return rc;
+}
+
+int mdr_pop_trace(mdr_pop *p, int32_t b, uint64_t *out, int64_t cap, int64_t *n) {
+  if (!p || !n) return fail(MDR_ERR_ARG, "null argument");
+  if (b < 0 || b >= p->B || !p->tr_buf || !p->tr_per) return fail(MDR_ERR_ARG, "no trace of this individual");
+  CK(cudaSetDevice(p->inst->device));
+  long long cnt = 0;
+  CK(cudaMemcpy(&cnt, p->tr_cnt + b, sizeof(long long), cudaMemcpyDeviceToHost));
+  *n = cnt;
+  if (cnt > p->tr_per) return fail(MDR_ERR_CAPACITY, "trace overflow");
+  if (!out || cap < cnt) return fail(MDR_ERR_CAPACITY, "trace output buffer too small");
+  if (cnt) CK(cudaMemcpy(out, p->tr_buf + (size_t)b * p->tr_per, sizeof(uint64_t) * cnt, cudaMemcpyDeviceToHost));
   return MDR_OK;
 }
 

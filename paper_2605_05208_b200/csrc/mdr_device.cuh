@@ -35,6 +35,9 @@
 #ifndef MDR_LARGE_CU
 #define MDR_LARGE_CU 16
 #endif
+#ifndef MDR_EVAL_OCC
+#define MDR_EVAL_OCC 16  // warps per SM the staged evaluators are register-budgeted for (launch bounds)
+#endif
 #ifndef MDR_LARGE_CT
 #define MDR_LARGE_CT 32
 #endif
@@ -112,6 +115,10 @@ struct DevPop {
   int *nanflag;               // [B]
   int *scratch_seq;           // [B][J][Kp]
   int4 *scratch_meta;         // [B][J]
+  // accepted-step trace (on_feasible replay): per individual [tcap] words, trcount used
+  unsigned long long *trace;
+  long long *trcount;
+  long long tcap;
   // best-feasible snapshot
   int *best_m;
   int4 *best_meta;
@@ -123,6 +130,7 @@ struct LsParams {
   double kappa, lam_min, lam_max;
   int B;
   int snapshot;  // keep the best-feasible snapshot (for on_feasible)
+  int trace;     // record every accepted step: {op<<56 | feasible<<55 | n moves, D bits, keys...}
 };
 
 // ---------------------------------------------------------------------------

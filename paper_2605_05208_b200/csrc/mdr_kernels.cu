@@ -359,7 +359,7 @@ __global__ void __launch_bounds__(256, MDR_EVAL_MINB) k_eval(DevInst I, DevPop P
 #endif
 // CTA-task evaluators (relocate, swap, 2-opt*) with staged route boundaries
 template <bool WIN, int OP, int CU, int CT>
-__global__ void __launch_bounds__(32 * CU, 16 / CU) k_eval_c(DevInst I, DevPop P, LsParams L) {
+__global__ void __launch_bounds__(32 * CU, MDR_EVAL_OCC / CU) k_eval_c(DevInst I, DevPop P, LsParams L) {
   extern __shared__ __align__(16) unsigned char smx_c[];
   RB *R = reinterpret_cast<RB *>(smx_c);
   // per-warp depot-indexed precomputes (front-insertion prefixes, 2-opt* A sides)
@@ -594,7 +594,7 @@ __device__ __forceinline__ void pipe_stage(const DevInst &I, const DevPop &P, co
 }
 
 template <bool WIN, int OP, int CU, int CT>
-__global__ void __launch_bounds__(32 * CU, 16 / CU) k_eval_p(DevInst I, DevPop P, LsParams L) {
+__global__ void __launch_bounds__(32 * CU, MDR_EVAL_OCC / CU) k_eval_p(DevInst I, DevPop P, LsParams L) {
   static_assert(OP == 0 || OP == 1, "pipelined form: relocate and swap");
   static_assert(CT <= 32, "one staged customer per lane");
   extern __shared__ __align__(16) unsigned char smx_c[];
@@ -851,7 +851,8 @@ template <bool WIN>
 __global__ void __launch_bounds__(256) k_select(DevInst I, DevPop P, LsParams L) {
   extern __shared__ unsigned long long smx[];
   __shared__ OK red[8];
-  __shared__ int s_flag, s_nm, s_mnew, s_snap, s_nt, s_empty;
+  __shared__ int s_flag, s_nm, s_mnew, s_snap, s_nt, s_empty, s_feas;
+  __shared__ double s_D;
   __shared__ unsigned long long s_leader;
   const int b = blockIdx.x;
   if (b >= L.B) return;
@@ -1052,6 +1053,8 @@ __global__ void __launch_bounds__(256) k_select(DevInst I, DevPop P, LsParams L)
         P.lam[b * 4 + i] = L.lam_max < x ? L.lam_max : x;
       }
       s_snap = 0;
+      s_feas = feas;
+      s_D = tot[0];
       if (feas) {
         st.n_feasible++;
         if (tot[0] < st.bestD) { st.bestD = tot[0]; st.n_improving++; s_snap = L.snapshot; }
@@ -1063,6 +1066,19 @@ __global__ void __launch_bounds__(256) k_select(DevInst I, DevPop P, LsParams L)
       P.st[b] = st;
     }
     __syncthreads();
+    if (L.trace) {  // the accepted step for the host's per-state on_feasible replay
+      const long long at = P.trcount[b];
+      unsigned long long *T = P.trace + (size_t)b * P.tcap + at;
+      if (at + 2 + nm <= P.tcap) {
+        for (int t = threadIdx.x; t < nm; t += blockDim.x) T[2 + t] = sel[t];
+        if (threadIdx.x == 0) {
+          T[0] = ((unsigned long long)op << 56) | ((unsigned long long)(s_feas ? 1 : 0) << 55) | (unsigned)nm;
+          T[1] = (unsigned long long)__double_as_longlong(s_D);
+        }
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) P.trcount[b] = at + 2 + nm;  // past tcap: overflow, reported by the host
+    }
     if (s_snap) {  // best-feasible snapshot, only when the caller wants it (on_feasible)
       const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
       for (int r = wid; r < mn; r += nw) {
@@ -1277,7 +1293,8 @@ static void launch_staged_one(const DevInst &I, const DevPop &P, const LsParams 
   // pipelined relocate / swap (k_eval_p): two route-boundary buffers; MDR_NO_PIPE=1 selects k_eval_c
   static int pipe_env = -1;
   if (pipe_env < 0) pipe_env = getenv("MDR_NO_PIPE") ? 0 : 1;
-  const bool pipe = pipe_env && !MDR_REL_WARP && !MDR_SWAP_WARP && CT <= 32;
+  // measured: +2.3 % at C4 (large shape); the small shape (8 warps x 8 items, 2 CTAs/SM) is 2-3 % slower
+  const bool pipe = pipe_env && !MDR_REL_WARP && !MDR_SWAP_WARP && CT <= 32 && CT == MDR_LARGE_CT;
   const size_t smo[3] = {pipe ? 2 * smr : (MDR_REL_WARP ? smw : smr), pipe ? 2 * smr : smr, smw};
   if (sm_set[0] < smo[0] || sm_set[1] < smo[1] || sm_set[2] < smo[2]) {
     void *fn[3] = {pipe ? (void *)k_eval_p<WIN, 0, CU, CT> : (void *)k_eval_c<WIN, 0, CU, CT>,
@@ -1292,7 +1309,8 @@ static void launch_staged_one(const DevInst &I, const DevPop &P, const LsParams 
       cudaFuncAttributes fa;
       size_t st = 3 * 1024;
       if (cudaFuncGetAttributes(&fa, fn[q]) == cudaSuccess) st = fa.sharedSizeBytes + 1024;
-      int pct = (int)(((16 / CU) * (smo[q] + st) * 100 + 228 * 1024 - 1) / (228 * 1024));
+      int pct = (int)(((MDR_EVAL_OCC / CU > 0 ? MDR_EVAL_OCC / CU : 1) * (smo[q] + st) * 100 + 228 * 1024 - 1) /
+                      (228 * 1024));
       if (getenv("MDR_CARVEOUT")) pct = atoi(getenv("MDR_CARVEOUT"));
       if (pct > 100) pct = 100;
       cudaFuncSetAttribute(fn[q], cudaFuncAttributePreferredSharedMemoryCarveout, pct);

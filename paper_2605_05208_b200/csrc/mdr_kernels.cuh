@@ -20,6 +20,7 @@ void launch_repair(const DevInst &I, const DevPop &P, int B, int op, const int *
                    void *pre, void *suf, double *c1, double *c2, int *p1, double *fold, int *foldi, int Pcap,
                    int *status, long long *stats, cudaStream_t s);
 size_t repair_attr_bytes();
+void launch_route_attrs(const DevInst &I, const DevPop &P, int b0, int nb, double *out, cudaStream_t s);
 void launch_construct(const DevInst &I, const DevPop &P, int B, const int *ooff, const int *order, void *pre,
                       void *suf, int Jd, int *n_left, int *left, int *status, cudaStream_t s);
 void launch_breakdown(const DevInst &I, const DevPop &P, int B, const double *lam, double *rt, double *out,

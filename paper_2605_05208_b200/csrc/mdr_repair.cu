@@ -571,6 +571,28 @@ __global__ void __launch_bounds__(128) k_breakdown(DevInst I, DevPop P, int B, c
   }
 }
 
+// route_attr (evaluation.py:97-106) of every route of individuals b0 .. b0+nb-1: the
+// scalar left fold with Python max/min; out[(b - b0) * J + r] = {dist, load, T, E, L, TW}
+__global__ void k_route_attrs(DevInst I, DevPop P, int b0, int nb, double *out) {
+  const int b = b0 + blockIdx.x;
+  if (blockIdx.x >= nb) return;
+  const int m = P.m[b];
+  const int4 *RM = P.rmeta + (size_t)b * P.J;
+  for (int r = threadIdx.x; r < m; r += blockDim.x) {
+    const int4 mt = RM[r];
+    const int *sq = P.seq + ((size_t)b * P.J + r) * P.Kp;
+    const int n = mt.x + (I.open ? 1 : 2);
+    RAt a = r_single(I, sq[0]);
+    for (int i = 1; i < n; i++) a = r_cat(I, a, sq[i - 1], r_single(I, sq[i]), sq[i]);
+    double *o = out + ((size_t)blockIdx.x * P.J + r) * 6;
+    o[0] = a.dist; o[1] = a.load; o[2] = a.T; o[3] = a.E; o[4] = a.L; o[5] = a.TW;
+  }
+}
+
+void launch_route_attrs(const DevInst &I, const DevPop &P, int b0, int nb, double *out, cudaStream_t s) {
+  if (nb > 0) k_route_attrs<<<nb, 128, 0, s>>>(I, P, b0, nb, out);
+}
+
 void launch_breakdown(const DevInst &I, const DevPop &P, int B, const double *lam, double *rt, double *out,
                       cudaStream_t s) {
   if (B <= 0) return;

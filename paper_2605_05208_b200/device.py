@@ -183,7 +183,7 @@ class Population:
 
     def local_search(self, perms: np.ndarray, depth: int, multi_move: bool, kappa: float, lam_min: float,
                      lam_max: float, deadline_s: float = -1.0, rounds_per_sync: int = 8, stream=None,
-                     snapshot_best: bool = False):
+                     snapshot_best: bool = False, trace: bool = False):
         """perms: uint8 [B, max_passes, n_ops]. Returns a list of per-individual stats dicts."""
         B = self.B
         perms = np.ascontiguousarray(perms, dtype=np.uint8)
@@ -197,6 +197,7 @@ class Population:
         cfg.rounds_per_sync = int(rounds_per_sync)
         cfg.use_graph = 0
         cfg.snapshot_best = int(bool(snapshot_best))
+        cfg.trace = int(bool(trace))
         st = (LsStats * max(B, 1))()
         s = stream if stream is not None else _cur_stream(self.dinst.device)
         rc = _lib.lib().mdr_local_search(self.handle, C.byref(cfg), st, s)
@@ -252,6 +253,31 @@ class Population:
         self.B = B
         self.n_cust = int(ooff[-1])
         return [left[b * n_customers: b * n_customers + n_left[b]].tolist() for b in range(B)]
+
+    def trace(self, b: int) -> list:
+        """Accepted steps of individual b's last traced descent: [(op, feasible, D, [keys])]."""
+        n = C.c_int64(0)
+        L = _lib.lib()
+        rc = L.mdr_pop_trace(self.handle, b, None, 0, C.byref(n))
+        if rc not in (_lib.MDR_OK, _lib.MDR_ERR_CAPACITY) or n.value < 0:
+            check(rc, "mdr_pop_trace")
+        buf = np.zeros(max(n.value, 1), np.uint64)
+        check(L.mdr_pop_trace(self.handle, b, ptr(buf, C.POINTER(C.c_uint64)), buf.size, C.byref(n)), "mdr_pop_trace")
+        out, at, w = [], 0, buf.tolist()
+        while at < n.value:
+            head = w[at]
+            k = head & 0xffffffff
+            D = float(np.array([w[at + 1]], np.uint64).view(np.float64)[0])
+            out.append((int(head >> 56), bool((head >> 55) & 1), D, w[at + 2: at + 2 + k]))
+            at += 2 + k
+        return out
+
+    def route_attrs(self, b0: int, nb: int, stream=None) -> np.ndarray:
+        """[nb, J_cap, 6] route_attr {dist, load, T, E, L, TW} of every route (mdr_pop_route_attrs)."""
+        out = np.zeros((max(nb, 1), self.J_cap, 6), np.float64)
+        s = stream if stream is not None else _cur_stream(self.dinst.device)
+        check(_lib.lib().mdr_pop_route_attrs(self.handle, b0, nb, ptr(out, f64p), s), "mdr_pop_route_attrs")
+        return out[:nb]
 
     def info(self) -> dict:
         """Evaluator shape of this population (mdr_pop_info)."""

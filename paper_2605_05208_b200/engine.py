@@ -180,7 +180,7 @@ def run(inst, cfg: SolverConfig, nbr=None) -> RunStats:
         prev = R.stats.best_cost
         x = dcrex([m.sol for m in R.pop.members], inst, R.consts, R.penalties, R.div_bandit, R.ins_bandit, R.rng)
         local_search(x.offspring, R.penalties, R.search, R.nbr, R.consts, inst, R.rng, deadline=R.deadline,
-                     on_feasible=R.snapshot_feasible)
+                     on_feasible=R.snapshot_feasible, feasible_best_only=True)  # keeps only the best
         x.offspring.meta["generation"] = R.gen
         R.absorb(x.offspring, R.pop.members[x.main_index], x.diversity_level, x.insertion_op)
         R.close_generation(prev)
@@ -221,7 +221,7 @@ def _batched_generation(R: "_Run", batch: int, device: int) -> None:
     pens = [R.penalties.clone() for _ in offspring]
     rngs = [random.Random(R.rng.getrandbits(64)) for _ in offspring]
     local_search_population(offspring, pens, R.search, R.nbr, R.consts, inst, rngs, deadline=R.deadline,
-                            device=device, on_feasible=R.snapshot_feasible)
+                            device=device, on_feasible=R.snapshot_feasible, feasible_best_only=True)
     R.penalties.lam[:] = pens[-1].lam
     t3 = time.perf_counter()
     # evaluation.evaluate of every offspring on the device, where the descent left them

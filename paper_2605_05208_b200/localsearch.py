@@ -24,7 +24,8 @@ import numpy as np
 from ._lib import CapacityError
 from .batch import SolutionCache, evaluate_candidates, leader_and_followers
 from .device import Population
-from .moves import ALL_OPS, Op, move_plan
+from .evaluation import RouteAttr
+from .moves import ALL_OPS, Move, Op, move_plan
 from .session import same_consts, session_for
 
 VIOLATION_TOL = 1e-9
@@ -67,8 +68,12 @@ def select_moves(leader, followers) -> list:
     return chosen
 
 
-def apply_moves(sol, moves, inst) -> None:
-    """Host twin of the device apply (localsearch.py:58-82)."""
+_STALE = object()  # attr of a route a replayed step rewrote: refreshed from the device at the end
+
+
+def apply_moves(sol, moves, inst, _stale=None) -> None:
+    """Host twin of the device apply (localsearch.py:58-82); rewritten routes'
+    attr caches are reset (the device refreshes them after a descent)."""
     used: set = set()
     for mv in moves:
         t = mv.routes_touched()
@@ -76,17 +81,21 @@ def apply_moves(sol, moves, inst) -> None:
             raise ValueError("conflicting moves: route sets intersect")
         used |= t
     plans = [move_plan(sol, mv, inst) for mv in moves]
-    route_cls = type(sol.routes[0]) if sol.routes else None
+    from .genetic import _route_cls
+    route_cls = _route_cls(sol)
     new_routes = []
     for ps in plans:
         for p in ps:
             if p.route_index is None:
-                new_routes.append(route_cls(p.depart, p.arrive, p.customers))
+                nr = route_cls(p.depart, p.arrive, p.customers)
+                if hasattr(nr, "attr"):
+                    nr.attr = _stale
+                new_routes.append(nr)
             else:
                 r = sol.routes[p.route_index]
                 r.depart, r.arrive, r.customers = p.depart, p.arrive, p.customers
                 if hasattr(r, "attr"):
-                    r.attr = None
+                    r.attr = _stale
     sol.routes.extend(nr for nr in new_routes if nr.customers)
     sol.drop_empty_routes()
 
@@ -152,7 +161,7 @@ class DeviceSearch:
         return p
 
     def run(self, sols, lams, perms, cfg: SearchConfig, kappa=0.5, lam_min=0.01, lam_max=1e4,
-            deadline_s: float = -1.0, snapshot_best: bool = False):
+            deadline_s: float = -1.0, snapshot_best: bool = False, trace: bool = False):
         """Descents of all `sols` (not modified). Returns (routes, lams, stats)."""
         need = None
         for attempt in range(8):
@@ -160,7 +169,7 @@ class DeviceSearch:
             pop.upload(sols, lams)
             try:
                 stats = pop.local_search(perms, cfg.depth, cfg.multi_move, kappa, lam_min, lam_max, deadline_s,
-                                         snapshot_best=snapshot_best)
+                                         snapshot_best=snapshot_best, trace=trace)
                 break
             except CapacityError as e:
                 need = getattr(e, "need", None) or dict(F=1, G=0, J=0, K=0)
@@ -171,37 +180,48 @@ class DeviceSearch:
         return routes, lam_out, stats
 
 
-def _apply_result(sol, routes):
+def _apply_result(sol, routes, attrs=None, open_routes: bool = False):
+    """Write a descent's final routes into `sol` in place (localsearch.py:58-82): route
+    objects are reused by index, changed routes get their route_attr refreshed (from
+    the device fold when `attrs` [J, 6] is given, else reset), new routes are appended
+    and the list is cut to the new route count (the device already dropped empties)."""
     from .genetic import _route_cls
-    route_cls = _route_cls(sol)
-    sol.routes = [route_cls(d, a, c) for d, a, c in routes]
+    cls = _route_cls(sol)
+    old = sol.routes
+    for i, (d, a, c) in enumerate(routes):
+        attr = RouteAttr(*(float(x) for x in attrs[i]), d, c[-1] if open_routes else a) \
+            if attrs is not None and c else None
+        if i < len(old):
+            r = old[i]
+            if r.depart != d or r.arrive != a or list(r.customers) != list(c):
+                r.depart, r.arrive, r.customers = d, a, list(c)
+                if hasattr(r, "attr"):
+                    r.attr = attr
+            elif getattr(r, "attr", None) is _STALE:
+                r.attr = attr
+        else:
+            r = cls(d, a, list(c))
+            if hasattr(r, "attr"):
+                r.attr = attr
+            old.append(r)
+    del old[len(routes):]
 
 
-def local_search(sol, penalties, cfg: SearchConfig, nbr, consts, inst, rng, deadline: Optional[float] = None,
-                 on_feasible=None):
-    """Reference-compatible descent of one solution (in place), run on the GPU.
+def _move_of(op: int, key: int) -> Move:
+    """Inverse of the device's 58-bit packing of Move.key() (csrc/mdr_device.cuh pack_key)."""
+    f = lambda sh, m: (key >> sh) & m  # noqa: E731
+    return Move(Op(op), f(46, 0xfff) - 1, f(25, 0x1ff) - 1, f(34, 0xfff) - 1, f(16, 0x1ff) - 1, f(14, 3), f(12, 3),
+                bool(f(11, 1)), bool(f(10, 1)), f(2, 0xff) - 1, f(0, 3) - 1)
 
-    on_feasible(D, sol) is invoked once, after the descent, with the feasible
-    state of lowest D passed through (first reached on ties) -- the only state
-    a best-tracking callback such as engine.snapshot_feasible keeps.
-    """
-    search = _searcher(inst, consts, nbr)
-    ops = enabled_operators(inst)
-    perms = draw_permutations(rng, ops, cfg.depth + 1)[None]
-    dl = -1.0 if deadline is None else max(0.0, deadline - time.monotonic())
-    routes, lam, stats = search.run([sol], [penalties.lam], perms, cfg, penalties.kappa, penalties.lam_min,
-                                    penalties.lam_max, dl, snapshot_best=on_feasible is not None)
-    st = stats[0]
-    _advance(rng, ops, st["passes"])
-    _apply_result(sol, routes[0])
-    penalties.lam[:] = [float(x) for x in lam[0]]
-    if on_feasible is not None and st["n_feasible"] > 0:
-        best_routes, bestD = search.pop.download_best()
-        snap = sol.clone() if hasattr(sol, "clone") else None
-        if snap is not None:
-            _apply_result(snap, best_routes[0])
-            on_feasible(float(bestD[0]), snap)
-    return sol
+
+def _replay(sol, steps, inst, on_feasible) -> None:
+    """Re-apply a traced descent on the host (apply_moves per accepted step) and
+    call on_feasible(D, sol) on every feasible post-step state, in order
+    (localsearch.py:126-134); D is the device's totals()[0] of that state."""
+    for op, feasible, D, keys in steps:
+        apply_moves(sol, [_move_of(op, k) for k in keys], inst, _STALE)
+        if feasible:
+            on_feasible(D, sol)
 
 
 _SEARCHERS: dict = {}
@@ -224,12 +244,52 @@ def _searcher(inst, consts, nbr, device: int = 0) -> DeviceSearch:
     return s
 
 
+def _finish(search, sols, penalties, rngs, routes, lam, stats, inst, ops, on_feasible, best_only: bool):
+    """Hand a device descent back to the caller's objects: rng advanced by the
+    passes used, penalties updated, routes mutated in place with route_attr
+    refreshed from the device, and on_feasible called -- per feasible post-step
+    state by replaying the traced steps (localsearch.py:126-134), or, with
+    best_only, once with the lowest-D feasible state (first reached on ties)."""
+    pop = search.pop
+    attrs = pop.route_attrs(0, len(sols))
+    best = pop.download_best() if (on_feasible is not None and best_only) else None
+    for b, (sol, pen, rng) in enumerate(zip(sols, penalties, rngs)):
+        _advance(rng, ops, stats[b]["passes"])
+        pen.lam[:] = [float(x) for x in lam[b]]
+        if on_feasible is not None and not best_only:
+            _replay(sol, pop.trace(b), inst, on_feasible)
+            got = [(r.depart, r.arrive, list(r.customers)) for r in sol.routes]
+            if got != [(d, a, list(c)) for d, a, c in routes[b]]:
+                raise RuntimeError("host replay of the traced descent diverged from the device result")
+        _apply_result(sol, routes[b], attrs[b], inst.open_routes)
+        if best is not None and stats[b]["n_feasible"] > 0:
+            snap = sol.clone()
+            _apply_result(snap, best[0][b])
+            on_feasible(float(best[1][b]), snap)
+
+
+def local_search(sol, penalties, cfg: SearchConfig, nbr, consts, inst, rng, deadline: Optional[float] = None,
+                 on_feasible=None, feasible_best_only: bool = False):
+    """Reference-compatible descent of one solution (in place), run on the GPU
+    (localsearch.py:97-140): `sol`'s routes are mutated in place with their
+    attr caches refreshed, `penalties.lam` adapted, `rng` advanced by one shuffle
+    per pass, and on_feasible(D, sol) called on every feasible post-step state
+    (the device records the accepted steps; the host replays them only when a
+    callback is given).  feasible_best_only=True calls it once, with the
+    lowest-D feasible state -- all a best-tracking callback keeps -- without the
+    replay."""
+    local_search_population([sol], [penalties], cfg, nbr, consts, inst, [rng], deadline, on_feasible=on_feasible,
+                            feasible_best_only=feasible_best_only)
+    return sol
+
+
 def local_search_population(sols, penalties, cfg: SearchConfig, nbr, consts, inst, rngs,
-                            deadline: Optional[float] = None, device: int = 0, on_feasible=None):
-    """B independent descents in one device run; solutions and penalty states
-    are updated in place.  Returns the per-individual stats.  on_feasible(D, sol),
-    if given, is called per individual (in order) with its lowest-D feasible
-    state passed through, as `local_search` does."""
+                            deadline: Optional[float] = None, device: int = 0, on_feasible=None,
+                            feasible_best_only: bool = False):
+    """B independent descents in one device run; each solution, penalty state
+    and rng is updated in place exactly as a separate `local_search` call would
+    do it (on_feasible(D, sol) per individual, in order).  Returns the
+    per-individual stats."""
     if not (len(sols) == len(penalties) == len(rngs)):
         raise ValueError("sols, penalties and rngs must have the same length")
     if not sols:
@@ -243,15 +303,8 @@ def local_search_population(sols, penalties, cfg: SearchConfig, nbr, consts, ins
     perms = np.stack([draw_permutations(r, ops, cfg.depth + 1) for r in rngs])
     lams = [p.lam for p in penalties]
     dl = -1.0 if deadline is None else max(0.0, deadline - time.monotonic())
+    replay = on_feasible is not None and not feasible_best_only
     routes, lam, stats = search.run(sols, lams, perms, cfg, p0.kappa, p0.lam_min, p0.lam_max, dl,
-                                    snapshot_best=on_feasible is not None)
-    best = search.pop.download_best() if on_feasible is not None else None
-    for b, (sol, pen, rng) in enumerate(zip(sols, penalties, rngs)):
-        _advance(rng, ops, stats[b]["passes"])
-        _apply_result(sol, routes[b])
-        pen.lam[:] = [float(x) for x in lam[b]]
-        if best is not None and stats[b]["n_feasible"] > 0:
-            snap = sol.clone()
-            _apply_result(snap, best[0][b])
-            on_feasible(float(best[1][b]), snap)
+                                    snapshot_best=on_feasible is not None and feasible_best_only, trace=replay)
+    _finish(search, sols, penalties, rngs, routes, lam, stats, inst, ops, on_feasible, feasible_best_only)
     return stats

@@ -50,7 +50,8 @@ def _oracle_kernels(setattr_):
             cache[k] = O.OracleInstance(inst, consts, nbr)
         return cache[k]
 
-    def local_search(sol, penalties, cfg, nbr, consts, inst, rng, deadline=None, on_feasible=None):
+    def local_search(sol, penalties, cfg, nbr, consts, inst, rng, deadline=None, on_feasible=None,
+                     feasible_best_only=False):
         ops = enabled_operators(inst)
         perms = draw_permutations(rng, ops, cfg.depth + 1)
         routes, lam, st, tr = O.local_search(oi_for(inst, consts, nbr), sol, penalties.lam, cfg.depth,
@@ -66,7 +67,7 @@ def _oracle_kernels(setattr_):
         return sol
 
     def local_search_population(sols, penalties, cfg, nbr, consts, inst, rngs, deadline=None, device=0,
-                                on_feasible=None):
+                                on_feasible=None, feasible_best_only=False):
         for s, p, r in zip(sols, penalties, rngs):
             local_search(s, p, cfg, nbr, consts, inst, r, deadline, on_feasible)
 
@@ -121,7 +122,8 @@ def _oracle_kernels(setattr_):
     class _Searcher:
         pop = host_pop
 
-    def lsp_capture(sols, penalties, cfg, nbr, consts, inst, rngs, deadline=None, device=0, on_feasible=None):
+    def lsp_capture(sols, penalties, cfg, nbr, consts, inst, rngs, deadline=None, device=0, on_feasible=None,
+                    feasible_best_only=False):
         host_pop.sols, host_pop.consts, host_pop.inst = sols, consts, inst
         return local_search_population(sols, penalties, cfg, nbr, consts, inst, rngs, deadline, device, on_feasible)
 

@@ -227,19 +227,38 @@ def test_deadline_stops_early():
     assert sorted(sol.customer_list()) == sorted(sols[0].customer_list())
 
 
-def test_on_feasible_reports_best_feasible_state():
-    inst, consts, nbr, sols = _synthetic_states("mdvrp", 30, 2, 21, 1)
-    sol = sols[0].clone()
-    seen = []
-    P.local_search(sol, P.PenaltyState(), P.SearchConfig(500, True), nbr, consts, inst, random.Random(3),
-                   on_feasible=lambda D, s: seen.append((D, G.routes_of(s))))
+@pytest.mark.parametrize("seed", [3, 4, 5, 6])
+def test_on_feasible_per_state_and_attrs(seed):
+    """on_feasible(D, sol) fires on every feasible post-step state, in order
+    (localsearch.py:133-134: D values hex-equal to the oracle's trace); with
+    feasible_best_only once with the lowest D.  Routes are mutated in place and
+    their attr caches equal the scalar route_attr of the final routes."""
+    from oracle.scalar_ref import route_attr
+    inst, consts, nbr, sols = _synthetic_states(["mdvrp", "mdvrptw", "mdovrp", "mdvrptw"][seed % 4], 30, 2, 21 + seed, 1)
     oi = O.OracleInstance(inst, consts, nbr)
-    perms = draw_permutations(random.Random(3), P.enabled_operators(inst), 501)
-    _, _, st, tr = O.local_search(oi, sols[0], [1.0] * 4, 500, True, 0.5, 0.01, 1e4, perms, trace_cap=501)
+    perms = draw_permutations(random.Random(seed), P.enabled_operators(inst), 501)
+    want_routes, _, st, tr = O.local_search(oi, sols[0], [1.0] * 4, 500, True, 0.5, 0.01, 1e4, perms, trace_cap=501)
+    sol = sols[0].clone()
+    objs = list(sol.routes)
+    seen = []
+    P.local_search(sol, P.PenaltyState(), P.SearchConfig(500, True), nbr, consts, inst, random.Random(seed),
+                   on_feasible=lambda D, s: seen.append((D.hex(), G.routes_of(s))))
+    assert [d for d, _ in seen] == [float(x).hex() for x, f in zip(tr["D"], tr["feasible"]) if f]
+    assert G.routes_of(sol) == want_routes
+    assert any(r is o for r in sol.routes for o in objs)  # the caller's Route objects are mutated, not replaced
+    for r in sol.routes:
+        if r.attr is not None:
+            w = route_attr(r, inst)
+            assert [x.hex() for x in (r.attr.dist, r.attr.load, r.attr.T, r.attr.E, r.attr.L, r.attr.TW)] == \
+                [float(x).hex() for x in (w.dist, w.load, w.T, w.E, w.L, w.TW)]
+            assert (r.attr.first, r.attr.last) == (w.first, w.last)
+    best = []
+    P.local_search(sols[0].clone(), P.PenaltyState(), P.SearchConfig(500, True), nbr, consts, inst,
+                   random.Random(seed), on_feasible=lambda D, s: best.append(D), feasible_best_only=True)
     if st["n_feasible"]:
-        assert len(seen) == 1 and seen[0][0] == st["best_feasible_D"]
+        assert best == [st["best_feasible_D"]]
     else:
-        assert not seen
+        assert not best and not seen
 
 
 @pytest.mark.parametrize("name,pop,depth", [("C1", 6, 500), ("C3", 3, 60), ("C5", 1, 8)])
