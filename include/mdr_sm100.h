@@ -195,6 +195,21 @@ int mdr_set_profiling(mdr_pop *pop, int32_t on);
 int mdr_construct(mdr_pop *pop, int32_t B, const int32_t *ooff, const int32_t *order, int32_t *n_left, int32_t *left,
                   void *stream);
 
+/* The route exchange of DCREX (genetic.py:343-446) for B offspring of one generation.
+ * Population: M members, member m owns routes mroute[m] .. mroute[m+1]-1, route r has customers
+ * cust[coff[r] .. coff[r+1]) and endpoints dep[r], arr[r].  Offspring b: main parent main_idx[b],
+ * donors[b*(M-1) ..] in the order rng.shuffle left them, mt[b*625 ..] = rng.getstate()[1] after
+ * those draws (the stream rng.choice continues), sigma_bounds[2b..] = diversity_bounds.  Out:
+ * offspring b = member routes refs[b*J_cap .. +n_refs[b]) (in order); keep[b*C_cap + i] = 1 if the
+ * i-th customer slot (route order, then position) survives _remove_redundant; its unrouted
+ * customers (ascending) and sigma; mt is updated to each stream after its choice draws.
+ * Replaces the exchange half of genetic.dcrex. */
+int mdr_route_exchange(mdr_instance *inst, int32_t M, const int32_t *mroute, const int32_t *coff, const int32_t *cust,
+                       const int32_t *dep, const int32_t *arr, int32_t B, const int32_t *main_idx,
+                       const int32_t *donors, uint32_t *mt, const double *sigma_bounds, int32_t J_cap,
+                       int32_t C_cap, int32_t *refs, int32_t *n_refs, int32_t *keep, int32_t *unrouted,
+                       int32_t *n_unrouted, double *sigma);
+
 /* Forward simulation of n_routes node sequences (route r = seq[off[r] .. off[r+1]), depots
  * included as Route.sequence gives them): out[r*6 ..] = {distance, load, duration, time_warp,
  * late_count, minimal duration (want_min; else = duration)}.  Replaces simulate_route /

@@ -123,6 +123,9 @@ def lib():
                                             C.c_double, f64p, i64p, i32p]
         L.mdr_pop_trace.argtypes = [vp, C.c_int32, C.POINTER(C.c_uint64), C.c_int64, C.POINTER(C.c_int64)]
         L.mdr_pop_route_attrs.argtypes = [vp, C.c_int32, C.c_int32, f64p, vp]
+        L.mdr_route_exchange.argtypes = [vp, C.c_int32, i32p, i32p, i32p, i32p, i32p, C.c_int32, i32p, i32p,
+                                         C.POINTER(C.c_uint32), f64p, C.c_int32, C.c_int32, i32p, i32p, i32p, i32p,
+                                         i32p, f64p]
         L.mdr_construct.argtypes = [vp, C.c_int32, i32p, i32p, i32p, i32p, vp]
         L.mdr_route_sim.argtypes = [vp, C.c_int32, i32p, i32p, C.c_int32, f64p]
         _L = L
@@ -157,5 +160,5 @@ EXPORTED = ("mdr_last_error", "mdr_device_count", "mdr_build_info", "mdr_instanc
             "mdr_leader_followers", "mdr_totals", "mdr_local_search", "mdr_get_timing",
             "mdr_set_profiling", "mdr_shuffle_stream", "mdr_probe_l2_gbs",
             "mdr_probe_fp64_gops", "mdr_neighbor_build", "mdr_repair", "mdr_pop_download_range",
-            "mdr_population_select", "mdr_route_sim", "mdr_construct", "mdr_pop_trace", "mdr_pop_route_attrs",
+            "mdr_population_select", "mdr_route_sim", "mdr_construct", "mdr_pop_trace", "mdr_pop_route_attrs", "mdr_route_exchange",
             "mdr_pop_breakdown", "mdr_pop_info")

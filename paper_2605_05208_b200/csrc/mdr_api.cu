@@ -1235,6 +1235,99 @@ int mdr_pop_trace(mdr_pop *p, int32_t b, uint64_t *out, int64_t cap, int64_t *n)
   return MDR_OK;
 }
 
+int mdr_route_exchange(mdr_instance *inst, int32_t M, const int32_t *mroute, const int32_t *coff, const int32_t *cust,
+                       const int32_t *dep, const int32_t *arr, int32_t B, const int32_t *main_idx,
+                       const int32_t *donors, uint32_t *mt, const double *sigma_bounds, int32_t J_cap,
+                       int32_t C_cap, int32_t *refs, int32_t *n_refs, int32_t *keep, int32_t *unrouted,
+                       int32_t *n_unrouted, double *sigma) {
+  if (!inst || M < 2 || B < 0 || !mroute || !coff || !dep || !arr || (B && (!main_idx || !donors || !mt ||
+      !sigma_bounds || !refs || !n_refs || !keep || !unrouted || !n_unrouted || !sigma)))
+    return fail(MDR_ERR_ARG, "bad argument");
+  if (B == 0) return MDR_OK;
+  const DevInst &I = inst->I;
+  const int R = mroute[M], NC = I.N - I.ND, nc_all = coff[R];
+  int jmax = 1;
+  for (int m = 0; m < M; m++) {
+    if (mroute[m + 1] < mroute[m]) return fail(MDR_ERR_ARG, "mroute must be non-decreasing");
+    jmax = std::max(jmax, mroute[m + 1] - mroute[m]);
+  }
+  for (int b = 0; b < B; b++)
+    if (main_idx[b] < 0 || main_idx[b] >= M) return fail(MDR_ERR_ARG, "main index out of range");
+  for (size_t q = 0; q < (size_t)B * (M - 1); q++)
+    if (donors[q] < 0 || donors[q] >= M) return fail(MDR_ERR_ARG, "donor index out of range");
+  for (int q = 0; q < nc_all; q++)
+    if (cust[q] < I.ND || cust[q] >= I.N) return fail(MDR_ERR_ARG, "route member is not a customer");
+  CK(cudaSetDevice(inst->device));
+  const int words = (I.N + 31) / 32;
+  const int cnt_cap = std::max(I.N, J_cap * jmax + 3 * jmax);
+  std::vector<void *> tmp;
+  auto dmal = [&](size_t bytes) -> void * {
+    void *q = nullptr;
+    if (cudaMalloc(&q, bytes ? bytes : 1) != cudaSuccess) return nullptr;
+    tmp.push_back(q);
+    return q;
+  };
+  int rc = MDR_OK;
+  auto run = [&]() -> int {
+    XcPop X;
+    XcJob Jb;
+    XcOut O;
+    int *d_pop = (int *)dmal(sizeof(int) * ((size_t)(M + 1) + (R + 1) + nc_all + 2 * (size_t)R));
+    int *d_job = (int *)dmal(sizeof(int) * ((size_t)B + (size_t)B * (M - 1)));
+    uint32_t *d_mt = (uint32_t *)dmal(sizeof(uint32_t) * 625 * (size_t)B);
+    double *d_sig = (double *)dmal(sizeof(double) * 3 * (size_t)B);
+    int *d_out = (int *)dmal(sizeof(int) * ((size_t)B * (2 * J_cap + C_cap + NC + 3)));
+    int *d_scr = (int *)dmal(sizeof(int) * (size_t)B * (3 * (size_t)I.N + 3 * words + cnt_cap));
+    long long *d_key = (long long *)dmal(sizeof(long long) * (size_t)B * cnt_cap);
+    if (!d_pop || !d_job || !d_mt || !d_sig || !d_out || !d_scr || !d_key) return fail(MDR_ERR_CUDA, "cudaMalloc failed");
+    int *p = d_pop;
+    CK(cudaMemcpy(p, mroute, sizeof(int) * (M + 1), cudaMemcpyHostToDevice)); X.mroute = p; p += M + 1;
+    CK(cudaMemcpy(p, coff, sizeof(int) * (R + 1), cudaMemcpyHostToDevice)); X.coff = p; p += R + 1;
+    if (nc_all) CK(cudaMemcpy(p, cust, sizeof(int) * nc_all, cudaMemcpyHostToDevice));
+    X.cust = p; p += nc_all;
+    if (R) CK(cudaMemcpy(p, dep, sizeof(int) * R, cudaMemcpyHostToDevice));
+    X.dep = p; p += R;
+    if (R) CK(cudaMemcpy(p, arr, sizeof(int) * R, cudaMemcpyHostToDevice));
+    X.arr = p;
+    CK(cudaMemcpy(d_job, main_idx, sizeof(int) * B, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(d_job + B, donors, sizeof(int) * (size_t)B * (M - 1), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(d_mt, mt, sizeof(uint32_t) * 625 * (size_t)B, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(d_sig, sigma_bounds, sizeof(double) * 2 * (size_t)B, cudaMemcpyHostToDevice));
+    Jb.main = d_job; Jb.donors = d_job + B; Jb.mt = d_mt; Jb.sig = d_sig;
+    int *q = d_out;
+    O.refs = q; q += (size_t)B * J_cap;
+    O.orig = q; q += (size_t)B * J_cap;
+    O.keep = q; q += (size_t)B * C_cap;
+    O.unr = q; q += (size_t)B * NC;
+    O.nref = q; q += B;
+    O.nunr = q; q += B;
+    O.status = q;
+    O.sigma = d_sig + 2 * (size_t)B;
+    O.Jcap = J_cap; O.Ccap = C_cap;
+    int *sc = d_scr;
+    int *prv = sc, *nxt = sc + (size_t)B * I.N, *own = sc + 2 * (size_t)B * I.N;
+    unsigned *bits = (unsigned *)(sc + 3 * (size_t)B * I.N);
+    int *cntp = (int *)(bits + (size_t)B * 3 * words);
+    launch_exchange(I, X, Jb, O, B, M, prv, nxt, own, bits, cntp, d_key, cnt_cap, 0);
+    CK(cudaGetLastError());
+    std::vector<int> st(B);
+    CK(cudaMemcpy(st.data(), O.status, sizeof(int) * B, cudaMemcpyDeviceToHost));
+    for (int b = 0; b < B; b++)
+      if (st[b]) return fail(st[b], "route exchange: capacity (J_cap / C_cap) exceeded");
+    CK(cudaMemcpy(refs, O.refs, sizeof(int) * (size_t)B * J_cap, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(n_refs, O.nref, sizeof(int) * B, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(keep, O.keep, sizeof(int) * (size_t)B * C_cap, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(unrouted, O.unr, sizeof(int) * (size_t)B * NC, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(n_unrouted, O.nunr, sizeof(int) * B, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(sigma, O.sigma, sizeof(double) * B, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(mt, d_mt, sizeof(uint32_t) * 625 * (size_t)B, cudaMemcpyDeviceToHost));
+    return MDR_OK;
+  };
+  rc = run();
+  for (void *t : tmp) cudaFree(t);
+  return rc;
+}
+
 int mdr_route_sim(mdr_instance *inst, int32_t n_routes, const int32_t *off, const int32_t *seq, int32_t want_min,
                   double *out) {
   if (!inst || n_routes < 0 || (n_routes > 0 && (!off || !seq || !out))) return fail(MDR_ERR_ARG, "null argument");

@@ -358,8 +358,8 @@ __global__ void __launch_bounds__(256, MDR_EVAL_MINB) k_eval(DevInst I, DevPop P
 #define MDR_SWAP_WARP 0  // 1: per-customer warp sweep (sswap) instead of the flattened chunks
 #endif
 // CTA-task evaluators (relocate, swap, 2-opt*) with staged route boundaries
-template <bool WIN, int OP, int CU, int CT>
-__global__ void __launch_bounds__(32 * CU, MDR_EVAL_OCC / CU) k_eval_c(DevInst I, DevPop P, LsParams L) {
+template <bool WIN, int OP, int CU, int CT, int MINB>
+__global__ void __launch_bounds__(32 * CU, MINB) k_eval_c(DevInst I, DevPop P, LsParams L) {
   extern __shared__ __align__(16) unsigned char smx_c[];
   RB *R = reinterpret_cast<RB *>(smx_c);
   // per-warp depot-indexed precomputes (front-insertion prefixes, 2-opt* A sides)
@@ -593,8 +593,8 @@ __device__ __forceinline__ void pipe_stage(const DevInst &I, const DevPop &P, co
   }
 }
 
-template <bool WIN, int OP, int CU, int CT>
-__global__ void __launch_bounds__(32 * CU, MDR_EVAL_OCC / CU) k_eval_p(DevInst I, DevPop P, LsParams L) {
+template <bool WIN, int OP, int CU, int CT, int MINB>
+__global__ void __launch_bounds__(32 * CU, MINB) k_eval_p(DevInst I, DevPop P, LsParams L) {
   static_assert(OP == 0 || OP == 1, "pipelined form: relocate and swap");
   static_assert(CT <= 32, "one staged customer per lane");
   extern __shared__ __align__(16) unsigned char smx_c[];
@@ -847,16 +847,32 @@ __device__ bool apply_one(const DevInst &I, const DevPop &P, int b, int op, cons
   }
 }
 
+#ifdef MDR_SEL_PROF
+__device__ unsigned long long g_selprof[16];
+#define SELT(i) do { if (threadIdx.x == 0) { long long t__ = clock64(); atomicAdd(&g_selprof[i], (unsigned long long)(t__ - t_sel)); t_sel = t__; } } while (0)
+#else
+#define SELT(i) do { } while (0)
+#endif
 template <bool WIN>
-__global__ void __launch_bounds__(256) k_select(DevInst I, DevPop P, LsParams L) {
+#ifndef MDR_SEL_SORT
+#define MDR_SEL_SORT 2048  // followers sorted in shared memory up to this many (else repeated block argmin)
+#endif
+
+#ifndef MDR_SEL_THREADS
+#define MDR_SEL_THREADS 512  // one CTA per individual: more warps rebuild more touched routes at once
+#endif
+__global__ void __launch_bounds__(MDR_SEL_THREADS) k_select(DevInst I, DevPop P, LsParams L) {
   extern __shared__ unsigned long long smx[];
-  __shared__ OK red[8];
+  __shared__ OK red[MDR_SEL_THREADS / 32];
   __shared__ int s_flag, s_nm, s_mnew, s_snap, s_nt, s_empty, s_feas;
   __shared__ double s_D;
   __shared__ unsigned long long s_leader;
   const int b = blockIdx.x;
   if (b >= L.B) return;
   if (P.st[b].done) return;
+#ifdef MDR_SEL_PROF
+  long long t_sel = clock64();
+#endif
   const int J = P.J;
   unsigned long long *sel = smx;                            // [J] selected keys
   unsigned *used = reinterpret_cast<unsigned *>(sel + J);   // [J/32+1] route bitmask
@@ -900,7 +916,60 @@ __global__ void __launch_bounds__(256) k_select(DevInst I, DevPop P, LsParams L)
       s_nm = 1;
     }
     __syncthreads();
-    if (L.multi_move) {
+    if (L.multi_move && nf >= 256 && nf <= MDR_SEL_SORT) {
+      // followers sorted once by (dF, key) in shared memory (bitonic), then one
+      // warp walks them in order 32 at a time: the lowest lane whose move touches
+      // no used route is taken, the others re-check -- the greedy of
+      // select_moves without a block-wide argmin per selected move
+      const ulonglong2 *F = P.fol + (size_t)b * P.Fcap;
+      ulonglong2 *S = reinterpret_cast<ulonglong2 *>((reinterpret_cast<uintptr_t>(tl + 3 * J + 1) + 15) & ~uintptr_t(15));
+      int n2 = 32;
+      while (n2 < nf) n2 <<= 1;
+      for (int i = threadIdx.x; i < n2; i += blockDim.x)
+        S[i] = i < nf && F[i].y != s_leader ? F[i] : make_ulonglong2(~0ull, ~0ull);
+      __syncthreads();
+      for (int kk = 2; kk <= n2; kk <<= 1) {
+        for (int jj = kk >> 1; jj > 0; jj >>= 1) {
+          for (int i = threadIdx.x; i < n2; i += blockDim.x) {
+            const int l = i ^ jj;
+            if (l > i) {
+              const ulonglong2 a = S[i], c = S[l];
+              const bool gt = a.x > c.x || (a.x == c.x && a.y > c.y);
+              if (gt == ((i & kk) == 0)) { S[i] = c; S[l] = a; }
+            }
+          }
+          __syncthreads();
+        }
+      }
+      if (threadIdx.x < 32) {
+        const int lane = threadIdx.x;
+        int nm = s_nm;
+        for (int base = 0; base < nf; base += 32) {
+          const ulonglong2 e = S[base + lane];
+          const bool valid = e.x != ~0ull;
+          Cand c = unpack_key(e.y);
+          bool taken = false;
+          if (!__any_sync(0xffffffffu, valid)) break;
+          for (;;) {
+            bool ok = valid && !taken && !((used[c.r1 >> 5] >> (c.r1 & 31)) & 1u);
+            if (ok && c.r2 >= 0) ok = !((used[c.r2 >> 5] >> (c.r2 & 31)) & 1u);
+            const unsigned m = __ballot_sync(0xffffffffu, ok);
+            if (!m) break;
+            const int w = __ffs(m) - 1;
+            if (lane == w) {
+              taken = true;
+              sel[nm] = e.y;
+              used[c.r1 >> 5] |= 1u << (c.r1 & 31);
+              if (c.r2 >= 0) used[c.r2 >> 5] |= 1u << (c.r2 & 31);
+            }
+            nm++;
+            __syncwarp();
+          }
+        }
+        if (lane == 0) s_nm = nm;
+      }
+      __syncthreads();
+    } else if (L.multi_move) {
       const ulonglong2 *F = P.fol + (size_t)b * P.Fcap;
       for (;;) {
         OK x{~0ull, ~0ull};
@@ -924,6 +993,7 @@ __global__ void __launch_bounds__(256) k_select(DevInst I, DevPop P, LsParams L)
         __syncthreads();
       }
     }
+    SELT(0);  // leader + follower selection
     // ---- apply_moves (localsearch.py:58-82); touched routes staged in scratch
     const int m = P.m[b];
     const int nm = s_nm;
@@ -961,6 +1031,7 @@ __global__ void __launch_bounds__(256) k_select(DevInst I, DevPop P, LsParams L)
       if (threadIdx.x == 0) { P.st[b].done = 1; P.st[b].status = 3; }
       return;
     }
+    SELT(1);  // apply
     // drop_empty_routes (model.py:198-199), stable; DI tails were appended at m+t
     const int m2 = m + (op == 4 ? nm : 0);
     // drop_empty_routes removes every empty route, including ones the input carried
@@ -982,6 +1053,7 @@ __global__ void __launch_bounds__(256) k_select(DevInst I, DevPop P, LsParams L)
       __syncthreads();
       rebuild_routes<WIN>(I, P, b, tl, s_nt);
       __syncthreads();
+      SELT(2);  // incremental rebuild
       rebuild_fleet(I, P, b, sm_cnt);
     } else {
     if (threadIdx.x < 32) {
@@ -1021,8 +1093,10 @@ __global__ void __launch_bounds__(256) k_select(DevInst I, DevPop P, LsParams L)
     if (threadIdx.x == 0) P.m[b] = mn_;
     __syncthreads();
     rebuild_block<WIN>(I, P, b, sm_cnt);
+    SELT(3);  // full rebuild (a route emptied)
     }
     const int mn = s_mnew;
+    SELT(4);  // fleet (incremental path)
     // ---- totals, adapt_penalties, bookkeeping (localsearch.py:128-138)
     // the four pairwise sums run on four warps; the closure count (0/1 values,
     // exact in any order) on a fifth
@@ -1090,6 +1164,7 @@ __global__ void __launch_bounds__(256) k_select(DevInst I, DevPop P, LsParams L)
       if (threadIdx.x == 0) P.best_m[b] = mn;
     }
   }
+  SELT(5);  // totals, adapt, trace, snapshot
   // ---- advance the pass/operator cursor
   if (threadIdx.x == 0) {
     LsState st = P.st[b];
@@ -1236,7 +1311,9 @@ __global__ void __launch_bounds__(1024) k_pack(DevPop P, int b0, int B, int best
 // launchers
 // ---------------------------------------------------------------------------
 static size_t select_smem(const DevPop &P) {
-  return sizeof(unsigned long long) * P.J + sizeof(unsigned) * (P.J / 32 + 1) + sizeof(int) * (5 * P.J + P.ND + 8);
+  // sel [J] u64, used bitmask, newidx [2J], sm_cnt [ND+4], tl [3J+1] (+ alignment), sorted followers
+  return sizeof(unsigned long long) * P.J + sizeof(unsigned) * (P.J / 32 + 1) +
+         sizeof(int) * (5 * P.J + P.ND + 8 + 2) + 16 + sizeof(ulonglong2) * MDR_SEL_SORT;
 }
 
 void launch_rebuild(const DevInst &I, const DevPop &P, int B, bool win, cudaStream_t s) {
@@ -1279,72 +1356,67 @@ static void launch_eval_g_region(const DevInst &I, const DevPop &P, const LsPara
 }
 
 // the three staged evaluators of one (CU, CT) shape on the side streams
-template <bool WIN, int CU, int CT>
-static void launch_staged_one(const DevInst &I, const DevPop &P, const LsParams &L, const cudaStream_t *side, int only) {
-  static int gcd[MDR_MAXDEV][3];
-  static size_t sm_setd[MDR_MAXDEV][3];  // per evaluator: the sizes vary independently with J and ND
+// one staged evaluator with its own shape: CU warps per CTA, CT items per task,
+// MINB resident CTAs (register budget 64K / (32 CU MINB)), PIPE = the pipelined form
+template <bool WIN, int OP, int CU, int CT, int MINB, bool PIPE>
+static void launch_op(const DevInst &I, const DevPop &P, const LsParams &L, cudaStream_t st) {
+  static int gridd[MDR_MAXDEV];
+  static size_t smd[MDR_MAXDEV];
   const int dv = cur_dev();
-  int *gc = gcd[dv];
-  size_t *sm_set = sm_setd[dv];
-  // dynamic shared memory: staged route boundaries, plus the per-warp depot-indexed
-  // precomputes for the evaluators that use them (2-opt*; relocate in its warp form)
   const size_t smr = sizeof(RB) * (size_t)P.J;
-  const size_t smw = smr + (I.ND <= MDR_WDMAX ? sizeof(double) * 18 * (size_t)I.ND * CU : 0);
-  // pipelined relocate / swap (k_eval_p): two route-boundary buffers; MDR_NO_PIPE=1 selects k_eval_c
-  static int pipe_env = -1;
-  if (pipe_env < 0) pipe_env = getenv("MDR_NO_PIPE") ? 0 : 1;
-  // measured: +2.3 % at C4 (large shape); the small shape (8 warps x 8 items, 2 CTAs/SM) is 2-3 % slower
-  const bool pipe = pipe_env && !MDR_REL_WARP && !MDR_SWAP_WARP && CT <= 32 && CT == MDR_LARGE_CT;
-  const size_t smo[3] = {pipe ? 2 * smr : (MDR_REL_WARP ? smw : smr), pipe ? 2 * smr : smr, smw};
-  if (sm_set[0] < smo[0] || sm_set[1] < smo[1] || sm_set[2] < smo[2]) {
-    void *fn[3] = {pipe ? (void *)k_eval_p<WIN, 0, CU, CT> : (void *)k_eval_c<WIN, 0, CU, CT>,
-                   pipe ? (void *)k_eval_p<WIN, 1, CU, CT> : (void *)k_eval_c<WIN, 1, CU, CT>,
-                   (void *)k_eval_c<WIN, 2, CU, CT>};
-    for (int q = 0; q < 3; q++) {
-      if (sm_set[q] >= smo[q]) continue;
-      sm_set[q] = smo[q];
-      cudaFuncSetAttribute(fn[q], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smo[q]);
-      // shared-memory carveout just large enough for the resident CTAs (16 / CU):
-      // the rest of the 228 KB stays L1 for the gathers (+2 % on C4 vs the default)
-      cudaFuncAttributes fa;
-      size_t st = 3 * 1024;
-      if (cudaFuncGetAttributes(&fa, fn[q]) == cudaSuccess) st = fa.sharedSizeBytes + 1024;
-      int pct = (int)(((MDR_EVAL_OCC / CU > 0 ? MDR_EVAL_OCC / CU : 1) * (smo[q] + st) * 100 + 228 * 1024 - 1) /
-                      (228 * 1024));
-      if (getenv("MDR_CARVEOUT")) pct = atoi(getenv("MDR_CARVEOUT"));
-      if (pct > 100) pct = 100;
-      cudaFuncSetAttribute(fn[q], cudaFuncAttributePreferredSharedMemoryCarveout, pct);
-    }
+  // 2-opt* (and relocate's warp form) keep per-warp depot-indexed precomputes
+  const bool wd = (OP == 2 || (OP == 0 && MDR_REL_WARP)) && I.ND <= MDR_WDMAX;
+  const size_t sm = PIPE ? 2 * smr : smr + (wd ? sizeof(double) * 18 * (size_t)I.ND * CU : 0);
+  void *fn;
+  if constexpr (PIPE) fn = (void *)k_eval_p<WIN, OP, CU, CT, MINB>;
+  else fn = (void *)k_eval_c<WIN, OP, CU, CT, MINB>;
+  if (smd[dv] < sm) {
+    smd[dv] = sm;
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    // shared-memory carveout just large enough for the resident CTAs: the rest of
+    // the 228 KB stays L1 for the gathers (+2 % on C4 vs the default)
+    cudaFuncAttributes fa;
+    size_t stat = 3 * 1024;
+    if (cudaFuncGetAttributes(&fa, fn) == cudaSuccess) stat = fa.sharedSizeBytes + 1024;
+    int pct = (int)((MINB * (sm + stat) * 100 + 228 * 1024 - 1) / (228 * 1024));
+    if (getenv("MDR_CARVEOUT")) pct = atoi(getenv("MDR_CARVEOUT"));
+    cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, pct > 100 ? 100 : pct);
     cudaFuncSetAttribute(k_eval_g<WIN>, cudaFuncAttributePreferredSharedMemoryCarveout, 0);
-    gc[0] = 0;
+    gridd[dv] = 0;
   }
-  if (!gc[0]) {
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    int per = 1;
-    if (pipe) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_eval_p<WIN, 0, CU, CT>, 32 * CU, smo[0]);
-    else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_eval_c<WIN, 0, CU, CT>, 32 * CU, smo[0]);
-    gc[0] = sms * (per < 1 ? 1 : per);
-    if (pipe) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_eval_p<WIN, 1, CU, CT>, 32 * CU, smo[1]);
-    else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_eval_c<WIN, 1, CU, CT>, 32 * CU, smo[1]);
-    gc[1] = sms * (per < 1 ? 1 : per);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_eval_c<WIN, 2, CU, CT>, 32 * CU, smo[2]);
-    gc[2] = sms * (per < 1 ? 1 : per);
+  if (!gridd[dv]) {
+    int sms = 148, per = 1;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dv);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, (const void *)fn, 32 * CU, sm);
+    gridd[dv] = sms * (per < 1 ? 1 : per);
   }
-  if (pipe) {
-    if (only < 0 || only == 0) k_eval_p<WIN, 0, CU, CT><<<gc[0], 32 * CU, smo[0], side[0]>>>(I, P, L);
-    if (only < 0 || only == 1) k_eval_p<WIN, 1, CU, CT><<<gc[1], 32 * CU, smo[1], side[1]>>>(I, P, L);
-  } else {
-    if (only < 0 || only == 0) k_eval_c<WIN, 0, CU, CT><<<gc[0], 32 * CU, smo[0], side[0]>>>(I, P, L);
-    if (only < 0 || only == 1) k_eval_c<WIN, 1, CU, CT><<<gc[1], 32 * CU, smo[1], side[1]>>>(I, P, L);
-  }
-  if (only < 0 || only == 2) k_eval_c<WIN, 2, CU, CT><<<gc[2], 32 * CU, smo[2], side[2]>>>(I, P, L);
+  if constexpr (PIPE) k_eval_p<WIN, OP, CU, CT, MINB><<<gridd[dv], 32 * CU, sm, st>>>(I, P, L);
+  else k_eval_c<WIN, OP, CU, CT, MINB><<<gridd[dv], 32 * CU, sm, st>>>(I, P, L);
 }
 
-template <bool WIN, int CU, int CT>
-static void launch_staged(const DevInst &I, const DevPop &P, const LsParams &L, const cudaStream_t *side) {
-  launch_staged_one<WIN, CU, CT>(I, P, L, side, -1);
+// the staged evaluators of a population's shape (only < 0: all three, each on its stream).
+// Large shape (>= 100k customers in the population, 32 items per task), per operator,
+// measured on C4: relocate 20 warps x 96 registers (k_eval_c), swap 16 x 128 pipelined,
+// 2-opt* 24 x 80; small shape: 8 warps x 8 items, 2 CTAs per SM.
+template <bool WIN>
+static void launch_staged_one(const DevInst &I, const DevPop &P, const LsParams &L, const cudaStream_t *side, int only) {
+  static int pipe_env = -1;
+  if (pipe_env < 0) pipe_env = getenv("MDR_NO_PIPE") ? 0 : 1;
+  if (P.ct == MDR_LARGE_CT) {
+    if (only < 0 || only == 0) launch_op<WIN, 0, 10, MDR_LARGE_CT, 2, false>(I, P, L, side[0]);
+    if (only < 0 || only == 1) {
+      if (pipe_env) launch_op<WIN, 1, 16, MDR_LARGE_CT, 1, true>(I, P, L, side[1]);
+      else launch_op<WIN, 1, 16, MDR_LARGE_CT, 1, false>(I, P, L, side[1]);
+    }
+    if (only < 0 || only == 2) {  // 2-opt*: 24 x 80 with windows (C4 -7 %), 16 x 128 without (C5: 24 warps -24 %)
+      if (WIN) launch_op<WIN, 2, 8, MDR_LARGE_CT, 3, false>(I, P, L, side[2]);
+      else launch_op<WIN, 2, 16, MDR_LARGE_CT, 1, false>(I, P, L, side[2]);
+    }
+  } else {
+    if (only < 0 || only == 0) launch_op<WIN, 0, MDR_SMALL_CU, MDR_SMALL_CT, 2, false>(I, P, L, side[0]);
+    if (only < 0 || only == 1) launch_op<WIN, 1, MDR_SMALL_CU, MDR_SMALL_CT, 2, false>(I, P, L, side[1]);
+    if (only < 0 || only == 2) launch_op<WIN, 2, MDR_SMALL_CU, MDR_SMALL_CT, 2, false>(I, P, L, side[2]);
+  }
 }
 
 // kt (profiling only): 7 timing events; the branches are then serialised on s and
@@ -1362,18 +1434,15 @@ static void launch_eval_t(const DevInst &I, const DevPop &P, const LsParams &L, 
   if (P.staged && kt) {
     const cudaStream_t ser[3] = {s, s, s};
     cudaEventRecord(kt[0], s);
-    if (P.ct == MDR_LARGE_CT) launch_staged_one<WIN, MDR_LARGE_CU, MDR_LARGE_CT>(I, P, L, ser, 0);
-    else launch_staged_one<WIN, MDR_SMALL_CU, MDR_SMALL_CT>(I, P, L, ser, 0);
+    launch_staged_one<WIN>(I, P, L, ser, 0);
     cudaEventRecord(kt[1], s);
     if (P.gbase[1] > 0) launch_eval_g_region<WIN>(I, P, L, s, 1);
     cudaEventRecord(kt[2], s);
-    if (P.ct == MDR_LARGE_CT) launch_staged_one<WIN, MDR_LARGE_CU, MDR_LARGE_CT>(I, P, L, ser, 1);
-    else launch_staged_one<WIN, MDR_SMALL_CU, MDR_SMALL_CT>(I, P, L, ser, 1);
+    launch_staged_one<WIN>(I, P, L, ser, 1);
     cudaEventRecord(kt[3], s);
     if (P.gbase[1] > 0) launch_eval_g_region<WIN>(I, P, L, s, 2);
     cudaEventRecord(kt[4], s);
-    if (P.ct == MDR_LARGE_CT) launch_staged_one<WIN, MDR_LARGE_CU, MDR_LARGE_CT>(I, P, L, ser, 2);
-    else launch_staged_one<WIN, MDR_SMALL_CU, MDR_SMALL_CT>(I, P, L, ser, 2);
+    launch_staged_one<WIN>(I, P, L, ser, 2);
     cudaEventRecord(kt[5], s);
     if (!WIN) k_eval<WIN, 3><<<g[3], 256, 0, s>>>(I, P, L);
     k_eval<WIN, 4><<<g[4], 256, 0, s>>>(I, P, L);
@@ -1385,8 +1454,7 @@ static void launch_eval_t(const DevInst &I, const DevPop &P, const LsParams &L, 
     // persistent grids back-fill each other's tails
     cudaEventRecord(ev[0], s);
     for (int q = 0; q < 3; q++) cudaStreamWaitEvent(side[q], ev[0], 0);
-    if (P.ct == MDR_LARGE_CT) launch_staged<WIN, MDR_LARGE_CU, MDR_LARGE_CT>(I, P, L, side);
-    else launch_staged<WIN, MDR_SMALL_CU, MDR_SMALL_CT>(I, P, L, side);
+    launch_staged_one<WIN>(I, P, L, side, -1);
     const bool ov0 = P.gbase[1] > 0;
     if (ov0) {  // each producer's intra-route queue drained right behind it, on its branch
       launch_eval_g_region<WIN>(I, P, L, side[0], 1);
@@ -1442,13 +1510,13 @@ void launch_select(const DevInst &I, const DevPop &P, const LsParams &L, bool wi
       cudaFuncSetAttribute(k_select<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
       set_t = sm;
     }
-    k_select<true><<<L.B, 256, sm, s>>>(I, P, L);
+    k_select<true><<<L.B, MDR_SEL_THREADS, sm, s>>>(I, P, L);
   } else {
     if (sm > 48 * 1024 && sm > set_f) {
       cudaFuncSetAttribute(k_select<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
       set_f = sm;
     }
-    k_select<false><<<L.B, 256, sm, s>>>(I, P, L);
+    k_select<false><<<L.B, MDR_SEL_THREADS, sm, s>>>(I, P, L);
   }
 }
 
@@ -1489,3 +1557,10 @@ void launch_lf_prep(const MatCands &c, const MatDeltas &d, unsigned long long *o
 }
 
 }  // namespace mdr
+
+#ifdef MDR_SEL_PROF
+// diagnostic build only (-DMDR_SEL_PROF): k_select phase clocks summed over all CTAs
+extern "C" int mdr_debug_selprof(unsigned long long out[16]) {
+  return cudaMemcpyFromSymbol(out, mdr::g_selprof, sizeof(unsigned long long) * 16) == cudaSuccess ? 0 : 4;
+}
+#endif

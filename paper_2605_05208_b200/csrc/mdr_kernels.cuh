@@ -46,4 +46,32 @@ void launch_unpack(const DevInst &I, const DevPop &P, int B, const int *rbase, c
 void launch_pack(const DevPop &P, int b0, int B, int best, int *rbase, int *coff, int *cust, int *dep, int *arr, int *hdr,
                  int cap_r, int cap_c, cudaStream_t s);
 
+struct XcPop {  // the population's members, flattened
+  const int *mroute;  // [M+1] first route of member m
+  const int *coff;    // [R+1] first customer of route r
+  const int *cust;
+  const int *dep, *arr;
+};
+
+struct XcJob {  // per offspring
+  const int *main, *donors;  // [B], [B][M-1]
+  uint32_t *mt;              // [B][625] state words + index (updated: the stream after the draws)
+  const double *sig;         // [B][2] sigma_min, sigma_max
+};
+
+struct XcOut {
+  int *refs;    // [B][Jcap] offspring routes as member routes (global route ids), then kept flags
+  int *nref;    // [B]
+  int *orig;    // [B][Jcap] 1 = main origin
+  int *keep;    // [B][Ccap] per offspring customer slot (route order, position order): 1 kept
+  int *unr;     // [B][NC] unrouted customers, ascending
+  int *nunr;    // [B]
+  double *sigma;  // [B]
+  int *status;    // [B]
+  int Jcap, Ccap;
+};
+
+void launch_exchange(const DevInst &I, const XcPop &X, const XcJob &Jb, const XcOut &O, int B, int M, int *prv,
+                     int *nxt, int *owner, unsigned *bits, int *cnt, long long *key, int cnt_cap, cudaStream_t s);
+
 }  // namespace mdr

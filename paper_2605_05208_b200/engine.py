@@ -9,8 +9,10 @@ tests/golden/engine.json).
 
 `run_batched(inst, cfg, batch)` is the B200 form: every generation builds
 `batch` offspring (one route exchange each, from the generation's population
-and bandit state), repairs them in one device call per insertion operator and
-descends them together with `local_search_population`; the population, the
+and bandit state, all exchanges in one device call with one rng per offspring
+drawn from the run's: `route_exchange_batch`), repairs them in one device call
+per insertion operator and descends them together with
+`local_search_population`; survivor selection runs on the device too; the population, the
 bandits and the best-so-far are then updated offspring by offspring in order.
 Each offspring's local search draws from its own `random.Random` seeded from
 the run's rng, and starts from the run's current penalty weights; the run's
@@ -27,7 +29,8 @@ from typing import Optional
 
 from .evaluation import EvalBreakdown, PenaltyState, ScalingConstants, evaluate
 from .genetic import (DIVERSITY_LEVELS, DiscountedUCB1, InsertionOperator, dcrex, improvement_reward,
-                      initialize_population, repair_insert, repair_population, route_exchange)
+                      initialize_population, repair_insert, repair_population, route_exchange,
+                      route_exchange_batch)
 from .localsearch import SearchConfig, _searcher, local_search, local_search_population
 from .model import INF, Route, Solution
 from .neighborhood import NeighborConfig, build_device
@@ -195,8 +198,9 @@ def _batched_generation(R: "_Run", batch: int, device: int) -> None:
     parents = list(R.pop.members)
     members = [m.sol for m in parents]
     kids, info = [], []
-    for _ in range(batch):
-        off, unrouted, level, _, main_index = route_exchange(members, inst, R.div_bandit, R.rng)
+    # one rng per offspring (drawn from the run's), so the B exchanges run together on the device
+    xr = [random.Random(R.rng.getrandbits(64)) for _ in range(batch)]
+    for off, unrouted, level, _, main_index in route_exchange_batch(members, inst, R.div_bandit, xr, device):
         op = InsertionOperator(R.ins_bandit.select())
         kids.append((off, unrouted))
         info.append((parents[main_index], level, op))

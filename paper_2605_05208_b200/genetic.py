@@ -428,6 +428,74 @@ def route_exchange(population: Sequence, inst, diversity_bandit: DiscountedUCB1,
     return off, unrouted, level, sigma, main_index
 
 
+def route_exchange_batch(population: Sequence, inst, diversity_bandit: DiscountedUCB1, rngs, device: int = 0):
+    """route_exchange for len(rngs) offspring of one generation at once: offspring j is
+    what route_exchange(population, inst, diversity_bandit, rngs[j]) returns, and
+    rngs[j] is advanced the same way.  The host draws each main parent and donor
+    order (rng.randrange, rng.shuffle); the exchanges themselves -- pair scoring,
+    the top-five choices on the continued MT19937 stream, redundancy removal --
+    run on the device, one CTA per offspring (mdr_route_exchange)."""
+    from . import _lib
+    import ctypes as C
+    M, B = len(population), len(rngs)
+    if M < 2:
+        raise ValueError("crossover needs at least two parents")
+    if B == 0:
+        return []
+    level = diversity_bandit.select()  # no update inside a batch: one level for all
+    mroute = np.zeros(M + 1, np.int32)
+    routes = [r for sol in population for r in sol.routes]
+    mroute[1:] = np.cumsum([len(sol.routes) for sol in population])
+    coff = np.zeros(len(routes) + 1, np.int32)
+    coff[1:] = np.cumsum([len(r.customers) for r in routes])
+    cust = np.ascontiguousarray([c for r in routes for c in r.customers] or [0], np.int32)
+    dep = np.ascontiguousarray([r.depart for r in routes] or [0], np.int32)
+    arr = np.ascontiguousarray([r.arrive for r in routes] or [0], np.int32)
+    mains = np.zeros(B, np.int32)
+    donors = np.zeros((B, M - 1), np.int32)
+    mt = np.zeros((B, 625), np.uint32)
+    sig = np.zeros((B, 2), np.float64)
+    for j, rng in enumerate(rngs):
+        m = rng.randrange(M)
+        order = [i for i in range(M) if i != m]
+        rng.shuffle(order)
+        mains[j], donors[j] = m, order
+        mt[j] = rng.getstate()[1]
+        sig[j] = diversity_bounds(level, inst, population[m])
+    J = max(len(s.routes) for s in population)
+    Jcap = 2 * J + 8
+    Ccap = 2 * inst.n_customers + 8
+    refs = np.zeros((B, Jcap), np.int32)
+    nref = np.zeros(B, np.int32)
+    keep = np.zeros((B, Ccap), np.int32)
+    unr = np.zeros((B, inst.n_customers), np.int32)
+    nunr = np.zeros(B, np.int32)
+    sigma = np.zeros(B, np.float64)
+    sess = session_for(inst, None, None, device)
+    P = _lib.ptr
+    _lib.check(_lib.lib().mdr_route_exchange(
+        sess.dinst.handle, M, P(mroute, _lib.i32p), P(coff, _lib.i32p), P(cust, _lib.i32p), P(dep, _lib.i32p),
+        P(arr, _lib.i32p), B, P(mains, _lib.i32p), P(donors, _lib.i32p), P(mt, C.POINTER(C.c_uint32)),
+        P(sig, _lib.f64p), Jcap, Ccap, P(refs, _lib.i32p), P(nref, _lib.i32p), P(keep, _lib.i32p),
+        P(unr, _lib.i32p), P(nunr, _lib.i32p), P(sigma, _lib.f64p)), "mdr_route_exchange")
+    out = []
+    cl = cust.tolist()
+    for j, rng in enumerate(rngs):
+        st = rng.getstate()
+        rng.setstate((st[0], tuple(int(x) for x in mt[j]), st[2]))
+        cls = _route_cls(population[int(mains[j])])
+        off_routes, at = [], 0
+        for r in refs[j, :nref[j]].tolist():
+            c0, c1 = int(coff[r]), int(coff[r + 1])
+            kept = [cl[p] for p, k in zip(range(c0, c1), keep[j, at:at + c1 - c0]) if k]
+            at += c1 - c0
+            off_routes.append(cls(int(dep[r]), int(arr[r]), kept))
+        off = type(population[int(mains[j])])(off_routes)
+        off.meta = dict(getattr(population[int(mains[j])], "meta", {}))
+        out.append((off, unr[j, :nunr[j]].tolist(), level, float(sigma[j]), int(mains[j])))
+    return out
+
+
 def dcrex(population: Sequence, inst, consts, penalties, diversity_bandit: DiscountedUCB1,
           insertion_bandit: DiscountedUCB1, rng, main_index: Optional[int] = None) -> CrossoverResult:
     """Diversity-controlled route exchange over multiple parents, then repair

@@ -105,6 +105,11 @@ def _oracle_kernels(setattr_):
 
     setattr_(E, "initialize_population", init_pop)
 
+    def exchange_batch(population, inst, bandit, rngs, device=0):  # the host exchange, one rng per offspring
+        return [GN.route_exchange(population, inst, bandit, r) for r in rngs]
+
+    setattr_(E, "route_exchange_batch", exchange_batch)
+
     class _HostPop:  # breakdowns of the last oracle batch, by the host evaluate
         sols = []
 
@@ -228,3 +233,33 @@ def test_islands_gloo_world2_exchange_elites():
     assert g0 == g1 == 4 and o0 == o1 == 12
     assert m0 == m1 == 2  # exchanges after generations 2 and 4
     assert gb0 == gb1 == min(b0, b1)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("variant,nc,nd,open_", [("mdvrp", 120, 4, False), ("mdvrptw", 90, 3, False),
+                                                 ("mdovrp", 100, 5, True)])
+def test_device_route_exchange_equals_host(variant, nc, nd, open_):
+    """route_exchange_batch (mdr_route_exchange, one CTA per offspring) == the host
+    route_exchange (genetic.py:343-446 restated) for every offspring, with each
+    rng advanced identically; populations with duplicate members and all levels."""
+    inst = W.make_instance(random.Random(nc), variant, n_customers=nc, n_depots=nd)
+    pop = [W.random_solution(random.Random(900 + i), inst) for i in range(9)]
+    pop.append(pop[3].clone())  # a duplicate member
+    for level in (0, 3, 9, 19):
+        bandit = GN.DiscountedUCB1(GN.DIVERSITY_LEVELS)
+        for a in range(GN.DIVERSITY_LEVELS):  # make `level` the bandit's choice
+            bandit.counts[a] = 1.0
+            bandit.rewards[a] = 100.0 if a == level else 0.0
+        seeds = [random.Random(level * 1000 + j).getrandbits(64) for j in range(24)]
+        got = GN.route_exchange_batch(pop, inst, bandit, [random.Random(s) for s in seeds])
+        for s, (off, unr, lv, sig, mi) in zip(seeds, got):
+            r = random.Random(s)
+            w_off, w_unr, w_lv, w_sig, w_mi = GN.route_exchange(pop, inst, bandit, r)
+            assert (mi, lv, sig, unr) == (w_mi, w_lv, w_sig, w_unr)
+            assert _routes(off) == _routes(w_off)
+        rs = [random.Random(s) for s in seeds]
+        GN.route_exchange_batch(pop, inst, bandit, rs)
+        for s, r in zip(seeds, rs):
+            w = random.Random(s)
+            GN.route_exchange(pop, inst, bandit, w)
+            assert r.getstate() == w.getstate()
