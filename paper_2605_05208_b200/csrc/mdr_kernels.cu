@@ -358,7 +358,10 @@ __global__ void __launch_bounds__(256, MDR_EVAL_MINB) k_eval(DevInst I, DevPop P
 #define MDR_SWAP_WARP 0  // 1: per-customer warp sweep (sswap) instead of the flattened chunks
 #endif
 // CTA-task evaluators (relocate, swap, 2-opt*) with staged route boundaries
-template <bool WIN, int OP, int CU, int CT, int MINB>
+// FAM (relocate only): 0 both candidate families, 1 the granular (customer, list slot)
+// items only, 2 the boundary (customer, route) items only -- two smaller kernels with
+// their own register budgets
+template <bool WIN, int OP, int CU, int CT, int MINB, int FAM = 0>
 __global__ void __launch_bounds__(32 * CU, MINB) k_eval_c(DevInst I, DevPop P, LsParams L) {
   extern __shared__ __align__(16) unsigned char smx_c[];
   RB *R = reinterpret_cast<RB *>(smx_c);
@@ -432,14 +435,17 @@ __global__ void __launch_bounds__(32 * CU, MINB) k_eval_c(DevInst I, DevPop P, L
     for (int i = 0; i < 4; i++) lam[i] = P.lam[b * 4 + i];
     Acc acc{~0ull, ~0ull, 0};
     const int ngc = (CT * I.W + 31) / 32;
-    const int nit = FLAT ? ngc : FLATR ? ngc + (CT * v.M + 31) / 32 : CT;
+    const int ngb = (CT * v.M + 31) / 32;
+    const int nit = FLAT ? ngc : FLATR ? (FAM == 1 ? ngc : FAM == 2 ? ngb : ngc + ngb) : CT;
     for (;;) {  // warps take the task's items dynamically
       int it = 0;
       if (lane == 0) it = atomicAdd(&s_item, 1);
       it = __shfl_sync(0xffffffffu, it, 0);
       if (it >= nit) break;
       if (FLATR) {
-        srel_chunk<WIN, CT>(I, P, v, R, b, it < ngc ? it : it - ngc, it >= ngc, s_rl, s_rld, lam, mm, acc);
+        if (FAM == 1) srel_chunk<WIN, CT>(I, P, v, R, b, it, false, s_rl, s_rld, lam, mm, acc);
+        else if (FAM == 2) srel_chunk<WIN, CT>(I, P, v, R, b, it, true, s_rl, s_rld, lam, mm, acc);
+        else srel_chunk<WIN, CT>(I, P, v, R, b, it < ngc ? it : it - ngc, it >= ngc, s_rl, s_rld, lam, mm, acc);
       } else if (FLAT) {
         sswap_chunk<WIN, CT>(I, P, v, R, b, it, s_sw, s_swd, lam, mm, acc);
       } else if (OP == 2 && local >= nch) {
@@ -1358,7 +1364,7 @@ static void launch_eval_g_region(const DevInst &I, const DevPop &P, const LsPara
 // the three staged evaluators of one (CU, CT) shape on the side streams
 // one staged evaluator with its own shape: CU warps per CTA, CT items per task,
 // MINB resident CTAs (register budget 64K / (32 CU MINB)), PIPE = the pipelined form
-template <bool WIN, int OP, int CU, int CT, int MINB, bool PIPE>
+template <bool WIN, int OP, int CU, int CT, int MINB, bool PIPE, int FAM = 0>
 static void launch_op(const DevInst &I, const DevPop &P, const LsParams &L, cudaStream_t st) {
   static int gridd[MDR_MAXDEV];
   static size_t smd[MDR_MAXDEV];
@@ -1369,7 +1375,7 @@ static void launch_op(const DevInst &I, const DevPop &P, const LsParams &L, cuda
   const size_t sm = PIPE ? 2 * smr : smr + (wd ? sizeof(double) * 18 * (size_t)I.ND * CU : 0);
   void *fn;
   if constexpr (PIPE) fn = (void *)k_eval_p<WIN, OP, CU, CT, MINB>;
-  else fn = (void *)k_eval_c<WIN, OP, CU, CT, MINB>;
+  else fn = (void *)k_eval_c<WIN, OP, CU, CT, MINB, FAM>;
   if (smd[dv] < sm) {
     smd[dv] = sm;
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
@@ -1391,7 +1397,7 @@ static void launch_op(const DevInst &I, const DevPop &P, const LsParams &L, cuda
     gridd[dv] = sms * (per < 1 ? 1 : per);
   }
   if constexpr (PIPE) k_eval_p<WIN, OP, CU, CT, MINB><<<gridd[dv], 32 * CU, sm, st>>>(I, P, L);
-  else k_eval_c<WIN, OP, CU, CT, MINB><<<gridd[dv], 32 * CU, sm, st>>>(I, P, L);
+  else k_eval_c<WIN, OP, CU, CT, MINB, FAM><<<gridd[dv], 32 * CU, sm, st>>>(I, P, L);
 }
 
 // the staged evaluators of a population's shape (only < 0: all three, each on its stream).
@@ -1403,7 +1409,16 @@ static void launch_staged_one(const DevInst &I, const DevPop &P, const LsParams 
   static int pipe_env = -1;
   if (pipe_env < 0) pipe_env = getenv("MDR_NO_PIPE") ? 0 : 1;
   if (P.ct == MDR_LARGE_CT) {
-    if (only < 0 || only == 0) launch_op<WIN, 0, 10, MDR_LARGE_CT, 2, false>(I, P, L, side[0]);
+    if (only < 0 || only == 0) {
+      static int split = -1;
+      if (split < 0) split = getenv("MDR_REL_SPLIT") ? atoi(getenv("MDR_REL_SPLIT")) : 0;
+      if (split) {  // granular then boundary family, each at 24 warps x 80 registers
+        launch_op<WIN, 0, 8, MDR_LARGE_CT, 3, false, 1>(I, P, L, side[0]);
+        launch_op<WIN, 0, 8, MDR_LARGE_CT, 3, false, 2>(I, P, L, side[0]);
+      } else {
+        launch_op<WIN, 0, 10, MDR_LARGE_CT, 2, false>(I, P, L, side[0]);
+      }
+    }
     if (only < 0 || only == 1) {
       if (pipe_env) launch_op<WIN, 1, 16, MDR_LARGE_CT, 1, true>(I, P, L, side[1]);
       else launch_op<WIN, 1, 16, MDR_LARGE_CT, 1, false>(I, P, L, side[1]);

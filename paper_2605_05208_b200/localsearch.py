@@ -188,9 +188,9 @@ def _apply_result(sol, routes, attrs=None, open_routes: bool = False):
     from .genetic import _route_cls
     cls = _route_cls(sol)
     old = sol.routes
+    rows = attrs[:len(routes)].tolist() if attrs is not None else None
     for i, (d, a, c) in enumerate(routes):
-        attr = RouteAttr(*(float(x) for x in attrs[i]), d, c[-1] if open_routes else a) \
-            if attrs is not None and c else None
+        attr = RouteAttr(*rows[i], d, c[-1] if open_routes else a) if rows is not None and c else None
         if i < len(old):
             r = old[i]
             if r.depart != d or r.arrive != a or list(r.customers) != list(c):

@@ -51,7 +51,7 @@ def num(x):
 
 def main():
     cfg, rep = sys.argv[1], sys.argv[2]
-    kre = re.compile(sys.argv[3] if len(sys.argv) > 3 else r"k_eval_c<.*, 0, \d+, \d+>")
+    kre = re.compile(sys.argv[3] if len(sys.argv) > 3 else r"k_eval_c<[^,]+, 0, \d+, \d+(, \d+)?>")
     out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     hdr, units = rows[0], rows[1]

@@ -34,7 +34,7 @@ tot = 0
 for row in sass[2:]:
     try:
         n = float(row[ie] or 0)
-    except ValueError:
+    except (ValueError, IndexError):
         continue
     t = row[ix].split()
     if not t:
