@@ -268,7 +268,7 @@ static int pop_build(mdr_pop *p, mdr_instance *inst, int32_t Bcap, int32_t J, in
   p->max_chunks = (size_t)Bcap * (size_t)(I.NC + J);  // tasks per round
   DA(A, P.partial, p->max_chunks);
   DA(A, P.tcount, p->max_chunks);
-  DA(A, P.task_next, 6);
+  DA(A, P.task_next, 8);  // [6]: relocate boundary family when split
   DA(A, P.opcnt, 6);
   DA(A, P.optasks, 6);
   DA(A, P.opb, (size_t)6 * Bcap);

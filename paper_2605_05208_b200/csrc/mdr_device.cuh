@@ -96,7 +96,7 @@ struct DevPop {
   int *chunk_off;             // [B+1]
   int *total_chunks;          // [1]
   int *active;                // [1]
-  int *task_next;             // [6] dynamic task counters of the per-operator k_eval
+  int *task_next;             // [8] dynamic task counters: per operator, [6] relocate boundary family (split)
   int *opcnt;                 // [6] individuals evaluating each operator this round
   int *optasks;               // [6] tasks per operator this round
   int *opb;                   // [6][Bcap] individual ids per operator

@@ -273,6 +273,7 @@ __global__ void __launch_bounds__(1024) k_plan(DevInst I, DevPop P, LsParams L) 
     P.task_next[op] = 0;
   }
   if (threadIdx.x == 0) {
+    P.task_next[6] = 0;
     *P.active = 0;
     P.gcount[0] = 0;
     P.gcount[1] = 0;
@@ -392,7 +393,7 @@ __global__ void __launch_bounds__(32 * CU, MINB) k_eval_c(DevInst I, DevPop P, L
       // grab MDR_TGC consecutive tasks at a time: consecutive tasks belong to
       // the same individual, so its tables stay hot in this SM's L1
       if (s_next >= s_end) {
-        int t0 = atomicAdd(P.task_next + OP, MDR_TGC);
+        int t0 = atomicAdd(P.task_next + (FAM == 2 ? 6 : OP), MDR_TGC);
         s_next = t0;
         s_end = min(t0 + MDR_TGC, total);
       }
@@ -1410,9 +1411,11 @@ static void launch_staged_one(const DevInst &I, const DevPop &P, const LsParams 
   if (pipe_env < 0) pipe_env = getenv("MDR_NO_PIPE") ? 0 : 1;
   if (P.ct == MDR_LARGE_CT) {
     if (only < 0 || only == 0) {
+      // with windows: granular then boundary family as two kernels, each at 24 warps x 80
+      // registers (C4 +2.4 %); without windows one kernel at 20 x 96 (the split is -9 % at C5)
       static int split = -1;
-      if (split < 0) split = getenv("MDR_REL_SPLIT") ? atoi(getenv("MDR_REL_SPLIT")) : 0;
-      if (split) {  // granular then boundary family, each at 24 warps x 80 registers
+      if (split < 0) split = getenv("MDR_REL_SPLIT") ? atoi(getenv("MDR_REL_SPLIT")) : 1;
+      if (split && WIN) {
         launch_op<WIN, 0, 8, MDR_LARGE_CT, 3, false, 1>(I, P, L, side[0]);
         launch_op<WIN, 0, 8, MDR_LARGE_CT, 3, false, 2>(I, P, L, side[0]);
       } else {

@@ -193,8 +193,8 @@ def _apply_result(sol, routes, attrs=None, open_routes: bool = False):
         attr = RouteAttr(*rows[i], d, c[-1] if open_routes else a) if rows is not None and c else None
         if i < len(old):
             r = old[i]
-            if r.depart != d or r.arrive != a or list(r.customers) != list(c):
-                r.depart, r.arrive, r.customers = d, a, list(c)
+            if r.depart != d or r.arrive != a or r.customers != c:
+                r.depart, r.arrive, r.customers = d, a, c
                 if hasattr(r, "attr"):
                     r.attr = attr
             elif getattr(r, "attr", None) is _STALE:
