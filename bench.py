@@ -376,13 +376,28 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
-def load_ncu(name):
-    """ncu metrics of this config's dominant evaluator from the committed capture
-    (profiles/ncu_roofline.json, written by tools/ncu_roofline.py)."""
+def load_ncu(name, evaluator="relocate"):
+    """ncu roofs of a config's evaluator from the committed captures
+    (profiles/ncu_roofline.json, written by tools/ncu_roofline.py).  An
+    evaluator launched as several kernels (relocate's granular and boundary
+    families) gets the duration-weighted mean of their roofs."""
     try:
-        return json.load(open(os.path.join(ROOT, "profiles", "ncu_roofline.json"))).get(name)
+        allj = json.load(open(os.path.join(ROOT, "profiles", "ncu_roofline.json"))).get(name) or {}
     except Exception:
         return None
+    parts = [v for k, v in allj.items() if k == evaluator or k.startswith(evaluator + "_")]
+    if not parts:
+        return None
+    if len(parts) == 1:
+        return parts[0]
+    w = [p["metrics"].get("duration_ns") or 1.0 for p in parts]
+    roofs = {k: sum(p["roofs"].get(k, 0.0) * x for p, x in zip(parts, w)) / sum(w) for k in parts[0]["roofs"]}
+    binding = max(roofs, key=roofs.get)
+    traffic = sum(p.get("dram_bytes_per_launch") or 0.0 for p in parts)
+    return {"binding": binding, "achieved": roofs[binding], "peak": 1.0, "frac": roofs[binding],
+            "unit": "fraction of the ncu peak of that unit (duration-weighted over the evaluator's kernels)",
+            "roofs": roofs, "dram_bytes_per_launch": traffic, "kernel": " + ".join(p["kernel"] for p in parts),
+            "metrics": {"parts": [p["metrics"] for p in parts]}, "source": parts[0]["source"]}
 
 
 def main():
@@ -513,14 +528,17 @@ def main():
     alg_bytes = float(sum(op_c[o] * ab[o] for o in range(6)))
     alg_fp64 = float(sum(op_c[o] * af[o] for o in range(6)))
     n_rounds_p = max(tm["kern_rounds"], 1)
-    # dominant kernel: the relocate evaluator (staged CTA kernel + the drain of its
-    # intra-route candidates), SURVEY.md 8(d) per-candidate figures x relocate candidates
-    rel_ms = tm["kern_relocate_ms"] + tm["kern_relocate_intra_ms"]
-    rel_avg_ms = rel_ms / n_rounds_p
-    rel_fp64 = op_c[0] * af[0] / n_rounds_p  # per launch
-    rel_bytes = op_c[0] * ab[0] / n_rounds_p
     eval_ms = sum(tm["kern_" + k + "_ms"] for k in ("relocate", "relocate_intra", "swap", "swap_intra",
                                                      "two_opt_star", "depot_generic"))
+    # dominant evaluator: the operator whose kernels (staged evaluator + its intra-route drain)
+    # take the most time in the profiled pass; SURVEY.md 8(d) per-candidate figures x its candidates
+    ev_ms = {0: tm["kern_relocate_ms"] + tm["kern_relocate_intra_ms"],
+             1: tm["kern_swap_ms"] + tm["kern_swap_intra_ms"], 2: tm["kern_two_opt_star_ms"]}
+    dom = max(ev_ms, key=ev_ms.get)
+    dom_name = ("relocate", "swap", "two_opt_star")[dom]
+    rel_avg_ms = ev_ms[dom] / n_rounds_p
+    rel_fp64 = op_c[dom] * af[dom] / n_rounds_p  # per launch
+    rel_bytes = op_c[dom] * ab[dom] / n_rounds_p
     peaks = {}
     try:
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -529,25 +547,26 @@ def main():
     hbm = float(peaks.get("hbm_gbs", 6650.0))
     l2_gbs = measure_l2_gbs(local)
     fp64_peak = measure_fp64_gops(local)
-    ncu = load_ncu(name)
+    ncu = load_ncu(name, dom_name)
     fp64_gops = rel_fp64 / (rel_avg_ms * 1e-3) / 1e9 if rel_avg_ms > 0 else 0.0
     rel_gbs = rel_bytes / (rel_avg_ms * 1e-3) / 1e9 if rel_avg_ms > 0 else 0.0
-    live = {"kernel": "relocate evaluator: k_eval_c<relocate> + its intra-route drain k_eval_g (region 1)",
+    live = {"kernel": f"{dom_name} evaluator: staged kernel(s) + its intra-route drain (k_eval_g)" if dom < 2
+            else "two_opt_star evaluator (staged kernel)",
             "avg_launch_ms": rel_avg_ms, "launches": int(n_rounds_p),
-            "share_of_eval_phase": rel_ms / eval_ms if eval_ms > 0 else None,
+            "share_of_eval_phase": ev_ms[dom] / eval_ms if eval_ms > 0 else None,
             "fp64": {"achieved_gops": fp64_gops, "peak_gops": fp64_peak, "frac": fp64_gops / fp64_peak,
-                     "per_candidate": af[0],
-                     "how": "SURVEY.md 8(d) fp64 ops per relocate candidate x relocate candidates per launch / "
-                            "CUDA-event launch time (profiled pass, evaluators serialised); peak = "
-                            "mdr_probe_fp64_gops (independent dadd/dmul chains, no FMA)"},
+                     "per_candidate": af[dom],
+                     "how": "SURVEY.md 8(d) fp64 ops per candidate x candidates per launch / CUDA-event launch "
+                            "time (profiled pass, evaluators serialised); peak = mdr_probe_fp64_gops "
+                            "(independent dadd/dmul chains, no FMA)"},
             "l2": {"achieved_gbs": rel_gbs, "peak_gbs": l2_gbs, "frac": rel_gbs / l2_gbs,
-                   "per_candidate_bytes": ab[0],
+                   "per_candidate_bytes": ab[dom],
                    "how": "SURVEY.md 8(d) algorithmic bytes per candidate; peak = mdr_probe_l2_gbs "
                           "(ld.global.cg over a 32 MiB L2-resident buffer)"},
             "hbm_peak_gbs": hbm, "hbm_peak_source": "MEASURED_PEAKS.json" if peaks else "fallback"}
     if ncu:
         roof = {"bound": ncu["binding"], "achieved": ncu["achieved"], "peak": ncu["peak"], "unit": ncu["unit"],
-                "frac": ncu["frac"], "traffic": ncu.get("dram_bytes_per_launch"),
+                "frac": ncu["frac"], "traffic": ncu.get("dram_bytes_per_launch"), "roofs": ncu.get("roofs"),
                 "kernel": ncu["kernel"], "ncu": ncu["metrics"], "source": ncu["source"], "live": live}
     else:  # no capture of this config committed: the live fp64 roof
         roof = {"bound": "fp64", "achieved": fp64_gops, "peak": fp64_peak, "unit": "Gop/s",

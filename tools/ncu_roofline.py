@@ -1,6 +1,7 @@
 """Binding-roof summary of a config's dominant evaluator from an ncu --set full capture.
 
-    python tools/ncu_roofline.py CONFIG REPORT.ncu-rep [KERNEL_REGEX] >> merges into profiles/ncu_roofline.json
+    python tools/ncu_roofline.py CONFIG REPORT.ncu-rep [KERNEL_REGEX [LABEL]]
+        -> merges profiles/ncu_roofline.json[CONFIG][LABEL] (LABEL default "relocate")
 
 For every captured launch of the kernel (default: the relocate staged
 evaluator, k_eval_c<*, 0, *, *>) it reads the utilisation of each SM-side roof
@@ -86,9 +87,12 @@ def main():
              "frac": roofs[binding], "roofs": roofs, "dram_bytes_per_launch": traffic,
              "metrics": {k: v for k, v in avg.items() if k not in roofs},
              "source": os.path.relpath(rep, ROOT)}
-    path = os.path.join(ROOT, "profiles", "ncu_roofline.json")
+    path = os.environ.get("NCU_ROOFLINE_OUT") or os.path.join(ROOT, "profiles", "ncu_roofline.json")
     allj = json.load(open(path)) if os.path.exists(path) else {}
-    allj[cfg] = entry
+    label = sys.argv[4] if len(sys.argv) > 4 else "relocate"
+    if not isinstance(allj.get(cfg), dict) or "binding" in allj.get(cfg, {}):
+        allj[cfg] = {}
+    allj[cfg][label] = entry
     json.dump(allj, open(path, "w"), indent=1, sort_keys=True)
     print(json.dumps(entry, indent=1))
 
