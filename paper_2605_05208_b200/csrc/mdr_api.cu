@@ -27,6 +27,10 @@ static int fail(int code, const std::string &msg) {
   return code;
 }
 
+namespace mdr {
+int mdr_fail(int code, const char *msg) { return fail(code, msg); }
+}  // namespace mdr
+
 #define CK(call)                                                                          \
   do {                                                                                    \
     cudaError_t e__ = (call);                                                             \
@@ -234,8 +238,12 @@ static int pop_build(mdr_pop *p, mdr_instance *inst, int32_t Bcap, int32_t J, in
   P.Bcap = Bcap; P.J = J; P.K = K; P.Kp = K + 2; P.Fcap = Fcap; P.FE = I.win ? 6 : 4;
   P.N = I.N; P.ND = I.ND;
   P.staged = (J * 160 <= 96 * 1024) ? 1 : 0;  // RB staging fits shared memory
-  // staged-evaluator shape: the large one once the population holds >= 100k customers
-  P.ct = (long long)Bcap * I.NC >= 100000 ? MDR_LARGE_CT : MDR_SMALL_CT;
+  // staged-evaluator shape: the large one once the population holds >= 100k customers, or
+  // >= 24k customers of instances with >= 768 (>= 24 large tasks per individual).  Measured:
+  // C4 at 64 / 32 individuals +17 % / +4 % with the large shape; C2 (64 x 288) and C3 (128 x 360)
+  // -22 % / -21 % with it
+  const long long tot = (long long)Bcap * I.NC;
+  P.ct = (tot >= 100000 || (I.NC >= 768 && tot >= 24000)) ? MDR_LARGE_CT : MDR_SMALL_CT;
   if (getenv("MDR_CT")) P.ct = atoi(getenv("MDR_CT")) == MDR_LARGE_CT ? MDR_LARGE_CT : MDR_SMALL_CT;
   if (getenv("MDR_NO_STAGED")) P.staged = 0;
   auto &A = p->allocs;

@@ -274,6 +274,7 @@ __global__ void __launch_bounds__(1024) k_plan(DevInst I, DevPop P, LsParams L) 
   }
   if (threadIdx.x == 0) {
     P.task_next[6] = 0;
+    P.task_next[7] = 0;
     *P.active = 0;
     P.gcount[0] = 0;
     P.gcount[1] = 0;
@@ -393,7 +394,7 @@ __global__ void __launch_bounds__(32 * CU, MINB) k_eval_c(DevInst I, DevPop P, L
       // grab MDR_TGC consecutive tasks at a time: consecutive tasks belong to
       // the same individual, so its tables stay hot in this SM's L1
       if (s_next >= s_end) {
-        int t0 = atomicAdd(P.task_next + (FAM == 2 ? 6 : OP), MDR_TGC);
+        int t0 = atomicAdd(P.task_next + (FAM == 2 ? 6 + OP : OP), MDR_TGC);
         s_next = t0;
         s_end = min(t0 + MDR_TGC, total);
       }
@@ -448,7 +449,7 @@ __global__ void __launch_bounds__(32 * CU, MINB) k_eval_c(DevInst I, DevPop P, L
         else if (FAM == 2) srel_chunk<WIN, CT>(I, P, v, R, b, it, true, s_rl, s_rld, lam, mm, acc);
         else srel_chunk<WIN, CT>(I, P, v, R, b, it < ngc ? it : it - ngc, it >= ngc, s_rl, s_rld, lam, mm, acc);
       } else if (FLAT) {
-        sswap_chunk<WIN, CT>(I, P, v, R, b, it, s_sw, s_swd, lam, mm, acc);
+        sswap_chunk<WIN, CT, FAM>(I, P, v, R, b, it, s_sw, s_swd, lam, mm, acc);
       } else if (OP == 2 && local >= nch) {
         const int ra = (local - nch) * CT + it;
         if (ra < v.M) stos_r<WIN>(I, P, v, R, b, ra, lam, mm, acc);
@@ -1423,8 +1424,16 @@ static void launch_staged_one(const DevInst &I, const DevPop &P, const LsParams 
       }
     }
     if (only < 0 || only == 1) {
-      if (pipe_env) launch_op<WIN, 1, 16, MDR_LARGE_CT, 1, true>(I, P, L, side[1]);
-      else launch_op<WIN, 1, 16, MDR_LARGE_CT, 1, false>(I, P, L, side[1]);
+      static int sw_split = -1;
+      if (sw_split < 0) sw_split = getenv("MDR_SWAP_SPLIT") ? atoi(getenv("MDR_SWAP_SPLIT")) : 0;
+      if (sw_split) {  // v-side segment length 1, then 2: two kernels with half the live state
+        launch_op<WIN, 1, 10, MDR_LARGE_CT, 2, false, 1>(I, P, L, side[1]);
+        launch_op<WIN, 1, 10, MDR_LARGE_CT, 2, false, 2>(I, P, L, side[1]);
+      } else if (pipe_env) {
+        launch_op<WIN, 1, 16, MDR_LARGE_CT, 1, true>(I, P, L, side[1]);
+      } else {
+        launch_op<WIN, 1, 16, MDR_LARGE_CT, 1, false>(I, P, L, side[1]);
+      }
     }
     if (only < 0 || only == 2) {  // 2-opt*: 24 x 80 with windows (C4 -7 %), 16 x 128 without (C5: 24 warps -24 %)
       if (WIN) launch_op<WIN, 2, 8, MDR_LARGE_CT, 3, false>(I, P, L, side[2]);

@@ -15,6 +15,7 @@ struct MatDeltas {
   unsigned char *fn;
 };
 
+int mdr_fail(int code, const char *msg);  // sets mdr_last_error (mdr_api.cu)
 void launch_rebuild(const DevInst &I, const DevPop &P, int B, bool win, cudaStream_t s);
 void launch_repair(const DevInst &I, const DevPop &P, int B, int op, const int *pend_off, const int *pend,
                    void *pre, void *suf, double *c1, double *c2, int *p1, double *fold, int *foldi, int Pcap,

@@ -17,6 +17,7 @@
 #include <cstdint>
 
 #include "../../include/mdr_sm100.h"
+#include "mdr_kernels.cuh"
 
 namespace {
 
@@ -111,8 +112,8 @@ extern "C" int mdr_neighbor_build(int32_t device, int32_t n, int32_t n_depots, c
                                   float *kernel_ms) {
   if (n < 1 || n_depots < 0 || n_depots > n || theta < 1 || theta > NB_SLOTS / 2 || !dist || !tw_early ||
       !tw_late || !service || !lists)
-    return MDR_ERR_ARG;
-  if (cudaSetDevice(device) != cudaSuccess) return MDR_ERR_CUDA;
+    return mdr::mdr_fail(MDR_ERR_ARG, "mdr_neighbor_build: bad argument");
+  if (cudaSetDevice(device) != cudaSuccess) return mdr::mdr_fail(MDR_ERR_CUDA, "mdr_neighbor_build: cudaSetDevice");
   const size_t nn = (size_t)n * n;
   const bool alias = time == nullptr || time == dist;
   double *dd = nullptr, *dt = nullptr, *dv = nullptr;
@@ -150,5 +151,5 @@ extern "C" int mdr_neighbor_build(int32_t device, int32_t n, int32_t n_depots, c
   cudaFree(dv);
   cudaFree(dl);
   cudaFree(dm);
-  return rc;
+  return rc == MDR_OK ? rc : mdr::mdr_fail(rc, "mdr_neighbor_build: CUDA error");
 }

@@ -171,18 +171,19 @@ void launch_survivors(int n, int mu, double xi, const double *dist, const double
 }  // namespace mdr
 
 #include "../../include/mdr_sm100.h"
+#include "mdr_kernels.cuh"
 
 extern "C" int mdr_population_select(int32_t device, int32_t n, int32_t row0, const int64_t *edge_off,
                                      const int64_t *edge_keys, double *dist, int32_t mu, double xi,
                                      const double *cost, const int64_t *birth, int32_t *removed) {
   if (n < 0 || row0 < 0 || row0 > n || mu < 0 || !edge_off || !dist || (n > mu && (!cost || !birth || !removed)))
-    return MDR_ERR_ARG;
+    return mdr::mdr_fail(MDR_ERR_ARG, "mdr_population_select: bad argument");
   if (n == 0) return MDR_OK;
-  if (cudaSetDevice(device) != cudaSuccess) return MDR_ERR_CUDA;
+  if (cudaSetDevice(device) != cudaSuccess) return mdr::mdr_fail(MDR_ERR_CUDA, "mdr_population_select: cudaSetDevice");
   const size_t nn = (size_t)n * n;
   const long long nk = edge_off[n];
   for (int i = 0; i < n; i++)
-    if (edge_off[i + 1] < edge_off[i]) return MDR_ERR_ARG;
+    if (edge_off[i + 1] < edge_off[i]) return mdr::mdr_fail(MDR_ERR_ARG, "mdr_population_select: edge_off must be non-decreasing");
   long long *d_off = nullptr, *d_keys = nullptr, *d_birth = nullptr;
   double *d_dist = nullptr, *d_cost = nullptr, *d_div = nullptr;
   unsigned char *d_alive = nullptr;
@@ -221,5 +222,5 @@ extern "C" int mdr_population_select(int32_t device, int32_t n, int32_t row0, co
   cudaFree(d_div);
   cudaFree(d_alive);
   cudaFree(d_rem);
-  return rc;
+  return rc == MDR_OK ? rc : mdr::mdr_fail(rc, "mdr_population_select: CUDA error");
 }

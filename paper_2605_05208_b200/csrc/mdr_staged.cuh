@@ -574,7 +574,9 @@ __device__ __forceinline__ void sswap_stage(const DevInst &I, const IV &v, const
 }
 
 // one 32-item chunk of the task's (customer, slot) space; full-warp call
-template <bool WIN, int CT>
+// XF: which v-side segments this call evaluates -- 0 all, 1 length 1 only, 2 length 2 only
+// (the swap evaluator can run as two kernels, each with half the live state)
+template <bool WIN, int CT, int XF = 0>
 __device__ void sswap_chunk(const DevInst &I, const DevPop &P, const IV &v, const RB *R, int b, int chunk,
                             const SWU *C, const double *UD, const double lam[4], bool mm, Acc &acc) {
   const int lane = threadIdx.x & 31;
@@ -621,7 +623,7 @@ __device__ void sswap_chunk(const DevInst &I, const DevPop &P, const IV &v, cons
     }
   }
 #pragma unroll
-  for (int xi = 0; xi < NV; xi++) {
+  for (int xi = (XF == 2 ? 1 : 0); xi < (XF == 1 ? 1 : NV); xi++) {
     const int lv_ = xi == 0 ? 1 : 2, av = xi == 2;
     const bool xok = inter && pv + lv_ <= k2;
     At<WIN> X, S2;
