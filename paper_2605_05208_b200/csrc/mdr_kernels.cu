@@ -366,10 +366,10 @@ __global__ void __launch_bounds__(256, MDR_EVAL_MINB) k_eval(DevInst I, DevPop P
 template <bool WIN, int OP, int CU, int CT, int MINB, int FAM = 0>
 __global__ void __launch_bounds__(32 * CU, MINB) k_eval_c(DevInst I, DevPop P, LsParams L) {
   extern __shared__ __align__(16) unsigned char smx_c[];
-  RB *R = reinterpret_cast<RB *>(smx_c);
+  RBT<WIN> *R = reinterpret_cast<RBT<WIN> *>(smx_c);
   // per-warp depot-indexed precomputes (front-insertion prefixes, 2-opt* A sides)
   const int WS = I.ND <= MDR_WDMAX ? 18 * I.ND : 0;
-  double *Wd = WS ? reinterpret_cast<double *>(smx_c + sizeof(RB) * P.J) + (threadIdx.x >> 5) * WS : nullptr;
+  double *Wd = WS ? reinterpret_cast<double *>(smx_c + sizeof(RBT<WIN>) * P.J) + (threadIdx.x >> 5) * WS : nullptr;
   __shared__ double s_u[CU][MDR_USLOT];
   constexpr bool FLAT = OP == 1 && !MDR_SWAP_WARP;
   __shared__ __align__(16) double s_swd[FLAT ? CT * MDR_SWD : 1];
@@ -508,12 +508,12 @@ __device__ __forceinline__ void mb_wait(unsigned long long *bar, unsigned parity
 }
 
 template <bool WIN>
-__device__ __forceinline__ void stage_routes_warp(const DevInst &I, const IV &v, RB *R, int lane) {
+__device__ __forceinline__ void stage_routes_warp(const DevInst &I, const IV &v, RBT<WIN> *R, int lane) {
   for (int r = lane; r < v.M; r += 32) {
     const int4 mt = __ldg(v.rm + r);
     const int n = mt.x + (I.open ? 1 : 2);
     const int *sq = v.seq + r * v.Kp;
-    RB &x = R[r];
+    RBT<WIN> &x = R[r];
     x.k = mt.x; x.dep = mt.y; x.arr = mt.z; x.clo = mt.w; x.n = n;
     const double4 rc = ldg4(v.rc + r);
     x.rc[0] = rc.x; x.rc[1] = rc.y; x.rc[2] = rc.z; x.rc[3] = rc.w;
@@ -532,7 +532,7 @@ __device__ __forceinline__ void stage_routes_warp(const DevInst &I, const IV &v,
 
 // k_eval_p's stager: one warp fetches the next task and stages it into buffer nb
 struct PipeShared {
-  RB *R0;
+  void *R0;  // RBT<WIN>[2][J]
   double *ud;  // [2][CT * UDW]
   void *cust;  // RLU[2][CT] or SWU[2][CT]
   unsigned long long *bar_ready, *bar_free;
@@ -580,7 +580,7 @@ __device__ __forceinline__ void pipe_stage(const DevInst &I, const DevPop &P, co
   const int b = S.b[nb];
   if (b >= 0) {
     const IV v = make_iv(P, b);
-    RB *R = S.R0 + (size_t)nb * P.J;
+    RBT<WIN> *R = reinterpret_cast<RBT<WIN> *>(S.R0) + (size_t)nb * P.J;
     if (S.rbuf[nb] != b) {
       stage_routes_warp<WIN>(I, v, R, lane);
       __syncwarp();
@@ -606,7 +606,7 @@ __global__ void __launch_bounds__(32 * CU, MINB) k_eval_p(DevInst I, DevPop P, L
   static_assert(OP == 0 || OP == 1, "pipelined form: relocate and swap");
   static_assert(CT <= 32, "one staged customer per lane");
   extern __shared__ __align__(16) unsigned char smx_c[];
-  RB *const R0 = reinterpret_cast<RB *>(smx_c);
+  RBT<WIN> *const R0 = reinterpret_cast<RBT<WIN> *>(smx_c);
   constexpr int UDW = OP == 0 ? MDR_RLD : MDR_SWD;
   __shared__ __align__(16) double s_ud[2][CT * UDW];
   __shared__ RLU s_rl[OP == 0 ? 2 : 1][OP == 0 ? CT : 1];
@@ -641,7 +641,7 @@ __global__ void __launch_bounds__(32 * CU, MINB) k_eval_p(DevInst I, DevPop P, L
     const int b = s_b[buf];
     if (b < 0) break;
     const IV v = make_iv(P, b);
-    const RB *R = R0 + (size_t)buf * P.J;
+    const RBT<WIN> *R = R0 + (size_t)buf * P.J;
     double lam[4];
 #pragma unroll
     for (int i = 0; i < 4; i++) lam[i] = P.lam[b * 4 + i];
@@ -1371,7 +1371,7 @@ static void launch_op(const DevInst &I, const DevPop &P, const LsParams &L, cuda
   static int gridd[MDR_MAXDEV];
   static size_t smd[MDR_MAXDEV];
   const int dv = cur_dev();
-  const size_t smr = sizeof(RB) * (size_t)P.J;
+  const size_t smr = sizeof(RBT<WIN>) * (size_t)P.J;
   // 2-opt* (and relocate's warp form) keep per-warp depot-indexed precomputes
   const bool wd = (OP == 2 || (OP == 0 && MDR_REL_WARP)) && I.ND <= MDR_WDMAX;
   const size_t sm = PIPE ? 2 * smr : smr + (wd ? sizeof(double) * 18 * (size_t)I.ND * CU : 0);

@@ -16,21 +16,27 @@
 
 namespace mdr {
 
-struct RB {
+template <bool WIN>
+struct RBT {
   double sf[6];  // S[r][1] (suffix after the departure depot), empty when n-1 < 1
   double pb[6];  // P[r][k] (prefix up to the last customer)
   double rc[4];  // route D, V1, V2, V3
   int k, dep, arr, clo;
   int sf_first, sf_last, pb_last, n;
+  // with windows: a 176-byte stride (11 x 16 B), so lanes reading consecutive routes hit
+  // distinct banks (C4 +1.8 %); without windows the 160-byte stride keeps two C5 CTAs'
+  // route tables in shared memory (the padded stride measured -6 % at C5)
+  int pad[WIN ? 4 : 0];
 };
+static_assert(sizeof(RBT<true>) == 176 && sizeof(RBT<false>) == 160, "staged route strides");
 
 template <bool WIN>
-__device__ __forceinline__ void stage_routes(const DevInst &I, const IV &v, RB *R) {
+__device__ __forceinline__ void stage_routes(const DevInst &I, const IV &v, RBT<WIN> *R) {
   for (int r = threadIdx.x; r < v.M; r += blockDim.x) {
     const int4 mt = __ldg(v.rm + r);
     const int n = mt.x + (I.open ? 1 : 2);
     const int *sq = v.seq + r * v.Kp;
-    RB &x = R[r];
+    RBT<WIN> &x = R[r];
     x.k = mt.x; x.dep = mt.y; x.arr = mt.z; x.clo = mt.w; x.n = n;
     const double4 rc = ldg4(v.rc + r);
     x.rc[0] = rc.x; x.rc[1] = rc.y; x.rc[2] = rc.z; x.rc[3] = rc.w;
@@ -48,9 +54,9 @@ __device__ __forceinline__ void stage_routes(const DevInst &I, const IV &v, RB *
 }
 
 template <bool WIN>
-__device__ __forceinline__ At<WIN> rb_sf(const RB &x) { return ld_at<WIN>(x.sf, x.sf_first, x.sf_last); }
+__device__ __forceinline__ At<WIN> rb_sf(const RBT<WIN> &x) { return ld_at<WIN>(x.sf, x.sf_first, x.sf_last); }
 template <bool WIN>
-__device__ __forceinline__ At<WIN> rb_pb(const RB &x) { return ld_at<WIN>(x.pb, x.dep, x.pb_last); }
+__device__ __forceinline__ At<WIN> rb_pb(const RBT<WIN> &x) { return ld_at<WIN>(x.pb, x.dep, x.pb_last); }
 
 // (0 + cA) + cB, old terms, fleet delta, combine (batch.py:545-553) and record.
 // The 58-bit key is packed lazily: only when the candidate can displace the
@@ -89,13 +95,13 @@ __device__ __forceinline__ bool two_route_delta(const DevInst &I, const double c
 // RELOCATE (moves.py:280-311, batch.py:391-428), warp task = customer u
 // ---------------------------------------------------------------------------
 template <bool WIN>
-__device__ void srelocate(const DevInst &I, const DevPop &P, const IV &v, const RB *R, int b, int u,
+__device__ void srelocate(const DevInst &I, const DevPop &P, const IV &v, const RBT<WIN> *R, int b, int u,
                           const double lam[4], bool mm, Acc &acc, double *U, double *Wd) {
   const int lane = threadIdx.x & 31;
   const int lu = __ldg(v.loc + u);
   if (lu < 0) return;
   const int ru = loc_r(lu), pu = loc_p(lu);
-  const RB &X1 = R[ru];
+  const RBT<WIN> &X1 = R[ru];
   const int k1 = X1.k;
   const int nxt = pu + 2 <= k1 ? __ldg(v.seq + ru * v.Kp + pu + 2) : u;
   // U[0..4] removal terms l=1, U[5..9] l=2, U[10..15] seg l=1, U[16..21] seg l=2
@@ -134,7 +140,7 @@ __device__ void srelocate(const DevInst &I, const DevPop &P, const IV &v, const 
   // one candidate: target (r2, tgt) with prefix P2 and (possibly empty) suffix S2,
   // joined to the segment by the links Lp (P2.last -> seg.first) and Ls (seg.last -> S2.first)
   auto eval_links = [&](int len, int rev, int r2, int tgt, const At<WIN> &P2, const At<WIN> &S2, Link Lp, Link Ls,
-                        const RB &X2, unsigned long long &o, unsigned long long &key) -> bool {
+                        const RBT<WIN> &X2, unsigned long long &o, unsigned long long &key) -> bool {
     At<WIN> seg = ld_at<WIN>(U + (len == 1 ? 10 : 16), rev ? (len == 1 ? u : nxt) : u, rev ? u : (len == 1 ? u : nxt));
     At<WIN> B = a_cat_l<WIN>(P2, seg, Lp);
     if (S2.first >= 0) B = a_cat_l<WIN>(B, S2, Ls);
@@ -147,7 +153,7 @@ __device__ void srelocate(const DevInst &I, const DevPop &P, const IV &v, const 
                                 [&] { return key_of(ru, pu, r2, tgt, len, 0, rev, 0, -1, -1); }, key, mm,
                                 P.nanflag + b, o);
   };
-  auto eval_inter = [&](int len, int rev, int r2, int tgt, const At<WIN> &P2, const At<WIN> &S2, const RB &X2,
+  auto eval_inter = [&](int len, int rev, int r2, int tgt, const At<WIN> &P2, const At<WIN> &S2, const RBT<WIN> &X2,
                         unsigned long long &o, unsigned long long &key) -> bool {
     const int sf = rev ? (len == 1 ? u : nxt) : u, sl = rev ? u : (len == 1 ? u : nxt);
     Link Ls{0.0, 0.0};
@@ -217,7 +223,7 @@ __device__ void srelocate(const DevInst &I, const DevPop &P, const IV &v, const 
       int tgt = 0;
       At<WIN> P2, S2;
       if (in) {
-        const RB &X2 = R[rb];
+        const RBT<WIN> &X2 = R[rb];
         if (side == 0) {
           tgt = 0;
           P2 = a_node<WIN>(I, X2.dep);
@@ -239,7 +245,7 @@ __device__ void srelocate(const DevInst &I, const DevPop &P, const IV &v, const 
           if (same) { gqf = true; key = key_of(ru, pu, rb, tgt, len, 0, rev, 0, -1, -1); }
           else if (side == 0 && Wd) {
             // B = (node(dep_rb) (+) seg) (+) S[rb][1] from the precomputed prefix
-            const RB &X2 = R[rb];
+            const RBT<WIN> &X2 = R[rb];
             const int sl = rev ? u : (len == 1 ? u : nxt);
             At<WIN> B = ld_at<WIN>(Wd + (vi * I.ND + X2.dep) * 6, X2.dep, sl);
             if (S2.first >= 0) B = a_cat_l<WIN>(B, S2, link_of(I, sl, S2.first));
@@ -277,13 +283,13 @@ struct RLU {
 #define MDR_RLD 24  // doubles per staged customer: removal terms l=1,2 [10], seg l=1 [6], seg l=2 [6], fleet_dec [1]
 
 template <bool WIN>
-__device__ __forceinline__ void srel_stage(const DevInst &I, const IV &v, const RB *R, int u, RLU &c, double *U) {
+__device__ __forceinline__ void srel_stage(const DevInst &I, const IV &v, const RBT<WIN> *R, int u, RLU &c, double *U) {
   c.u = -1;
   if (u >= I.N) return;
   const int lu = __ldg(v.loc + u);
   if (lu < 0) return;
   const int ru = loc_r(lu), pu = loc_p(lu);
-  const RB &X1 = R[ru];
+  const RBT<WIN> &X1 = R[ru];
   const int k1 = X1.k, n1 = X1.n;
   const int nxt = pu + 2 <= k1 ? __ldg(v.seq + ru * v.Kp + pu + 2) : u;
   c.u = u; c.ru = ru; c.pu = pu; c.nxt = nxt;
@@ -303,7 +309,7 @@ __device__ __forceinline__ void srel_stage(const DevInst &I, const IV &v, const 
 
 // one 32-item chunk: granular items [0, CT*W) when bnd == false, else (customer, route) items [0, CT*M)
 template <bool WIN, int CT>
-__device__ void srel_chunk(const DevInst &I, const DevPop &P, const IV &v, const RB *R, int b, int chunk, bool bnd,
+__device__ void srel_chunk(const DevInst &I, const DevPop &P, const IV &v, const RBT<WIN> *R, int b, int chunk, bool bnd,
                            const RLU *C, const double *UD, const double lam[4], bool mm, Acc &acc) {
   const int lane = threadIdx.x & 31;
   const int per = bnd ? v.M : I.W;
@@ -317,12 +323,12 @@ __device__ void srel_chunk(const DevInst &I, const DevPop &P, const IV &v, const
     U = UD + j * MDR_RLD;
   }
   const bool uok = u >= 0;
-  const RB &X1 = R[uok ? ru : 0];
+  const RBT<WIN> &X1 = R[uok ? ru : 0];
   const int k1 = X1.k;
   const double fdec1 = U[22];
   constexpr int nvar = WIN ? 2 : 3;
   auto eval_links = [&](int len, int rev, int r2, int tgt, const At<WIN> &P2, const At<WIN> &S2, Link Lp, Link Ls,
-                        const RB &X2, unsigned long long &o, unsigned long long &key) -> bool {
+                        const RBT<WIN> &X2, unsigned long long &o, unsigned long long &key) -> bool {
     At<WIN> seg = ld_at<WIN>(U + (len == 1 ? 10 : 16), rev ? (len == 1 ? u : nxt) : u, rev ? u : (len == 1 ? u : nxt));
     At<WIN> B = a_cat_l<WIN>(P2, seg, Lp);
     if (S2.first >= 0) B = a_cat_l<WIN>(B, S2, Ls);
@@ -391,7 +397,7 @@ __device__ void srel_chunk(const DevInst &I, const DevPop &P, const IV &v, const
     int tgt = 0;
     At<WIN> P2, S2;
     if (in) {
-      const RB &X2 = R[rb];
+      const RBT<WIN> &X2 = R[rb];
       if (side == 0) {
         tgt = 0;
         P2 = a_node<WIN>(I, X2.dep);
@@ -431,13 +437,13 @@ __device__ void srel_chunk(const DevInst &I, const DevPop &P, const IV &v, const
 // once per lane and shared by the combos that use it.
 // ---------------------------------------------------------------------------
 template <bool WIN>
-__device__ void sswap(const DevInst &I, const DevPop &P, const IV &v, const RB *R, int b, int u, const double lam[4],
+__device__ void sswap(const DevInst &I, const DevPop &P, const IV &v, const RBT<WIN> *R, int b, int u, const double lam[4],
                       bool mm, Acc &acc, double *U) {
   const int lane = threadIdx.x & 31;
   const int lu = __ldg(v.loc + u);
   if (lu < 0) return;
   const int ru = loc_r(lu), pu = loc_p(lu);
-  const RB &X1 = R[ru];
+  const RBT<WIN> &X1 = R[ru];
   const int k1 = X1.k, n1 = X1.n;
   const int *sq1 = v.seq + ru * v.Kp;
   const int nxtu = pu + 2 <= k1 ? __ldg(sq1 + pu + 2) : u;
@@ -521,7 +527,7 @@ __device__ void sswap(const DevInst &I, const DevPop &P, const IV &v, const RB *
             if (S2.first >= 0) B = a_cat_l<WIN>(B, S2, link_of(I, B.last, S2.first));
             double cA[5], cB[5];
             contrib_fast<WIN>(I, A, X1.dep, X1.arr, k1 - lu_ + lv_, cA);
-            const RB &X2 = R[rv];
+            const RBT<WIN> &X2 = R[rv];
             contrib_fast<WIN>(I, B, X2.dep, X2.arr, k2 - lv_ + lu_, cB);
             fol = two_route_delta<WIN>(I, cA, cB, X1.rc, X2.rc, X1.clo, X2.clo, 0.0, 1, lam, acc,
                                        [&] { return key_of(ru, pu, rv, pv, lu_, lv_, au, av, -1, -1); }, key, mm,
@@ -551,7 +557,7 @@ struct SWU {
 #define MDR_SWD 30  // doubles per staged customer: seg l=1, seg l=2, P[ru][pu], S[ru][pu+2], S[ru][pu+3]
 
 template <bool WIN>
-__device__ __forceinline__ void sswap_stage(const DevInst &I, const IV &v, const RB *R, int u, SWU &c, double *U) {
+__device__ __forceinline__ void sswap_stage(const DevInst &I, const IV &v, const RBT<WIN> *R, int u, SWU &c, double *U) {
   c.u = -1;
   if (u >= I.N) return;
   const int lu = __ldg(v.loc + u);
@@ -577,7 +583,7 @@ __device__ __forceinline__ void sswap_stage(const DevInst &I, const IV &v, const
 // XF: which v-side segments this call evaluates -- 0 all, 1 length 1 only, 2 length 2 only
 // (the swap evaluator can run as two kernels, each with half the live state)
 template <bool WIN, int CT, int XF = 0>
-__device__ void sswap_chunk(const DevInst &I, const DevPop &P, const IV &v, const RB *R, int b, int chunk,
+__device__ void sswap_chunk(const DevInst &I, const DevPop &P, const IV &v, const RBT<WIN> *R, int b, int chunk,
                             const SWU *C, const double *UD, const double lam[4], bool mm, Acc &acc) {
   const int lane = threadIdx.x & 31;
   const int W = I.W;
@@ -599,7 +605,7 @@ __device__ void sswap_chunk(const DevInst &I, const DevPop &P, const IV &v, cons
     int lv = __ldg(v.loc + vv);
     if (lv >= 0) { rv = loc_r(lv); pv = loc_p(lv); }
   }
-  const RB &X1 = R[ru < 0 ? 0 : ru];
+  const RBT<WIN> &X1 = R[ru < 0 ? 0 : ru];
   const int k1 = X1.k;
   const bool same = rv == ru;
   const bool inter = rv >= 0 && !same;
@@ -658,7 +664,7 @@ __device__ void sswap_chunk(const DevInst &I, const DevPop &P, const IV &v, cons
           if (S2.first >= 0) B = a_cat_l<WIN>(B, S2, link_of(I, B.last, S2.first));
           double cA[5], cB[5];
           contrib_fast<WIN>(I, A, X1.dep, X1.arr, k1 - lu_ + lv_, cA);
-          const RB &X2 = R[rv];
+          const RBT<WIN> &X2 = R[rv];
           contrib_fast<WIN>(I, B, X2.dep, X2.arr, k2 - lv_ + lu_, cB);
           fol = two_route_delta<WIN>(I, cA, cB, X1.rc, X2.rc, X1.clo, X2.clo, 0.0, 1, lam, acc,
                                      [&] { return key_of(ru, pu, rv, pv, lu_, lv_, au, av, -1, -1); }, key, mm,
@@ -677,8 +683,8 @@ __device__ void sswap_chunk(const DevInst &I, const DevPop &P, const IV &v, cons
 // A = PA (+) SB, B = PB (+) SA for the cut (r1, p1, r2, p2); SA/SB may be empty
 // uA / uB: which end of the A / B link is warp-uniform (0 = the prefix's last node, 1 = the suffix's first)
 template <bool WIN>
-__device__ __forceinline__ bool tos_eval(const DevInst &I, const DevPop &P, const IV &v, int b, const RB &X1,
-                                         const RB &X2, int r1, int p1, int r2, int p2, const At<WIN> &PA,
+__device__ __forceinline__ bool tos_eval(const DevInst &I, const DevPop &P, const IV &v, int b, const RBT<WIN> &X1,
+                                         const RBT<WIN> &X2, int r1, int p1, int r2, int p2, const At<WIN> &PA,
                                          const At<WIN> &SB, const At<WIN> &PB, const At<WIN> &SA, int uA, int uB,
                                          const double lam[4], Acc &acc, bool mm, unsigned long long &o,
                                          unsigned long long &key) {
@@ -704,8 +710,8 @@ __device__ __forceinline__ bool tos_eval(const DevInst &I, const DevPop &P, cons
 
 // A-side terms given (cA precomputed, nullptr = zero route); B = PB (+) SA computed
 template <bool WIN>
-__device__ __forceinline__ bool tos_eval_pre(const DevInst &I, const DevPop &P, const IV &v, int b, const RB &X1,
-                                             const RB &X2, int r1, int p1, int r2, int p2, const double *cA,
+__device__ __forceinline__ bool tos_eval_pre(const DevInst &I, const DevPop &P, const IV &v, int b, const RBT<WIN> &X1,
+                                             const RBT<WIN> &X2, int r1, int p1, int r2, int p2, const double *cA,
                                              const At<WIN> &PB, const At<WIN> &SA, int uB, const double lam[4],
                                              Acc &acc, bool mm, unsigned long long &o, unsigned long long &key) {
   At<WIN> B = PB;
@@ -727,13 +733,13 @@ __device__ __forceinline__ bool tos_eval_pre(const DevInst &I, const DevPop &P, 
 
 // warp task = customer u: granular cut and the two boundary families
 template <bool WIN>
-__device__ void stos_u(const DevInst &I, const DevPop &P, const IV &v, const RB *R, int b, int u, const double lam[4],
+__device__ void stos_u(const DevInst &I, const DevPop &P, const IV &v, const RBT<WIN> *R, int b, int u, const double lam[4],
                        bool mm, Acc &acc, double *U, double *Wd) {
   const int lane = threadIdx.x & 31;
   const int lu = __ldg(v.loc + u);
   if (lu < 0) return;
   const int ru = loc_r(lu), pu = loc_p(lu);
-  const RB &X1 = R[ru];
+  const RBT<WIN> &X1 = R[ru];
   const int n1 = X1.n;
   const int *sq1 = v.seq + ru * v.Kp;
   // u-side pieces: U[0..5] P[ru][pu+1], U[6..11] S[ru][pu+2], U[12..17] P[ru][pu], U[18..23] S[ru][pu+1]
@@ -764,7 +770,7 @@ __device__ void stos_u(const DevInst &I, const DevPop &P, const IV &v, const RB 
     bool fol = false;
     unsigned long long o = 0, key = 0;
     if (rv >= 0) {
-      const RB &X2 = R[rv];
+      const RBT<WIN> &X2 = R[rv];
       fol = tos_eval<WIN>(I, P, v, b, X1, X2, ru, pu + 1, rv, pv, PU1, suf<WIN>(v, rv, pv + 1, X2.n),
                           pre<WIN>(v, rv, pv), SU2, 0, 1, lam, acc, mm, o, key);
     }
@@ -793,7 +799,7 @@ __device__ void stos_u(const DevInst &I, const DevPop &P, const IV &v, const RB 
       bool fol = false;
       unsigned long long o = 0, key = 0;
       if (in) {
-        const RB &X2 = R[rb];
+        const RBT<WIN> &X2 = R[rb];
         bool drop = (pu + 1 == X1.k);
         if (!I.open) drop = drop && (X1.arr == X2.arr);
         if (!drop) {
@@ -814,7 +820,7 @@ __device__ void stos_u(const DevInst &I, const DevPop &P, const IV &v, const RB 
       bool fol = false;
       unsigned long long o = 0, key = 0;
       if (in) {
-        const RB &X2 = R[rb];
+        const RBT<WIN> &X2 = R[rb];
         At<WIN> SB = X2.sf_first >= 0 ? rb_sf<WIN>(X2) : a_empty<WIN>();
         if (Wd)
           fol = tos_eval_pre<WIN>(I, P, v, b, X2, X1, rb, 0, ru, pu, Wd + (I.ND + X2.dep) * 5, PU0, SB, 0, lam, acc,
@@ -831,10 +837,10 @@ __device__ void stos_u(const DevInst &I, const DevPop &P, const IV &v, const RB 
 
 // warp task = route ra: route pairs (ra, 0, rb, k_rb) (moves.py:401-404)
 template <bool WIN>
-__device__ void stos_r(const DevInst &I, const DevPop &P, const IV &v, const RB *R, int b, int ra, const double lam[4],
+__device__ void stos_r(const DevInst &I, const DevPop &P, const IV &v, const RBT<WIN> *R, int b, int ra, const double lam[4],
                        bool mm, Acc &acc) {
   const int lane = threadIdx.x & 31;
-  const RB &X1 = R[ra];
+  const RBT<WIN> &X1 = R[ra];
   const At<WIN> PA = a_node<WIN>(I, X1.dep);
   const At<WIN> SA = X1.sf_first >= 0 ? rb_sf<WIN>(X1) : a_empty<WIN>();
   for (int base = 0; base < v.M; base += 32) {
@@ -843,7 +849,7 @@ __device__ void stos_r(const DevInst &I, const DevPop &P, const IV &v, const RB 
     unsigned long long o = 0, key = 0;
     if (rb < v.M && rb != ra) {
       // kA = 0 + (k_rb - k_rb) = 0: route ra empties, its new terms are exact zeros
-      const RB &X2 = R[rb];
+      const RBT<WIN> &X2 = R[rb];
       fol = tos_eval_pre<WIN>(I, P, v, b, X1, X2, ra, 0, rb, X2.k, nullptr, rb_pb<WIN>(X2), SA, 1, lam, acc, mm, o,
                               key);
     }

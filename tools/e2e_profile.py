@@ -9,10 +9,11 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import bench  # noqa: E402
 import paper_2605_05208_b200 as P  # noqa: E402
 
-spec, inst, consts, nbr, sols = bench.make_workload("C4", list(range(256)))
+NPOP = int(sys.argv[1]) if len(sys.argv) > 1 else 256
+spec, inst, consts, nbr, sols = bench.make_workload("C4", list(range(NPOP)))
 cfg = P.SearchConfig(depth=500, multi_move=True)
 run = lambda: P.local_search_population([s.clone() for s in sols], [P.PenaltyState() for _ in sols], cfg, nbr,  # noqa
-                                        consts, inst, [random.Random(i) for i in range(256)])
+                                        consts, inst, [random.Random(i) for i in range(NPOP)])
 run()
 pr = cProfile.Profile()
 pr.enable()
