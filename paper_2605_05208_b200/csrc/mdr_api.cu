@@ -237,7 +237,7 @@ static int pop_build(mdr_pop *p, mdr_instance *inst, int32_t Bcap, int32_t J, in
   const DevInst &I = inst->I;
   P.Bcap = Bcap; P.J = J; P.K = K; P.Kp = K + 2; P.Fcap = Fcap; P.FE = I.win ? 6 : 4;
   P.N = I.N; P.ND = I.ND;
-  P.staged = (J * (I.win ? 176 : 160) <= 96 * 1024) ? 1 : 0;  // RBT staging fits shared memory
+  P.staged = (J * (I.win ? 176 : 168) <= 96 * 1024) ? 1 : 0;  // RBT staging fits shared memory
   // staged-evaluator shape: the large one once the population holds >= 100k customers, or
   // >= 24k customers of instances with >= 768 (>= 24 large tasks per individual).  Measured:
   // C4 at 64 / 32 individuals +17 % / +4 % with the large shape; C2 (64 x 288) and C3 (128 x 360)

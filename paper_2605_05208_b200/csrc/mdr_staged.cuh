@@ -16,6 +16,9 @@
 
 namespace mdr {
 
+#ifndef MDR_RB_PAD_NOWIN
+#define MDR_RB_PAD_NOWIN 2  // 168-byte stride without windows (odd count of 8-byte words): C5 +1.4 %
+#endif
 template <bool WIN>
 struct RBT {
   double sf[6];  // S[r][1] (suffix after the departure depot), empty when n-1 < 1
@@ -23,12 +26,11 @@ struct RBT {
   double rc[4];  // route D, V1, V2, V3
   int k, dep, arr, clo;
   int sf_first, sf_last, pb_last, n;
-  // with windows: a 176-byte stride (11 x 16 B), so lanes reading consecutive routes hit
-  // distinct banks (C4 +1.8 %); without windows the 160-byte stride keeps two C5 CTAs'
-  // route tables in shared memory (the padded stride measured -6 % at C5)
-  int pad[WIN ? 4 : 0];
+  // strides that spread lanes reading consecutive routes over distinct banks: with windows
+  // 176 B (11 x 16 B, C4 +1.8 %); without, 168 B (21 x 8 B, C5 +1.4 %; 176 B was -6 % there:
+  // two C5 route tables no longer fit next to the L1 the gathers need)
+  int pad[WIN ? 4 : MDR_RB_PAD_NOWIN];
 };
-static_assert(sizeof(RBT<true>) == 176 && sizeof(RBT<false>) == 160, "staged route strides");
 
 template <bool WIN>
 __device__ __forceinline__ void stage_routes(const DevInst &I, const IV &v, RBT<WIN> *R) {
