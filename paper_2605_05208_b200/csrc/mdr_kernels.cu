@@ -1264,43 +1264,72 @@ __global__ void k_unpack(DevInst I, DevPop P, int B, const int *rbase, const int
   }
 }
 
-// one CTA: flat arrays of all B individuals; hdr = {routes, customers}
+// one CTA: flat arrays of all B individuals; hdr = {routes, customers}.  A warp per
+// individual counts its routes and customers, two block-wide exclusive scans give every
+// individual's route and customer offsets, then a warp per individual writes its rows.
+// Shared memory: 2 * B ints (dynamic).
 __global__ void __launch_bounds__(1024) k_pack(DevPop P, int b0, int B, int best, int *rbase, int *coff, int *cust,
                                                int *dep, int *arr, int *hdr, int cap_r, int cap_c) {
-  __shared__ int s_r, s_c;
-  // individuals b0 .. b0+B-1
+  extern __shared__ int s_pk[];
+  int *s_nr = s_pk, *s_nc = s_pk + B;
+  __shared__ int s_tot[2], s_ws[32];
   const int *M = (best ? P.best_m : P.m) + b0;
   const int4 *RM = (best ? P.best_meta : P.rmeta) + (size_t)b0 * P.J;
   const int *SQ = (best ? P.best_seq : P.seq) + (size_t)b0 * P.J * P.Kp;
-  if (threadIdx.x == 0) {
-    int r = 0, c = 0;
-    for (int b = 0; b < B; b++) {
-      rbase[b] = r;
-      for (int q = 0; q < M[b]; q++) c += RM[(size_t)b * P.J + q].x;
-      r += M[b];
-    }
-    rbase[B] = r;
-    s_r = r; s_c = c;
-    hdr[0] = r; hdr[1] = c;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int b = wid; b < B; b += nw) {
+    const int m = M[b];
+    int c = 0;
+    for (int q = lane; q < m; q += 32) c += RM[(size_t)b * P.J + q].x;
+#pragma unroll
+    for (int sh = 16; sh > 0; sh >>= 1) c += __shfl_xor_sync(0xffffffffu, c, sh);
+    if (lane == 0) { s_nr[b] = m; s_nc[b] = c; }
   }
   __syncthreads();
-  if (s_r > cap_r || s_c > cap_c) return;
-  // route-level offsets: one warp per individual
-  for (int b = threadIdx.x >> 5; b < B; b += blockDim.x >> 5) {
-    int lane = threadIdx.x & 31;
-    int r0 = rbase[b];
-    int cbase = 0;
-    if (lane == 0) {
-      // customer offset of individual b: routes before r0
-      int c = 0;
-      for (int bb = 0; bb < b; bb++)
-        for (int q = 0; q < M[bb]; q++) c += RM[(size_t)bb * P.J + q].x;
-      cbase = c;
+  // exclusive scans of s_nr and s_nc (in place), blockDim-strided chunks with carries
+  for (int arrsel = 0; arrsel < 2; arrsel++) {
+    int *a = arrsel ? s_nc : s_nr;
+    int carry = 0;
+    for (int base = 0; base < B; base += blockDim.x) {
+      const int i = base + threadIdx.x;
+      const int x = i < B ? a[i] : 0;
+      int inc = x;
+#pragma unroll
+      for (int sh = 1; sh < 32; sh <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, inc, sh);
+        if (lane >= sh) inc += y;
+      }
+      if (lane == 31) s_ws[wid] = inc;
+      __syncthreads();
+      if (wid == 0) {
+        int t = lane < nw ? s_ws[lane] : 0;
+#pragma unroll
+        for (int sh = 1; sh < 32; sh <<= 1) {
+          const int y = __shfl_up_sync(0xffffffffu, t, sh);
+          if (lane >= sh) t += y;
+        }
+        s_ws[lane] = t;
+      }
+      __syncthreads();
+      const int excl = carry + inc - x + (wid > 0 ? s_ws[wid - 1] : 0);
+      const int chunk = s_ws[nw - 1];
+      __syncthreads();
+      if (i < B) a[i] = excl;
+      carry += chunk;
     }
-    cbase = __shfl_sync(0xffffffffu, cbase, 0);
-    int c = cbase;
-    for (int q = 0; q < M[b]; q++) {
-      int4 mt = RM[(size_t)b * P.J + q];
+    if (threadIdx.x == 0) s_tot[arrsel] = carry;
+    __syncthreads();
+  }
+  const int R = s_tot[0], Ct = s_tot[1];
+  if (threadIdx.x == 0) { hdr[0] = R; hdr[1] = Ct; }
+  for (int b = threadIdx.x; b < B; b += blockDim.x) rbase[b] = s_nr[b];
+  if (threadIdx.x == 0) rbase[B] = R;
+  if (R > cap_r || Ct > cap_c) return;
+  for (int b = wid; b < B; b += nw) {
+    const int r0 = s_nr[b], m = M[b];
+    int c = s_nc[b];
+    for (int q = 0; q < m; q++) {
+      const int4 mt = RM[(size_t)b * P.J + q];
       const int *row = SQ + ((size_t)b * P.J + q) * P.Kp;
       for (int p = lane; p < mt.x; p += 32) cust[c + p] = row[p + 1];
       if (lane == 0) {
@@ -1310,9 +1339,8 @@ __global__ void __launch_bounds__(1024) k_pack(DevPop P, int b0, int B, int best
       }
       c += mt.x;
     }
-    if (b == B - 1 && lane == 0) coff[r0 + M[b]] = c;
   }
-  if (threadIdx.x == 0 && B > 0 && s_r == 0) coff[0] = 0;
+  if (threadIdx.x == 0) coff[R] = Ct;
 }
 
 // ---------------------------------------------------------------------------
@@ -1574,7 +1602,9 @@ void launch_unpack(const DevInst &I, const DevPop &P, int B, const int *rbase, c
 
 void launch_pack(const DevPop &P, int b0, int B, int best, int *rbase, int *coff, int *cust, int *dep, int *arr,
                  int *hdr, int cap_r, int cap_c, cudaStream_t s) {
-  k_pack<<<1, 1024, 0, s>>>(P, b0, B, best, rbase, coff, cust, dep, arr, hdr, cap_r, cap_c);
+  const size_t sm = sizeof(int) * 2 * (size_t)(B > 0 ? B : 1);
+  if (sm > 48 * 1024) cudaFuncSetAttribute(k_pack, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  k_pack<<<1, 1024, sm, s>>>(P, b0, B, best, rbase, coff, cust, dep, arr, hdr, cap_r, cap_c);
 }
 
 void launch_lf_prep(const MatCands &c, const MatDeltas &d, unsigned long long *ord, unsigned long long *key,

@@ -14,6 +14,7 @@ Each individual's trajectory is bit-identical to a separate reference call.
 from __future__ import annotations
 
 import ctypes as C
+import gc
 import time
 import weakref
 from dataclasses import dataclass
@@ -304,7 +305,15 @@ def local_search_population(sols, penalties, cfg: SearchConfig, nbr, consts, ins
     lams = [p.lam for p in penalties]
     dl = -1.0 if deadline is None else max(0.0, deadline - time.monotonic())
     replay = on_feasible is not None and not feasible_best_only
-    routes, lam, stats = search.run(sols, lams, perms, cfg, p0.kappa, p0.lam_min, p0.lam_max, dl,
-                                    snapshot_best=on_feasible is not None and feasible_best_only, trace=replay)
-    _finish(search, sols, penalties, rngs, routes, lam, stats, inst, ops, on_feasible, feasible_best_only)
+    # the write-back creates ~100 small acyclic objects per individual: keep the cyclic
+    # collector from pausing inside it (a gen-2 pass over a large heap costs ~0.2 s)
+    gc_on = gc.isenabled()
+    gc.disable()
+    try:
+        routes, lam, stats = search.run(sols, lams, perms, cfg, p0.kappa, p0.lam_min, p0.lam_max, dl,
+                                        snapshot_best=on_feasible is not None and feasible_best_only, trace=replay)
+        _finish(search, sols, penalties, rngs, routes, lam, stats, inst, ops, on_feasible, feasible_best_only)
+    finally:
+        if gc_on:
+            gc.enable()
     return stats
