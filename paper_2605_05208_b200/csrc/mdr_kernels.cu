@@ -862,6 +862,9 @@ __device__ unsigned long long g_selprof[16];
 #define SELT(i) do { } while (0)
 #endif
 template <bool WIN>
+#ifndef MDR_SWAP_SHAPE_DEFAULT
+#define MDR_SWAP_SHAPE_DEFAULT 1  // 20 warps x 96 with the u-side-outer swap: C4 +2.4 % over the pipelined 16 x 128
+#endif
 #ifndef MDR_SEL_SORT
 #define MDR_SEL_SORT 2048  // followers sorted in shared memory up to this many (else repeated block argmin)
 #endif
@@ -1430,6 +1433,14 @@ static void launch_op(const DevInst &I, const DevPop &P, const LsParams &L, cuda
   else k_eval_c<WIN, OP, CU, CT, MINB, FAM><<<gridd[dv], 32 * CU, sm, st>>>(I, P, L);
 }
 
+// swap evaluator shape (large populations): 0 pipelined 16 warps x 128 registers,
+// 1 k_eval_c 20 x 96 (default), 2 k_eval_c 24 x 80 (MDR_SWAP_SHAPE overrides)
+static int swap_shape(bool win) {
+  static int v = -2;
+  if (v == -2) v = getenv("MDR_SWAP_SHAPE") ? atoi(getenv("MDR_SWAP_SHAPE")) : -1;
+  return v >= 0 ? v : (win ? MDR_SWAP_SHAPE_DEFAULT : 0);  // without windows: pipelined 16 x 128 (C5)
+}
+
 // the staged evaluators of a population's shape (only < 0: all three, each on its stream).
 // Large shape (>= 100k customers in the population, 32 items per task), per operator,
 // measured on C4: relocate 20 warps x 96 registers (k_eval_c), swap 16 x 128 pipelined,
@@ -1457,6 +1468,10 @@ static void launch_staged_one(const DevInst &I, const DevPop &P, const LsParams 
       if (sw_split) {  // v-side segment length 1, then 2: two kernels with half the live state
         launch_op<WIN, 1, 10, MDR_LARGE_CT, 2, false, 1>(I, P, L, side[1]);
         launch_op<WIN, 1, 10, MDR_LARGE_CT, 2, false, 2>(I, P, L, side[1]);
+      } else if (swap_shape(WIN) == 1) {
+        launch_op<WIN, 1, 10, MDR_LARGE_CT, 2, false>(I, P, L, side[1]);
+      } else if (swap_shape(WIN) == 2) {
+        launch_op<WIN, 1, 8, MDR_LARGE_CT, 3, false>(I, P, L, side[1]);
       } else if (pipe_env) {
         launch_op<WIN, 1, 16, MDR_LARGE_CT, 1, true>(I, P, L, side[1]);
       } else {
