@@ -862,6 +862,15 @@ __device__ unsigned long long g_selprof[16];
 #define SELT(i) do { } while (0)
 #endif
 template <bool WIN>
+#ifndef MDR_TOS_W_MINB
+#define MDR_TOS_W_MINB 3  // 2-opt* with windows: 8-warp CTAs, this many per SM
+#endif
+#ifndef MDR_TOS_NW_SHAPE
+#define MDR_TOS_NW_SHAPE 0  // 2-opt* without windows: 0 = 16 warps x 128, 1 = 24 x 80
+#endif
+#ifndef MDR_REL_NW_SHAPE
+#define MDR_REL_NW_SHAPE 0  // relocate without windows: 0 = 20 warps x 96, 1 = 24 x 80
+#endif
 #ifndef MDR_SWAP_SHAPE_DEFAULT
 #define MDR_SWAP_SHAPE_DEFAULT 1  // 20 warps x 96 with the u-side-outer swap: C4 +2.4 % over the pipelined 16 x 128
 #endif
@@ -1459,7 +1468,8 @@ static void launch_staged_one(const DevInst &I, const DevPop &P, const LsParams 
         launch_op<WIN, 0, 8, MDR_LARGE_CT, 3, false, 1>(I, P, L, side[0]);
         launch_op<WIN, 0, 8, MDR_LARGE_CT, 3, false, 2>(I, P, L, side[0]);
       } else {
-        launch_op<WIN, 0, 10, MDR_LARGE_CT, 2, false>(I, P, L, side[0]);
+        if (MDR_REL_NW_SHAPE == 1) launch_op<WIN, 0, 8, MDR_LARGE_CT, 3, false>(I, P, L, side[0]);
+        else launch_op<WIN, 0, 10, MDR_LARGE_CT, 2, false>(I, P, L, side[0]);
       }
     }
     if (only < 0 || only == 1) {
@@ -1479,7 +1489,8 @@ static void launch_staged_one(const DevInst &I, const DevPop &P, const LsParams 
       }
     }
     if (only < 0 || only == 2) {  // 2-opt*: 24 x 80 with windows (C4 -7 %), 16 x 128 without (C5: 24 warps -24 %)
-      if (WIN) launch_op<WIN, 2, 8, MDR_LARGE_CT, 3, false>(I, P, L, side[2]);
+      if (WIN) launch_op<WIN, 2, 8, MDR_LARGE_CT, MDR_TOS_W_MINB, false>(I, P, L, side[2]);
+      else if (MDR_TOS_NW_SHAPE == 1) launch_op<WIN, 2, 8, MDR_LARGE_CT, 3, false>(I, P, L, side[2]);
       else launch_op<WIN, 2, 16, MDR_LARGE_CT, 1, false>(I, P, L, side[2]);
     }
   } else {

@@ -283,6 +283,10 @@ __device__ void srelocate(const DevInst &I, const DevPop &P, const IV &v, const 
 #define MDR_REL_SIDE_UNROLL 1  // front/back sides of a boundary item one after the other: fewer live pieces (C4 +1.5 %, C5 +3.6 % vs unrolled)
 #endif
 constexpr int kRelSideUnroll = MDR_REL_SIDE_UNROLL;
+#ifndef MDR_REL_VAR_UNROLL
+#define MDR_REL_VAR_UNROLL 3  // segment variants of a relocate item unrolled (3 = all)
+#endif
+constexpr int kRelVarUnroll = MDR_REL_VAR_UNROLL;
 struct RLU {
   int u, ru, pu, nxt;  // u < 0: out of range or not routed
 };
@@ -378,7 +382,7 @@ __device__ void srel_chunk(const DevInst &I, const DevPop &P, const IV &v, const
         S2 = a_empty<WIN>();
       }
     }
-#pragma unroll
+#pragma unroll kRelVarUnroll
     for (int vi = 0; vi < nvar; vi++) {
       const int len = vi == 0 ? 1 : 2, rev = vi == 2;
       bool ok = rv >= 0 && pu + len <= k1 && !(same && tgt > pu && tgt <= pu + len);
@@ -414,7 +418,7 @@ __device__ void srel_chunk(const DevInst &I, const DevPop &P, const IV &v, const
         S2 = I.open ? a_empty<WIN>() : a_node<WIN>(I, X2.arr);
       }
     }
-#pragma unroll
+#pragma unroll kRelVarUnroll
     for (int vi = 0; vi < nvar; vi++) {
       const int len = vi == 0 ? 1 : 2, rev = vi == 2;
       bool ok = in && pu + len <= k1 && !(same && tgt == pu + len);

@@ -1,0 +1,10 @@
+set -x
+run() { MDR_LIB=$PWD/paper_2605_05208_b200/$1 timeout 900 python bench.py --config $2 --pop $3 --steps 3 --warmup 2 --no-cpu-baseline --no-numpy-ref --no-e2e --no-repair > gpurun_out/r3_${1%.so}_$2_$4.jsonl 2> gpurun_out/r3_${1%.so}_$2_$4.err; }
+for rep in a b; do
+  for L in libmdr_sm100.so libmdr_var1.so libmdr_side2.so; do run $L C4 256 $rep; done
+done
+for L in libmdr_sm100.so libmdr_var1.so libmdr_side2.so; do run $L C5 128 a; done
+for f in gpurun_out/r3_*.jsonl; do python -c "
+import json
+d=json.loads(open('$f').read().strip().splitlines()[-1]); pr=d['profile']
+print('$f'.split('/')[-1], round(d['value']/1e9,3), 'G/s', round(d['ms_per_step'],1), 'ms', {k: round(v,1) for k,v in pr['evaluators_ms'].items()})"; done
