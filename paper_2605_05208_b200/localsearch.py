@@ -299,17 +299,17 @@ def local_search_population(sols, penalties, cfg: SearchConfig, nbr, consts, ins
     for p in penalties[1:]:  # one device launch carries one (kappa, lam_min, lam_max)
         if (p.kappa, p.lam_min, p.lam_max) != (p0.kappa, p0.lam_min, p0.lam_max):
             raise ValueError("local_search_population: all penalty states must share kappa, lam_min and lam_max")
-    search = _searcher(inst, consts, nbr, device)
-    ops = enabled_operators(inst)
-    perms = np.stack([draw_permutations(r, ops, cfg.depth + 1) for r in rngs])
-    lams = [p.lam for p in penalties]
-    dl = -1.0 if deadline is None else max(0.0, deadline - time.monotonic())
-    replay = on_feasible is not None and not feasible_best_only
-    # the write-back creates ~100 small acyclic objects per individual: keep the cyclic
-    # collector from pausing inside it (a gen-2 pass over a large heap costs ~0.2 s)
+    # the call creates ~100 small acyclic objects per individual: keep the cyclic collector
+    # from pausing inside it (a gen-2 pass over a large heap costs up to ~1 s)
     gc_on = gc.isenabled()
     gc.disable()
     try:
+        search = _searcher(inst, consts, nbr, device)
+        ops = enabled_operators(inst)
+        perms = np.stack([draw_permutations(r, ops, cfg.depth + 1) for r in rngs])
+        lams = [p.lam for p in penalties]
+        dl = -1.0 if deadline is None else max(0.0, deadline - time.monotonic())
+        replay = on_feasible is not None and not feasible_best_only
         routes, lam, stats = search.run(sols, lams, perms, cfg, p0.kappa, p0.lam_min, p0.lam_max, dl,
                                         snapshot_best=on_feasible is not None and feasible_best_only, trace=replay)
         _finish(search, sols, penalties, rngs, routes, lam, stats, inst, ops, on_feasible, feasible_best_only)

@@ -105,10 +105,14 @@ def _oracle_kernels(setattr_):
 
     setattr_(E, "initialize_population", init_pop)
 
+    from oracle import exchange_ref as XR
+
     def exchange_batch(population, inst, bandit, rngs, device=0):  # the host exchange, one rng per offspring
-        return [GN.route_exchange(population, inst, bandit, r) for r in rngs]
+        return [XR.route_exchange(population, inst, bandit, r) for r in rngs]
 
     setattr_(E, "route_exchange_batch", exchange_batch)
+    setattr_(GN, "route_exchange", lambda population, inst, bandit, rng, main_index=None, device=0:
+             XR.route_exchange(population, inst, bandit, rng, main_index))
 
     class _HostPop:  # breakdowns of the last oracle batch, by the host evaluate
         sols = []
@@ -242,6 +246,7 @@ def test_device_route_exchange_equals_host(variant, nc, nd, open_):
     """route_exchange_batch (mdr_route_exchange, one CTA per offspring) == the host
     route_exchange (genetic.py:343-446 restated) for every offspring, with each
     rng advanced identically; populations with duplicate members and all levels."""
+    from oracle import exchange_ref as XR
     inst = W.make_instance(random.Random(nc), variant, n_customers=nc, n_depots=nd)
     pop = [W.random_solution(random.Random(900 + i), inst) for i in range(9)]
     pop.append(pop[3].clone())  # a duplicate member
@@ -254,12 +259,12 @@ def test_device_route_exchange_equals_host(variant, nc, nd, open_):
         got = GN.route_exchange_batch(pop, inst, bandit, [random.Random(s) for s in seeds])
         for s, (off, unr, lv, sig, mi) in zip(seeds, got):
             r = random.Random(s)
-            w_off, w_unr, w_lv, w_sig, w_mi = GN.route_exchange(pop, inst, bandit, r)
+            w_off, w_unr, w_lv, w_sig, w_mi = XR.route_exchange(pop, inst, bandit, r)
             assert (mi, lv, sig, unr) == (w_mi, w_lv, w_sig, w_unr)
             assert _routes(off) == _routes(w_off)
         rs = [random.Random(s) for s in seeds]
         GN.route_exchange_batch(pop, inst, bandit, rs)
         for s, r in zip(seeds, rs):
             w = random.Random(s)
-            GN.route_exchange(pop, inst, bandit, w)
+            XR.route_exchange(pop, inst, bandit, w)
             assert r.getstate() == w.getstate()

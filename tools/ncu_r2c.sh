@@ -12,7 +12,7 @@ for CFG in C4 C5; do
   python tools/ncu_roofline.py $CFG /tmp/prof3_$CFG.ncu-rep "k_eval_c<$W, 0, \d+, 32, \d+, 1>" relocate_granular > /dev/null
   python tools/ncu_roofline.py $CFG /tmp/prof3_$CFG.ncu-rep "k_eval_c<$W, 0, \d+, 32, \d+, 2>" relocate_boundary > /dev/null
   python tools/ncu_roofline.py $CFG /tmp/prof3_$CFG.ncu-rep "k_eval_c<$W, 0, \d+, 32, \d+, 0>" relocate > /dev/null
-  python tools/ncu_roofline.py $CFG /tmp/prof3_$CFG.ncu-rep "k_eval_p<$W, 1, " swap > /dev/null
+  python tools/ncu_roofline.py $CFG /tmp/prof3_$CFG.ncu-rep "k_eval_[cp]<$W, 1, " swap > /dev/null
   python tools/ncu_roofline.py $CFG /tmp/prof3_$CFG.ncu-rep "k_eval_c<$W, 2, " two_opt_star > /dev/null
   python tools/ncu_summary.py /tmp/prof3_$CFG.ncu-rep > gpurun_out/r2_ncu_${CFG}_summary.txt 2>&1
   ncu -i /tmp/prof3_$CFG.ncu-rep --page raw --csv --metrics gpu__time_duration.sum,sm__inst_issued.avg.pct_of_peak_sustained_active,l1tex__throughput.avg.pct_of_peak_sustained_active,sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active,launch__registers_per_thread > gpurun_out/r2_ncu_${CFG}_kernels.csv 2>&1
