@@ -76,6 +76,8 @@ struct mdr_pop {
   double *rp_fold = nullptr;
   int *rp_foldi = nullptr;
   double *bd_rt = nullptr, *bd_io = nullptr;  // mdr_pop_breakdown scratch
+  double *ra_buf = nullptr;                    // mdr_pop_route_attrs output (kept: a per-call
+  size_t ra_cap = 0;                           // cudaMalloc/cudaFree cost up to ~0.4 s at times)
   unsigned long long *tr_buf = nullptr;        // accepted-step trace (cfg.trace)
   long long *tr_cnt = nullptr;
   size_t tr_cap[2] = {0, 0};
@@ -347,6 +349,7 @@ void mdr_pop_destroy(mdr_pop *p) {
   for (int q = 0; q < 4; q++)
     if (p->fev[q]) cudaEventDestroy(p->fev[q]);
   if (p->tr_buf) cudaFree(p->tr_buf);
+  if (p->ra_buf) cudaFree(p->ra_buf);
   if (p->tr_cnt) cudaFree(p->tr_cnt);
   for (void *q : {(void *)p->rp_pre, (void *)p->rp_suf, (void *)p->rp_c1, (void *)p->rp_c2, (void *)p->rp_p1, (void *)p->rp_pend,
                   (void *)p->rp_status, (void *)p->rp_stats, (void *)p->rp_fold, (void *)p->rp_foldi,
@@ -1216,18 +1219,13 @@ int mdr_pop_route_attrs(mdr_pop *p, int32_t b0, int32_t nb, double *out, void *s
   cudaStream_t s = (cudaStream_t)stream;
   CK(cudaSetDevice(p->inst->device));
   const size_t n = (size_t)nb * p->P.J * 6;
-  double *d = nullptr;
-  CK(cudaMalloc(&d, sizeof(double) * n));
-  auto run = [&]() -> int {
-    launch_route_attrs(p->inst->I, p->P, b0, nb, d, s);
-    CK(cudaGetLastError());
-    CK(cudaMemcpyAsync(out, d, sizeof(double) * n, cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-    return MDR_OK;
-  };
-  const int rc = run();
-  cudaFree(d);
-  return rc;
+  int rc;
+  if ((rc = regrow(&p->ra_buf, p->ra_cap, n))) return rc;
+  launch_route_attrs(p->inst->I, p->P, b0, nb, p->ra_buf, s);
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(out, p->ra_buf, sizeof(double) * n, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  return MDR_OK;
 }
 
 int mdr_pop_trace(mdr_pop *p, int32_t b, uint64_t *out, int64_t cap, int64_t *n) {
@@ -1271,7 +1269,7 @@ int mdr_route_exchange(mdr_instance *inst, int32_t M, const int32_t *mroute, con
   std::vector<void *> tmp;
   auto dmal = [&](size_t bytes) -> void * {
     void *q = nullptr;
-    if (cudaMalloc(&q, bytes ? bytes : 1) != cudaSuccess) return nullptr;
+    if (cudaMallocAsync(&q, bytes ? bytes : 1, 0) != cudaSuccess) return nullptr;  // pool: no device sync
     tmp.push_back(q);
     return q;
   };
@@ -1332,7 +1330,7 @@ int mdr_route_exchange(mdr_instance *inst, int32_t M, const int32_t *mroute, con
     return MDR_OK;
   };
   rc = run();
-  for (void *t : tmp) cudaFree(t);
+  for (void *t : tmp) cudaFreeAsync(t, 0);
   return rc;
 }
 
@@ -1352,10 +1350,10 @@ int mdr_route_sim(mdr_instance *inst, int32_t n_routes, const int32_t *off, cons
   double *d_raw = nullptr, *d_out = nullptr;
   int rc = MDR_OK;
   auto run = [&]() -> int {
-    CK(cudaMalloc(&d_off, sizeof(int) * (n_routes + 1)));
-    CK(cudaMalloc(&d_seq, sizeof(int) * ns));
-    CK(cudaMalloc(&d_raw, sizeof(double) * ns));
-    CK(cudaMalloc(&d_out, sizeof(double) * 6 * n_routes));
+    CK(cudaMallocAsync(&d_off, sizeof(int) * (n_routes + 1), 0));
+    CK(cudaMallocAsync(&d_seq, sizeof(int) * ns, 0));
+    CK(cudaMallocAsync(&d_raw, sizeof(double) * ns, 0));
+    CK(cudaMallocAsync(&d_out, sizeof(double) * 6 * n_routes, 0));
     CK(cudaMemcpy(d_off, off, sizeof(int) * (n_routes + 1), cudaMemcpyHostToDevice));
     CK(cudaMemcpy(d_seq, seq, sizeof(int) * ns, cudaMemcpyHostToDevice));
     launch_route_sim(I, n_routes, d_off, d_seq, want_min, d_raw, d_out, 0);
@@ -1364,10 +1362,10 @@ int mdr_route_sim(mdr_instance *inst, int32_t n_routes, const int32_t *off, cons
     return MDR_OK;
   };
   rc = run();
-  cudaFree(d_off);
-  cudaFree(d_seq);
-  cudaFree(d_raw);
-  cudaFree(d_out);
+  if (d_off) cudaFreeAsync(d_off, 0);
+  if (d_seq) cudaFreeAsync(d_seq, 0);
+  if (d_raw) cudaFreeAsync(d_raw, 0);
+  if (d_out) cudaFreeAsync(d_out, 0);
   return rc;
 }
 

@@ -191,20 +191,20 @@ extern "C" int mdr_population_select(int32_t device, int32_t n, int32_t row0, co
   int rc = MDR_ERR_CUDA;
   const int nrem = n > mu ? n - mu : 0;
   do {
-    if (cudaMalloc(&d_off, sizeof(long long) * (n + 1)) != cudaSuccess) break;
-    if (cudaMalloc(&d_keys, sizeof(long long) * (nk > 0 ? nk : 1)) != cudaSuccess) break;
-    if (cudaMalloc(&d_dist, sizeof(double) * nn) != cudaSuccess) break;
+    if (cudaMallocAsync(&d_off, sizeof(long long) * (n + 1), 0) != cudaSuccess) break;
+    if (cudaMallocAsync(&d_keys, sizeof(long long) * (nk > 0 ? nk : 1), 0) != cudaSuccess) break;
+    if (cudaMallocAsync(&d_dist, sizeof(double) * nn, 0) != cudaSuccess) break;
     if (cudaMemcpy(d_off, edge_off, sizeof(long long) * (n + 1), cudaMemcpyHostToDevice) != cudaSuccess) break;
     if (nk > 0 && cudaMemcpy(d_keys, edge_keys, sizeof(long long) * nk, cudaMemcpyHostToDevice) != cudaSuccess) break;
     if (cudaMemcpy(d_dist, dist, sizeof(double) * nn, cudaMemcpyHostToDevice) != cudaSuccess) break;
     mdr::launch_edge_dist(n, row0, d_off, d_keys, d_dist, 0);
     if (cudaGetLastError() != cudaSuccess) break;
     if (nrem) {
-      if (cudaMalloc(&d_cost, sizeof(double) * n) != cudaSuccess) break;
-      if (cudaMalloc(&d_birth, sizeof(long long) * n) != cudaSuccess) break;
-      if (cudaMalloc(&d_div, sizeof(double) * n) != cudaSuccess) break;
-      if (cudaMalloc(&d_alive, n) != cudaSuccess) break;
-      if (cudaMalloc(&d_rem, sizeof(int) * nrem) != cudaSuccess) break;
+      if (cudaMallocAsync(&d_cost, sizeof(double) * n, 0) != cudaSuccess) break;
+      if (cudaMallocAsync(&d_birth, sizeof(long long) * n, 0) != cudaSuccess) break;
+      if (cudaMallocAsync(&d_div, sizeof(double) * n, 0) != cudaSuccess) break;
+      if (cudaMallocAsync(&d_alive, n, 0) != cudaSuccess) break;
+      if (cudaMallocAsync(&d_rem, sizeof(int) * nrem, 0) != cudaSuccess) break;
       if (cudaMemcpy(d_cost, cost, sizeof(double) * n, cudaMemcpyHostToDevice) != cudaSuccess) break;
       if (cudaMemcpy(d_birth, birth, sizeof(long long) * n, cudaMemcpyHostToDevice) != cudaSuccess) break;
       mdr::launch_survivors(n, mu, xi, d_dist, d_cost, d_birth, d_alive, d_div, d_rem, 0);
@@ -214,13 +214,13 @@ extern "C" int mdr_population_select(int32_t device, int32_t n, int32_t row0, co
     if (cudaMemcpy(dist, d_dist, sizeof(double) * nn, cudaMemcpyDeviceToHost) != cudaSuccess) break;
     rc = MDR_OK;
   } while (0);
-  cudaFree(d_off);
-  cudaFree(d_keys);
-  cudaFree(d_dist);
-  cudaFree(d_cost);
-  cudaFree(d_birth);
-  cudaFree(d_div);
-  cudaFree(d_alive);
-  cudaFree(d_rem);
+  if (d_off) cudaFreeAsync(d_off, 0);
+  if (d_keys) cudaFreeAsync(d_keys, 0);
+  if (d_dist) cudaFreeAsync(d_dist, 0);
+  if (d_cost) cudaFreeAsync(d_cost, 0);
+  if (d_birth) cudaFreeAsync(d_birth, 0);
+  if (d_div) cudaFreeAsync(d_div, 0);
+  if (d_alive) cudaFreeAsync(d_alive, 0);
+  if (d_rem) cudaFreeAsync(d_rem, 0);
   return rc == MDR_OK ? rc : mdr::mdr_fail(rc, "mdr_population_select: CUDA error");
 }
