@@ -510,10 +510,12 @@ def main():
     rounds = pop.timing()["rounds"] - rounds0
     # the timed individuals' final states (checked against the oracle below)
     final_routes = [pop.download_range(b, 1, sh)[0] for b in range(min(per, os.cpu_count() or 1))]
-    # per round: plan, 3 staged evaluators, the depot (+ 2-opt without windows) enumerators,
+    # per round: plan, the staged evaluators (relocate as two family kernels on windowed
+    # instances with the large shape), the depot (+ 2-opt without windows) enumerators,
     # 3 generic-path drains (one per queue region), select; per step: unpack + rebuild
     n_enum = 2 if inst.has_windows else 3
-    launches = rounds * (1 + 3 + n_enum + 3 + 1) + 2 * args.steps
+    n_staged = 4 if (inst.has_windows and pop.info()["items_per_task"] == 32) else 3
+    launches = rounds * (1 + n_staged + n_enum + 3 + 1) + 2 * args.steps
 
     # profiled pass (untimed; evaluation phase serialised): per-evaluator times,
     # eval-kernel share, per-op candidates

@@ -590,6 +590,9 @@ __device__ __forceinline__ void sswap_stage(const DevInst &I, const IV &v, const
 }
 
 // one 32-item chunk of the task's (customer, slot) space; full-warp call
+#ifndef MDR_SWAP_YOUTER_NW
+#define MDR_SWAP_YOUTER_NW 0  // u-side-outer swap also without windows (measured slower at C5)
+#endif
 // XF: which v-side segments this call evaluates -- 0 all, 1 length 1 only, 2 length 2 only
 // (the swap evaluator can run as two kernels, each with half the live state)
 template <bool WIN, int CT, int XF = 0>
@@ -623,7 +626,7 @@ __device__ void sswap_chunk(const DevInst &I, const DevPop &P, const IV &v, cons
   int k2 = 0, n2 = 0, nxtv = vv;
   At<WIN> P2;
   At<WIN> Y[NV];
-if constexpr (CT >= 32 && WIN) {  // large shape with windows: u-side variant outer (C4 swap -4.5 % at 20 warps x 96)
+if constexpr (CT >= 32 && (WIN || MDR_SWAP_YOUTER_NW)) {  // large shape with windows: u-side variant outer (C4 swap -4.5 % at 20 warps x 96)
   // u-side variant outer, v-side inner: only one donor-side prefix Y is live; the v-side
   // piece X and suffix S2 are re-formed per u-side variant (more work, fewer registers)
   if (inter) {
