@@ -66,8 +66,8 @@ struct mdr_pop {
   std::vector<cudaEvent_t> kev;  // per-round per-evaluator events when profiling (7 per round)
   cudaStream_t ls;               // private stream of the round loop (graph capture)
   cudaEvent_t join[2];
-  cudaStream_t side[3];          // fork/join branches of the per-operator evaluators
-  cudaEvent_t fev[4];
+  cudaStream_t side[4];          // fork/join branches of the per-operator evaluators ([3]: relocate boundary family)
+  cudaEvent_t fev[6];
   // repair scratch (mdr_repair), grown on demand
   char *rp_pre = nullptr, *rp_suf = nullptr;
   double *rp_c1 = nullptr, *rp_c2 = nullptr;
@@ -325,8 +325,8 @@ static int pop_build(mdr_pop *p, mdr_instance *inst, int32_t Bcap, int32_t J, in
   CK(cudaStreamCreateWithFlags(&p->ls, cudaStreamNonBlocking));
   CK(cudaEventCreateWithFlags(&p->join[0], cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&p->join[1], cudaEventDisableTiming));
-  for (int q = 0; q < 3; q++) CK(cudaStreamCreateWithFlags(&p->side[q], cudaStreamNonBlocking));
-  for (int q = 0; q < 4; q++) CK(cudaEventCreateWithFlags(&p->fev[q], cudaEventDisableTiming));
+  for (int q = 0; q < 4; q++) CK(cudaStreamCreateWithFlags(&p->side[q], cudaStreamNonBlocking));
+  for (int q = 0; q < 6; q++) CK(cudaEventCreateWithFlags(&p->fev[q], cudaEventDisableTiming));
   return MDR_OK;
 }
 
@@ -344,9 +344,9 @@ void mdr_pop_destroy(mdr_pop *p) {
   if (p->ls) cudaStreamDestroy(p->ls);
   for (int q = 0; q < 2; q++)
     if (p->join[q]) cudaEventDestroy(p->join[q]);
-  for (int q = 0; q < 3; q++)
-    if (p->side[q]) cudaStreamDestroy(p->side[q]);
   for (int q = 0; q < 4; q++)
+    if (p->side[q]) cudaStreamDestroy(p->side[q]);
+  for (int q = 0; q < 6; q++)
     if (p->fev[q]) cudaEventDestroy(p->fev[q]);
   if (p->tr_buf) cudaFree(p->tr_buf);
   if (p->ra_buf) cudaFree(p->ra_buf);

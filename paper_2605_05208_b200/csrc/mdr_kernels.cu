@@ -1455,7 +1455,8 @@ static int swap_shape(bool win) {
 // measured on C4: relocate 20 warps x 96 registers (k_eval_c), swap 16 x 128 pipelined,
 // 2-opt* 24 x 80; small shape: 8 warps x 8 items, 2 CTAs per SM.
 template <bool WIN>
-static void launch_staged_one(const DevInst &I, const DevPop &P, const LsParams &L, const cudaStream_t *side, int only) {
+static void launch_staged_one(const DevInst &I, const DevPop &P, const LsParams &L, const cudaStream_t *side, int only,
+                              bool rel_branch = false) {
   static int pipe_env = -1;
   if (pipe_env < 0) pipe_env = getenv("MDR_NO_PIPE") ? 0 : 1;
   if (P.ct == MDR_LARGE_CT) {
@@ -1466,7 +1467,9 @@ static void launch_staged_one(const DevInst &I, const DevPop &P, const LsParams 
       if (split < 0) split = getenv("MDR_REL_SPLIT") ? atoi(getenv("MDR_REL_SPLIT")) : 1;
       if (split && WIN) {
         launch_op<WIN, 0, 8, MDR_LARGE_CT, 3, false, 1>(I, P, L, side[0]);
-        launch_op<WIN, 0, 8, MDR_LARGE_CT, 3, false, 2>(I, P, L, side[0]);
+        // the boundary family on its own branch when the caller gave one (side[3]; joined
+        // into side[0] before the intra-route drain), else behind the granular one
+        launch_op<WIN, 0, 8, MDR_LARGE_CT, 3, false, 2>(I, P, L, only < 0 && rel_branch ? side[3] : side[0]);
       } else {
         if (MDR_REL_NW_SHAPE == 1) launch_op<WIN, 0, 8, MDR_LARGE_CT, 3, false>(I, P, L, side[0]);
         else launch_op<WIN, 0, 10, MDR_LARGE_CT, 2, false>(I, P, L, side[0]);
@@ -1534,8 +1537,13 @@ static void launch_eval_t(const DevInst &I, const DevPop &P, const LsParams &L, 
     // relocate / swap / 2-opt* as parallel branches (fork/join): their
     // persistent grids back-fill each other's tails
     cudaEventRecord(ev[0], s);
-    for (int q = 0; q < 3; q++) cudaStreamWaitEvent(side[q], ev[0], 0);
-    launch_staged_one<WIN>(I, P, L, side, -1);
+    for (int q = 0; q < 4; q++) cudaStreamWaitEvent(side[q], ev[0], 0);
+    static int rel_branch = -1;
+    if (rel_branch < 0) rel_branch = getenv("MDR_REL_NOBRANCH") ? 0 : 1;
+    launch_staged_one<WIN>(I, P, L, side, -1, rel_branch != 0);
+    // relocate's boundary family ran on side[3]: join it into side[0] (its drain follows)
+    cudaEventRecord(ev[4], side[3]);
+    cudaStreamWaitEvent(side[0], ev[4], 0);
     const bool ov0 = P.gbase[1] > 0;
     if (ov0) {  // each producer's intra-route queue drained right behind it, on its branch
       launch_eval_g_region<WIN>(I, P, L, side[0], 1);
