@@ -73,6 +73,7 @@ struct DevPop {
   int Bcap, J, K, Kp, Fcap, FE;
   int staged;  // relocate/swap/2-opt* use the CTA-staged evaluators (mdr_staged.cuh)
   int ct;      // items per CTA task of the staged evaluators (MDR_SMALL_CT / MDR_LARGE_CT)
+  int tsplit;  // sub-tasks per customer block (relocate boundary family, flattened swap): 1, 2 or 4
   int N, ND;
   int *m;
   int4 *rmeta;

@@ -380,7 +380,10 @@ __global__ void __launch_bounds__(32 * CU, MINB) k_eval_c(DevInst I, DevPop P, L
   __shared__ int s_t, s_b, s_lo, s_hi, s_next, s_end;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   double *U = s_u[wid];
-  const int total = P.optasks[OP];
+  // small populations: the relocate boundary family and the flattened swap split each
+  // customer-block task into SPL sub-tasks (contiguous chunk ranges) for more CTAs per round
+  const int SPL = ((OP == 0 && FAM == 2) || (OP == 1 && FLAT)) ? P.tsplit : 1;
+  const int total = P.optasks[OP] * SPL;
   const int cnt = P.opcnt[OP];
   const int *OFF = P.opoff + OP * (P.Bcap + 1);
   const int *OB = P.opb + OP * P.Bcap;
@@ -401,11 +404,12 @@ __global__ void __launch_bounds__(32 * CU, MINB) k_eval_c(DevInst I, DevPop P, L
       int t = s_next < s_end ? s_next++ : total;
       s_t = t;
       s_item = 0;
-      if (t < total && (t < s_lo || t >= s_hi)) {
+      const int tb = t / SPL;  // the customer-block task
+      if (t < total && (tb < s_lo || tb >= s_hi)) {
         int l2 = 0, h2 = cnt - 1;
         while (l2 < h2) {
           int mid = (l2 + h2 + 1) >> 1;
-          if (OFF[mid] <= t) l2 = mid; else h2 = mid - 1;
+          if (OFF[mid] <= tb) l2 = mid; else h2 = mid - 1;
         }
         s_b = OB[l2];
         s_lo = OFF[l2];
@@ -415,7 +419,7 @@ __global__ void __launch_bounds__(32 * CU, MINB) k_eval_c(DevInst I, DevPop P, L
     __syncthreads();
     const int t = s_t;
     if (t >= total) break;
-    const int b = s_b, local = t - s_lo;
+    const int b = s_b, local = t / SPL - s_lo, sub = t - (t / SPL) * SPL;
     const IV v = make_iv(P, b);
     if (b != staged) {
       stage_routes<WIN>(I, v, R);
@@ -438,12 +442,16 @@ __global__ void __launch_bounds__(32 * CU, MINB) k_eval_c(DevInst I, DevPop P, L
     Acc acc{~0ull, ~0ull, 0};
     const int ngc = (CT * I.W + 31) / 32;
     const int ngb = (CT * v.M + 31) / 32;
-    const int nit = FLAT ? ngc : FLATR ? (FAM == 1 ? ngc : FAM == 2 ? ngb : ngc + ngb) : CT;
+    const int nall = FLAT ? ngc : FLATR ? (FAM == 1 ? ngc : FAM == 2 ? ngb : ngc + ngb) : CT;
+    // sub-task `sub` of SPL owns chunks [c0, c1) of the customer-block task
+    const int c0 = (int)((long long)nall * sub / SPL), c1 = (int)((long long)nall * (sub + 1) / SPL);
+    const int nit = c1 - c0;
     for (;;) {  // warps take the task's items dynamically
       int it = 0;
       if (lane == 0) it = atomicAdd(&s_item, 1);
       it = __shfl_sync(0xffffffffu, it, 0);
       if (it >= nit) break;
+      it += c0;
       if (FLATR) {
         if (FAM == 1) srel_chunk<WIN, CT>(I, P, v, R, b, it, false, s_rl, s_rld, lam, mm, acc);
         else if (FAM == 2) srel_chunk<WIN, CT>(I, P, v, R, b, it, true, s_rl, s_rld, lam, mm, acc);

@@ -1,6 +1,6 @@
 # source-level look at the relocate boundary kernel (summarised on the box)
 CMD="python bench.py --config C4 --steps 1 --warmup 0 --no-cpu-baseline --no-numpy-ref --no-e2e --no-repair"
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:"k_eval_c<1, 0, 8, 32, 3, 2>" -s 100 -c 1 -o /tmp/prof_bnd $CMD > gpurun_out/ncu_bnd.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:"k_eval_c<[^,]*1, [^,]*0, [^,]*8, [^,]*32, [^,]*3, [^,]*2>" -s 100 -c 1 -o /tmp/prof_bnd $CMD > gpurun_out/ncu_bnd.log 2>&1
 echo rc=$?
 python tools/ncu_lines.py /tmp/prof_bnd.ncu-rep 0 60 > gpurun_out/bnd_lines.txt 2>&1
 python tools/ncu_summary.py /tmp/prof_bnd.ncu-rep > gpurun_out/bnd_summary.txt 2>&1
