@@ -739,7 +739,7 @@ int mdr_leader_followers(mdr_pop *p, const mdr_cands *cs, const mdr_deltas *d, i
     TA(k2, n);
     size_t t2 = 0;
     CK(cub::DeviceSelect::Flagged(nullptr, t2, cnt, flag, fidx, nsel, (int)n, s));
-    void *ts2 = nullptr;
+    char *ts2 = nullptr;
     TA(ts2, t2 + 1);
     CK(cub::DeviceSelect::Flagged(ts2, t2, cnt, flag, fidx, nsel, (int)n, s));
     int nf = 0;
@@ -751,7 +751,7 @@ int mdr_leader_followers(mdr_pop *p, const mdr_cands *cs, const mdr_deltas *d, i
       k_gather_u64<<<gb, 256, 0, s>>>(key, fidx, k1, nf);
       size_t t3 = 0;
       CK(cub::DeviceRadixSort::SortPairs(nullptr, t3, k1, k2, fidx, fidx2, nf, 0, 64, s));
-      void *ts3 = nullptr;
+      char *ts3 = nullptr;
       TA(ts3, t3 + 1);
       CK(cub::DeviceRadixSort::SortPairs(ts3, t3, k1, k2, fidx, fidx2, nf, 0, 58, s));
       k_gather_u64<<<gb, 256, 0, s>>>(ord, fidx2, k1, nf);

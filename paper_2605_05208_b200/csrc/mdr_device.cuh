@@ -301,28 +301,20 @@ __device__ __forceinline__ void tab_store_at(double *p, const At<WIN> &a) {
 template <bool WIN>
 __device__ __forceinline__ At<WIN> gat(const DevInst &I, const DevPop &P, int b, int r, int i, int j, int n) {
   if (j < i) return a_empty<WIN>();
-  const int *sq = P.seq + row_base(P, b, r);
+  const size_t rb = row_base(P, b, r);
+  const int *sq = P.seq + rb;
+  // one load sequence from a selected source (no divergent per-table branches)
+  const double *src = i == 0 ? P.tabP + (rb + j) * P.FE
+                             : (j == n - 1 ? P.tabS + (rb + i) * P.FE : P.tabT + ((rb + i) * P.Kp + j) * P.FE);
+  const double2 *e = reinterpret_cast<const double2 *>(src);
   At<WIN> a;
-  if (i == 0) {
-    a = tab_load<WIN>(P, P.tabP, b, r, j);
-    a.first = __ldg(sq); a.last = __ldg(sq + j);
-    return a;
-  }
-  if (j == n - 1) {
-    a = tab_load<WIN>(P, P.tabS, b, r, i);
-    a.first = __ldg(sq + i); a.last = __ldg(sq + j);
-    return a;
-  }
-  {
-    const double2 *e = reinterpret_cast<const double2 *>(P.tabT + ((row_base(P, b, r) + i) * P.Kp + j) * P.FE);
-    double2 x = __ldg(e), y = __ldg(e + 1);
-    a.dist = x.x; a.load = x.y; a.T = y.x;
-    if (WIN) {
-      double2 z = __ldg(e + 2);
-      a.E = y.y; a.L = z.x; a.TW = z.y;
-    } else {
-      a.E = 0.0; a.L = 0.0; a.TW = 0.0;
-    }
+  double2 x = __ldg(e), y = __ldg(e + 1);
+  a.dist = x.x; a.load = x.y; a.T = y.x;
+  if (WIN) {
+    double2 z = __ldg(e + 2);
+    a.E = y.y; a.L = z.x; a.TW = z.y;
+  } else {
+    a.E = 0.0; a.L = 0.0; a.TW = 0.0;
   }
   a.first = __ldg(sq + i); a.last = __ldg(sq + j);
   return a;
@@ -397,9 +389,13 @@ struct Delta {
   int fn;
 };
 
-// evaluate_candidates (batch.py:365-553) for one candidate of individual b
-template <bool WIN>
-__device__ Delta eval_cand(const DevInst &I, const DevPop &P, int b, int op, const Cand &c, const double lam[4]) {
+// evaluate_candidates (batch.py:365-553) for one candidate of individual b.
+// FOP >= 0 fixes the operator and SAME the same-route case at compile time
+// (the intra-route queue regions), so only that branch is generated.
+template <bool WIN, int FOP = -1, bool SAME = false>
+__device__ __forceinline__ Delta eval_cand(const DevInst &I, const DevPop &P, int b, int op, const Cand &c,
+                                           const double lam[4]) {
+  if (FOP >= 0) op = FOP;
   double nw[5], cA[5], cB[5];
   double fleet_delta = 0.0;
   int fn = 1, two = 0;
@@ -412,7 +408,7 @@ __device__ Delta eval_cand(const DevInst &I, const DevPop &P, int b, int op, con
     case 0: {  // RELOCATE batch.py:391-428
       At<WIN> seg = gat<WIN>(I, P, b, r1, p1 + 1, p1 + l1, n1);
       if (c.rev1) swap_ends(seg);
-      if (r1 == r2) {
+      if (SAME || r1 == r2) {
         bool before = p2 <= p1;
         At<WIN> x = gat<WIN>(I, P, b, r1, 0, before ? p2 : p1, n1);
         At<WIN> mid = before ? gat<WIN>(I, P, b, r1, p2 + 1, p1, n1) : gat<WIN>(I, P, b, r1, p1 + l1 + 1, p2, n1);
@@ -439,7 +435,7 @@ __device__ Delta eval_cand(const DevInst &I, const DevPop &P, int b, int op, con
     case 1: {  // SWAP batch.py:430-463
       At<WIN> segA = gat<WIN>(I, P, b, r1, p1 + 1, p1 + l1, n1);
       if (c.rev1) swap_ends(segA);
-      if (r1 == r2) {
+      if (SAME || r1 == r2) {
         At<WIN> segB = gat<WIN>(I, P, b, r1, p2 + 1, p2 + l2, n1);
         if (c.rev2) swap_ends(segB);
         At<WIN> x = a_cat<WIN>(I, gat<WIN>(I, P, b, r1, 0, p1, n1), segB);

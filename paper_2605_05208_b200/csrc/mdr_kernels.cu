@@ -113,43 +113,187 @@ __device__ double pw_sum(const double4 *a, int f, int n) {
   }
 }
 
-// per-route part (warp per route): SolutionIndex entries of its customers,
-// prefix/suffix tables (lane i folds positions i..n-1 -- the left fold from i
-// of batch.py:99-124), route terms and closure flag.  list == nullptr: all m.
+// per-route part: SolutionIndex entries of its customers (warp per route),
+// prefix/suffix tables (the left fold from i of batch.py:99-124) and route
+// terms.  The folds run on a group of G lanes per route, each lane folding the
+// row pair (i, n-1-i) -- n+1 steps per lane -- so a warp rebuilds 32/G routes
+// at once.  list == nullptr: all m.
 template <bool WIN>
-__device__ void rebuild_routes(const DevInst &I, const DevPop &P, int b, const int *list, int cnt) {
+__device__ __forceinline__ void fold_row(const DevInst &I, const DevPop &P, int b, int r, const int *sq, int i, int n,
+                                         int4 mt) {
+  At<WIN> acc = a_node<WIN>(I, sq[i]);
+  double *trow = P.tabT + (row_base(P, b, r) + i) * P.Kp * P.FE;  // T[r][i][*]
+  if (i == 0) tab_store<WIN>(P, P.tabP, b, r, 0, acc);
+  tab_store_at<WIN>(trow + i * P.FE, acc);
+  for (int j = i + 1; j < n; j++) {
+    acc = a_cat_ne<WIN>(I, acc, a_node<WIN>(I, sq[j]));
+    if (i == 0) tab_store<WIN>(P, P.tabP, b, r, j, acc);
+    tab_store_at<WIN>(trow + j * P.FE, acc);
+  }
+  tab_store<WIN>(P, P.tabS, b, r, i, acc);
+  if (i == 0) {
+    double o[5];
+    contrib<WIN>(I, acc, mt.y, mt.z, mt.x, o);
+    P.rcon[(size_t)b * P.J + r] = make_double4(acc.dist, o[1], o[2], o[3]);  // route_D is the raw table value
+    P.rmeta[(size_t)b * P.J + r].w = (int)o[4];
+  }
+}
+
+#ifdef MDR_SEL_PROF
+__device__ unsigned long long g_selprof[16];
+#define RBT_(i) do { if (threadIdx.x == 0) { long long t__ = clock64(); atomicAdd(&g_selprof[i], (unsigned long long)(t__ - t_rb)); t_rb = t__; } } while (0)
+#else
+#define RBT_(i) do { } while (0)
+#endif
+#ifndef MDR_RB_STAGED
+#define MDR_RB_STAGED 1  // 0: a warp per route, a lane per row, node/link reads from global memory
+#endif
+constexpr int kRbGroup = 8;                 // lanes per route in the staged folds
+constexpr size_t kRbStageBytes = 32 * 1024;  // staged positions (>= one route of 502 positions)
+
+// route positions staged in shared memory (structure of arrays): the node
+// attributes and the link from the previous position, so the folds' serial
+// steps read nothing from global memory
+template <bool WIN>
+struct RbStage {
+  double *load, *T, *E, *L, *c, *t;
+  int *v;
+  int cap;
+  __device__ __forceinline__ RbStage(void *buf, size_t bytes) {
+    cap = (int)(bytes / ((WIN ? 6 : 4) * sizeof(double) + sizeof(int)));
+    double *d = reinterpret_cast<double *>(buf);
+    load = d; T = d + cap; c = d + 2 * cap; t = d + 3 * cap;
+    E = WIN ? d + 4 * cap : nullptr;
+    L = WIN ? d + 5 * cap : nullptr;
+    v = reinterpret_cast<int *>(d + (WIN ? 6 : 4) * cap);
+  }
+  __device__ __forceinline__ At<WIN> node(int x) const {  // == a_node(I, v[x])
+    At<WIN> a;
+    a.dist = 0.0; a.load = load[x]; a.T = T[x];
+    if (WIN) { a.E = E[x]; a.L = L[x]; } else { a.E = 0.0; a.L = 0.0; }
+    a.TW = 0.0;
+    a.first = v[x]; a.last = v[x];
+    return a;
+  }
+};
+
+// fold of row i from the staged positions base..base+n-1 (same arithmetic as fold_row)
+template <bool WIN>
+__device__ __forceinline__ void fold_row_s(const DevInst &I, const DevPop &P, int b, int r, const RbStage<WIN> &St,
+                                           int base, int i, int n, int4 mt) {
+  At<WIN> acc = St.node(base + i);
+  double *trow = P.tabT + (row_base(P, b, r) + i) * P.Kp * P.FE;  // T[r][i][*]
+  if (i == 0) tab_store<WIN>(P, P.tabP, b, r, 0, acc);
+  tab_store_at<WIN>(trow + i * P.FE, acc);
+  for (int j = i + 1; j < n; j++) {
+    acc = a_cat_l<WIN>(acc, St.node(base + j), Link{St.c[base + j], St.t[base + j]});
+    if (i == 0) tab_store<WIN>(P, P.tabP, b, r, j, acc);
+    tab_store_at<WIN>(trow + j * P.FE, acc);
+  }
+  tab_store<WIN>(P, P.tabS, b, r, i, acc);
+  if (i == 0) {
+    double o[5];
+    contrib<WIN>(I, acc, mt.y, mt.z, mt.x, o);
+    P.rcon[(size_t)b * P.J + r] = make_double4(acc.dist, o[1], o[2], o[3]);
+    P.rmeta[(size_t)b * P.J + r].w = (int)o[4];
+  }
+}
+
+// whole CTA.  off: shared int[offcap] (route position offsets), stg: shared
+// staging buffer of stg_bytes.  Routes are staged in batches that fit; a group
+// of kRbGroup lanes folds each route, a lane taking the row pair (i, n-1-i).
+template <bool WIN>
+__device__ void rebuild_routes(const DevInst &I, const DevPop &P, int b, const int *list, int cnt, int *off,
+                               int offcap, void *stg, size_t stg_bytes) {
   int *LOC = P.loc + (size_t)b * P.N;
   int *NXS = P.nxs + (size_t)b * P.N;
-  int4 *RM = P.rmeta + (size_t)b * P.J;
-  double4 *RC = P.rcon + (size_t)b * P.J;
+  const int4 *RM = P.rmeta + (size_t)b * P.J;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  for (int q = wid; q < cnt; q += nw) {
-    const int r = list ? list[q] : q;
-    int4 mt = RM[r];
-    int k = mt.x, n = k + (I.open ? 1 : 2);
-    const int *sq = P.seq + row_base(P, b, r);
-    for (int p = lane; p < k; p += 32) {
-      LOC[sq[p + 1]] = (r << 9) | p;
-      NXS[sq[p + 1]] = p + 2 <= n - 1 ? sq[p + 2] : -1;
-    }
-    for (int i = lane; i < n; i += 32) {
-      At<WIN> acc = a_node<WIN>(I, sq[i]);
-      double *trow = P.tabT + (row_base(P, b, r) + i) * P.Kp * P.FE;  // T[r][i][*]
-      if (i == 0) tab_store<WIN>(P, P.tabP, b, r, 0, acc);
-      tab_store_at<WIN>(trow + i * P.FE, acc);
-      for (int j = i + 1; j < n; j++) {
-        acc = a_cat_ne<WIN>(I, acc, a_node<WIN>(I, sq[j]));
-        if (i == 0) tab_store<WIN>(P, P.tabP, b, r, j, acc);
-        tab_store_at<WIN>(trow + j * P.FE, acc);
+  // few routes (the incremental rebuild): a warp per route, one pass
+  if (!MDR_RB_STAGED || cnt <= nw || cnt + 1 > offcap || stg == nullptr) {
+    for (int q = wid; q < cnt; q += nw) {
+      const int r = list ? list[q] : q;
+      const int4 mt = RM[r];
+      const int k = mt.x, n = k + (I.open ? 1 : 2);
+      const int *sq = P.seq + row_base(P, b, r);
+      for (int p = lane; p < k; p += 32) {
+        LOC[sq[p + 1]] = (r << 9) | p;
+        NXS[sq[p + 1]] = p + 2 <= n - 1 ? sq[p + 2] : -1;
       }
-      tab_store<WIN>(P, P.tabS, b, r, i, acc);
-      if (i == 0) {
-        double o[5];
-        contrib<WIN>(I, acc, mt.y, mt.z, k, o);
-        RC[r] = make_double4(acc.dist, o[1], o[2], o[3]);  // route_D is the raw table value
-        RM[r].w = (int)o[4];
+      for (int i = lane; i < n; i += 32) fold_row<WIN>(I, P, b, r, sq, i, n, mt);
+    }
+    return;
+  }
+#ifdef MDR_SEL_PROF
+  long long t_rb = clock64();
+#endif
+  // position offsets of the routes: lengths loaded by all threads at once, then
+  // one warp scans them in shared memory
+  for (int q = threadIdx.x; q < cnt; q += blockDim.x) off[q + 1] = RM[list ? list[q] : q].x + (I.open ? 1 : 2);
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    int carry = 0;
+    for (int q0 = 0; q0 < cnt; q0 += 32) {
+      const int q = q0 + lane;
+      int x = q < cnt ? off[q + 1] : 0;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, x, d);
+        if (lane >= d) x += y;
+      }
+      if (q < cnt) off[q + 1] = carry + x;
+      carry += __shfl_sync(0xffffffffu, x, 31);
+    }
+    if (lane == 0) off[0] = 0;
+  }
+  __syncthreads();
+  RBT_(12);
+  const RbStage<WIN> St(stg, stg_bytes);
+  const int gid = threadIdx.x / kRbGroup, ng = blockDim.x / kRbGroup, sub = threadIdx.x % kRbGroup;
+  for (int q0 = 0; q0 < cnt;) {
+    int lo = q0 + 1, hi = cnt;  // routes q0..q1-1 whose positions fit the stage
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (off[mid] - off[q0] <= St.cap) lo = mid; else hi = mid - 1;
+    }
+    const int q1 = lo, p0 = off[q0], np = off[q1] - p0;
+    for (int x = threadIdx.x; x < np; x += blockDim.x) {
+      int a = q0, z = q1 - 1;  // the route holding position p0 + x
+      while (a < z) {
+        const int mid = (a + z + 1) >> 1;
+        if (off[mid] <= p0 + x) a = mid; else z = mid - 1;
+      }
+      const int p = p0 + x - off[a], n = off[a + 1] - off[a], r = list ? list[a] : a;
+      const int *sq = P.seq + row_base(P, b, r);
+      const int v = sq[p];
+      if (p >= 1 && p <= n - (I.open ? 1 : 2)) {  // SolutionIndex entries of the customers
+        LOC[v] = (r << 9) | (p - 1);
+        NXS[v] = p + 1 <= n - 1 ? sq[p + 1] : -1;
+      }
+      const double2 *np2 = reinterpret_cast<const double2 *>(I.node + v);
+      const double2 qs = __ldg(np2);
+      St.load[x] = qs.x; St.T[x] = qs.y;
+      if (WIN) { const double2 el = __ldg(np2 + 1); St.E[x] = el.x; St.L[x] = el.y; }
+      St.v[x] = v;
+      if (p > 0) { const Link lk = link_of(I, sq[p - 1], v); St.c[x] = lk.c; St.t[x] = lk.t; }
+    }
+    __syncthreads();
+    RBT_(13);
+    for (int q = q0 + gid; q < q1; q += ng) {
+      const int r = list ? list[q] : q;
+      const int4 mt = RM[r];
+      const int n = off[q + 1] - off[q], base = off[q] - p0;
+      for (int p = sub; p < (n + 1) / 2; p += kRbGroup) {
+        fold_row_s<WIN>(I, P, b, r, St, base, p, n, mt);
+        if (n - 1 - p != p) fold_row_s<WIN>(I, P, b, r, St, base, n - 1 - p, n, mt);
       }
     }
+    __syncthreads();
+    RBT_(14);
+#ifdef MDR_SEL_PROF
+    if (threadIdx.x == 0) atomicAdd(&g_selprof[15], 1ull);
+#endif
+    q0 = q1;
   }
 }
 
@@ -184,21 +328,24 @@ __device__ void rebuild_fleet(const DevInst &I, const DevPop &P, int b, int *sm_
 
 // rebuild one individual (whole block): loc, tables, route terms, fleet
 template <bool WIN>
-__device__ void rebuild_block(const DevInst &I, const DevPop &P, int b, int *sm_cnt) {
+__device__ void rebuild_block(const DevInst &I, const DevPop &P, int b, int *sm_cnt, int *off, int offcap, void *stg,
+                              size_t stg_bytes) {
   int *LOC = P.loc + (size_t)b * P.N;
   for (int v = threadIdx.x; v < P.N; v += blockDim.x) { LOC[v] = -1; P.nxs[(size_t)b * P.N + v] = -1; }
   __syncthreads();
-  rebuild_routes<WIN>(I, P, b, nullptr, P.m[b]);
+  rebuild_routes<WIN>(I, P, b, nullptr, P.m[b], off, offcap, stg, stg_bytes);
   __syncthreads();
   rebuild_fleet(I, P, b, sm_cnt);
 }
 
 template <bool WIN>
 __global__ void __launch_bounds__(256) k_rebuild(DevInst I, DevPop P, int B) {
-  extern __shared__ int sm_cnt[];
+  extern __shared__ int sm_cnt[];  // [ND + 1], off [J + 1], staging (16-B aligned)
   int b = blockIdx.x;
   if (b >= B) return;
-  rebuild_block<WIN>(I, P, b, sm_cnt);
+  int *off = sm_cnt + P.ND + 1;
+  void *stg = reinterpret_cast<void *>((reinterpret_cast<uintptr_t>(off + P.J + 1) + 15) & ~uintptr_t(15));
+  rebuild_block<WIN>(I, P, b, sm_cnt, off, P.J + 1, stg, kRbStageBytes);
 }
 
 // ---------------------------------------------------------------------------
@@ -687,8 +834,10 @@ __global__ void __launch_bounds__(32 * CU, MINB) k_eval_p(DevInst I, DevPop P, L
 }
 
 // generic evaluator: intra-route relocate/swap, 2-opt, depot operators,
-// one thread per queued candidate through eval_cand (batch.py:365-553)
-template <bool WIN>
+// one thread per queued candidate through eval_cand (batch.py:365-553).
+// FOP 0 / 1: the per-producer regions 1 / 2, which hold only same-route
+// relocate / swap candidates; -1: any operator (region 0, single queue).
+template <bool WIN, int FOP>
 #ifndef MDR_GMINB
 #define MDR_GMINB 3
 #endif
@@ -699,21 +848,30 @@ __global__ void __launch_bounds__(256, MDR_GMINB) k_eval_g(DevInst I, DevPop P, 
   const bool mm = L.multi_move != 0;
   const int wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  // the next batch's queue entry is loaded one iteration ahead (it heads the
+  // dependent load chain entry -> route meta -> table rows)
+#ifndef MDR_G_PREFETCH
+#define MDR_G_PREFETCH 1
+#endif
+  ulonglong2 nx = make_ulonglong2(0ull, 0ull);
+  if (MDR_G_PREFETCH && wid * 32 + lane < total) nx = Q[wid * 32 + lane];
   for (int base = wid * 32; base < total; base += nwarps * 32) {
     const int i = base + lane;
     const bool valid = i < total;
+    ulonglong2 e = nx;
+    if (!MDR_G_PREFETCH) e = valid ? Q[i] : make_ulonglong2(0ull, 0ull);
+    else if (i + nwarps * 32 < total) nx = Q[i + nwarps * 32];
     int b = -1, op = 0;
     unsigned long long key = 0, o = ~0ull;
     bool fol = false;
     if (valid) {
-      ulonglong2 e = Q[i];
       key = e.x;
       b = (int)(e.y & 0xffffffu);
       op = (int)(e.y >> 24);
       double lam[4];
 #pragma unroll
       for (int q = 0; q < 4; q++) lam[q] = P.lam[b * 4 + q];
-      Delta D = eval_cand<WIN>(I, P, b, op, unpack_key(key), lam);
+      Delta D = eval_cand<WIN, FOP, (FOP >= 0)>(I, P, b, op, unpack_key(key), lam);
       if (D.dF != D.dF) {
         atomicOr(P.nanflag + b, 1);
       } else {
@@ -864,12 +1022,15 @@ __device__ bool apply_one(const DevInst &I, const DevPop &P, int b, int op, cons
 }
 
 #ifdef MDR_SEL_PROF
-__device__ unsigned long long g_selprof[16];
 #define SELT(i) do { if (threadIdx.x == 0) { long long t__ = clock64(); atomicAdd(&g_selprof[i], (unsigned long long)(t__ - t_sel)); t_sel = t__; } } while (0)
 #else
 #define SELT(i) do { } while (0)
 #endif
-template <bool WIN>
+#ifndef MDR_SEL_WARP
+#define MDR_SEL_WARP 1  // 0: repeated block argmin for fewer than 256 followers too
+#endif
+constexpr int kSelWarpFw = 8;  // followers per lane of the warp selection
+
 #ifndef MDR_TOS_W_MINB
 #define MDR_TOS_W_MINB 3  // 2-opt* with windows: 8-warp CTAs, this many per SM
 #endif
@@ -885,11 +1046,14 @@ template <bool WIN>
 #ifndef MDR_SEL_SORT
 #define MDR_SEL_SORT 2048  // followers sorted in shared memory up to this many (else repeated block argmin)
 #endif
+constexpr size_t kSelStageBytes =
+    sizeof(ulonglong2) * MDR_SEL_SORT > kRbStageBytes ? sizeof(ulonglong2) * MDR_SEL_SORT : kRbStageBytes;
 
 #ifndef MDR_SEL_THREADS
 #define MDR_SEL_THREADS 512  // one CTA per individual: more warps rebuild more touched routes at once
 #endif
-__global__ void __launch_bounds__(MDR_SEL_THREADS) k_select(DevInst I, DevPop P, LsParams L) {
+template <bool WIN>
+__global__ void __launch_bounds__(MDR_SEL_THREADS, 1) k_select(DevInst I, DevPop P, LsParams L) {
   extern __shared__ unsigned long long smx[];
   __shared__ OK red[MDR_SEL_THREADS / 32];
   __shared__ int s_flag, s_nm, s_mnew, s_snap, s_nt, s_empty, s_feas;
@@ -900,6 +1064,8 @@ __global__ void __launch_bounds__(MDR_SEL_THREADS) k_select(DevInst I, DevPop P,
   if (P.st[b].done) return;
 #ifdef MDR_SEL_PROF
   long long t_sel = clock64();
+  const long long t_sel0 = t_sel;
+  if (threadIdx.x == 0) atomicAdd(&g_selprof[8], 1ull);  // active CTA-rounds
 #endif
   const int J = P.J;
   unsigned long long *sel = smx;                            // [J] selected keys
@@ -907,6 +1073,9 @@ __global__ void __launch_bounds__(MDR_SEL_THREADS) k_select(DevInst I, DevPop P,
   int *newidx = reinterpret_cast<int *>(used + (J / 32 + 1));  // [J+J]
   int *sm_cnt = newidx + 2 * J;                             // [ND]
   int *tl = sm_cnt + P.ND + 4;                              // [3J] touched routes
+  // sorted followers (select phase) / staged route positions (rebuild phase)
+  void *stg = reinterpret_cast<void *>((reinterpret_cast<uintptr_t>(tl + 3 * J + 1) + 15) & ~uintptr_t(15));
+  const size_t stg_bytes = kSelStageBytes;
   const int op = P.op_cur[b];
 
   // ---- leader (batch.py:587-597): the round's min (dF, key) of this individual
@@ -950,7 +1119,7 @@ __global__ void __launch_bounds__(MDR_SEL_THREADS) k_select(DevInst I, DevPop P,
       // no used route is taken, the others re-check -- the greedy of
       // select_moves without a block-wide argmin per selected move
       const ulonglong2 *F = P.fol + (size_t)b * P.Fcap;
-      ulonglong2 *S = reinterpret_cast<ulonglong2 *>((reinterpret_cast<uintptr_t>(tl + 3 * J + 1) + 15) & ~uintptr_t(15));
+      ulonglong2 *S = reinterpret_cast<ulonglong2 *>(stg);
       int n2 = 32;
       while (n2 < nf) n2 <<= 1;
       for (int i = threadIdx.x; i < n2; i += blockDim.x)
@@ -993,6 +1162,51 @@ __global__ void __launch_bounds__(MDR_SEL_THREADS) k_select(DevInst I, DevPop P,
             nm++;
             __syncwarp();
           }
+        }
+        if (lane == 0) s_nm = nm;
+      }
+      __syncthreads();
+    } else if (L.multi_move && nf <= 32 * kSelWarpFw && MDR_SEL_WARP) {
+      // up to 32 * kSelWarpFw followers: one warp holds them in registers and
+      // repeats a warp argmin over the non-conflicting ones (no CTA barriers)
+      if (threadIdx.x < 32) {
+        const ulonglong2 *F = P.fol + (size_t)b * P.Fcap;
+        const int lane = threadIdx.x;
+        unsigned long long eo[kSelWarpFw], ek[kSelWarpFw];
+        int e1[kSelWarpFw], e2[kSelWarpFw];
+#pragma unroll
+        for (int q = 0; q < kSelWarpFw; q++) {
+          const int i = lane + 32 * q;
+          eo[q] = ~0ull; ek[q] = ~0ull; e1[q] = 0; e2[q] = -1;
+          if (i < nf) {
+            const ulonglong2 e = F[i];
+            if (e.y != s_leader) {
+              const Cand c = unpack_key(e.y);
+              eo[q] = e.x; ek[q] = e.y; e1[q] = c.r1; e2[q] = c.r2;
+            }
+          }
+        }
+        int nm = s_nm;
+        for (;;) {
+          OK x{~0ull, ~0ull};
+#pragma unroll
+          for (int q = 0; q < kSelWarpFw; q++) {
+            bool conflict = (used[e1[q] >> 5] >> (e1[q] & 31)) & 1u;
+            if (e2[q] >= 0) conflict = conflict || ((used[e2[q] >> 5] >> (e2[q] & 31)) & 1u);
+            const OK y{eo[q], ek[q]};
+            if (eo[q] != ~0ull && !conflict && ok_less(y, x)) x = y;
+          }
+          x = warp_min(x);
+          if (x.o == ~0ull) break;
+          __syncwarp();
+          if (lane == 0) {
+            sel[nm] = x.k;
+            const Cand c = unpack_key(x.k);
+            used[c.r1 >> 5] |= 1u << (c.r1 & 31);
+            if (c.r2 >= 0) used[c.r2 >> 5] |= 1u << (c.r2 & 31);
+          }
+          nm++;
+          __syncwarp();
         }
         if (lane == 0) s_nm = nm;
       }
@@ -1079,49 +1293,71 @@ __global__ void __launch_bounds__(MDR_SEL_THREADS) k_select(DevInst I, DevPop P,
         s_mnew = m2;
       }
       __syncthreads();
-      rebuild_routes<WIN>(I, P, b, tl, s_nt);
+      rebuild_routes<WIN>(I, P, b, tl, s_nt, newidx, 2 * J, stg, stg_bytes);
       __syncthreads();
       SELT(2);  // incremental rebuild
       rebuild_fleet(I, P, b, sm_cnt);
     } else {
+    // drop the empty routes: lengths loaded by all threads at once, one warp
+    // scans keep flags and kept lengths in shared memory, then the sequences
+    // move position-parallel through the scratch rows
+    int *klen = tl, *oldof = tl + J, *off2 = tl + 2 * J;  // [J], [J], [J + 1] (tl has 3J + 1)
+    for (int r = threadIdx.x; r < m2; r += blockDim.x) klen[r] = P.rmeta[(size_t)b * J + r].x;
+    __syncthreads();
     if (threadIdx.x < 32) {
-      int carry = 0;
+      const int lane = threadIdx.x;
+      int carry = 0, pos = 0;
       for (int base = 0; base < m2; base += 32) {
-        int r = base + threadIdx.x;
-        bool keep = r < m2 && P.rmeta[(size_t)b * J + r].x > 0;
-        unsigned bal = __ballot_sync(0xffffffffu, keep);
-        if (r < m2) newidx[r] = keep ? carry + __popc(bal & ((1u << threadIdx.x) - 1)) : -1;
+        const int r = base + lane;
+        const bool keep = r < m2 && klen[r] > 0;
+        const unsigned bal = __ballot_sync(0xffffffffu, keep);
+        const int ni = carry + __popc(bal & ((1u << lane) - 1));
+        int x = keep ? klen[r] + 2 : 0;  // the k+2 used sequence slots
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+          const int y = __shfl_up_sync(0xffffffffu, x, d);
+          if (lane >= d) x += y;
+        }
+        if (keep) { oldof[ni] = r; off2[ni + 1] = pos + x; }
+        pos += __shfl_sync(0xffffffffu, x, 31);
         carry += __popc(bal);
       }
-      if (threadIdx.x == 0) s_mnew = carry;
+      if (lane == 0) { s_mnew = carry; off2[0] = 0; }
     }
     __syncthreads();
-    {
-      const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-      for (int r = wid; r < m2; r += nw) {
-        if (newidx[r] < 0) continue;
-        const int len = P.rmeta[(size_t)b * J + r].x + 2;
-        for (int x = lane; x < len; x += 32)
-          P.scratch_seq[row_base(P, b, newidx[r]) + x] = P.seq[row_base(P, b, r) + x];
+    const int mn_ = s_mnew, tot = off2[mn_];
+    for (int x = threadIdx.x; x < tot; x += blockDim.x) {
+      int a = 0, z = mn_ - 1;
+      while (a < z) {
+        const int mid = (a + z + 1) >> 1;
+        if (off2[mid] <= x) a = mid; else z = mid - 1;
       }
+      const int p = x - off2[a];
+      P.scratch_seq[row_base(P, b, a) + p] = P.seq[row_base(P, b, oldof[a]) + p];
     }
-    for (int r = threadIdx.x; r < m2; r += blockDim.x)
-      if (newidx[r] >= 0) P.scratch_meta[(size_t)b * J + newidx[r]] = P.rmeta[(size_t)b * J + r];
+    for (int q = threadIdx.x; q < mn_; q += blockDim.x)
+      P.scratch_meta[(size_t)b * J + q] = P.rmeta[(size_t)b * J + oldof[q]];
     __syncthreads();
-    const int mn_ = s_mnew;
-    {
-      const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-      for (int r = wid; r < mn_; r += nw) {
-        const int len = P.scratch_meta[(size_t)b * J + r].x + 2;
-        for (int x = lane; x < len; x += 32) P.seq[row_base(P, b, r) + x] = P.scratch_seq[row_base(P, b, r) + x];
+    for (int x = threadIdx.x; x < tot; x += blockDim.x) {
+      int a = 0, z = mn_ - 1;
+      while (a < z) {
+        const int mid = (a + z + 1) >> 1;
+        if (off2[mid] <= x) a = mid; else z = mid - 1;
       }
+      const int p = x - off2[a];
+      P.seq[row_base(P, b, a) + p] = P.scratch_seq[row_base(P, b, a) + p];
     }
-    for (int r = threadIdx.x; r < mn_; r += blockDim.x)
-      P.rmeta[(size_t)b * J + r] = P.scratch_meta[(size_t)b * J + r];
+    for (int q = threadIdx.x; q < mn_; q += blockDim.x) P.rmeta[(size_t)b * J + q] = P.scratch_meta[(size_t)b * J + q];
     if (threadIdx.x == 0) P.m[b] = mn_;
     __syncthreads();
-    rebuild_block<WIN>(I, P, b, sm_cnt);
+#ifdef MDR_SEL_PROF
+    if (threadIdx.x == 0) atomicAdd(&g_selprof[11], (unsigned long long)(clock64() - t_sel));
+#endif
+    rebuild_block<WIN>(I, P, b, sm_cnt, newidx, 2 * J, stg, stg_bytes);
     SELT(3);  // full rebuild (a route emptied)
+#ifdef MDR_SEL_PROF
+    if (threadIdx.x == 0) atomicAdd(&g_selprof[9], 1ull);
+#endif
     }
     const int mn = s_mnew;
     SELT(4);  // fleet (incremental path)
@@ -1193,6 +1429,9 @@ __global__ void __launch_bounds__(MDR_SEL_THREADS) k_select(DevInst I, DevPop P,
     }
   }
   SELT(5);  // totals, adapt, trace, snapshot
+#ifdef MDR_SEL_PROF
+  if (threadIdx.x == 0) atomicMax(&g_selprof[10], (unsigned long long)(t_sel - t_sel0));
+#endif
   // ---- advance the pass/operator cursor
   if (threadIdx.x == 0) {
     LsState st = P.st[b];
@@ -1369,11 +1608,15 @@ __global__ void __launch_bounds__(1024) k_pack(DevPop P, int b0, int B, int best
 static size_t select_smem(const DevPop &P) {
   // sel [J] u64, used bitmask, newidx [2J], sm_cnt [ND+4], tl [3J+1] (+ alignment), sorted followers
   return sizeof(unsigned long long) * P.J + sizeof(unsigned) * (P.J / 32 + 1) +
-         sizeof(int) * (5 * P.J + P.ND + 8 + 2) + 16 + sizeof(ulonglong2) * MDR_SEL_SORT;
+         sizeof(int) * (5 * P.J + P.ND + 8 + 2) + 16 + kSelStageBytes;
 }
 
 void launch_rebuild(const DevInst &I, const DevPop &P, int B, bool win, cudaStream_t s) {
-  size_t sm = sizeof(int) * (P.ND + 1);
+  const size_t sm = sizeof(int) * (P.ND + 1) + sizeof(int) * (P.J + 1) + 16 + kRbStageBytes;
+  if (sm > 48 * 1024) {  // per device: the attribute call is cheap and launch_rebuild is not in the round graph
+    cudaFuncSetAttribute(k_rebuild<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    cudaFuncSetAttribute(k_rebuild<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  }
   if (win) k_rebuild<true><<<B, 256, sm, s>>>(I, P, B);
   else k_rebuild<false><<<B, 256, sm, s>>>(I, P, B);
 }
@@ -1407,8 +1650,14 @@ template <bool WIN>
 static void launch_eval_g_region(const DevInst &I, const DevPop &P, const LsParams &L, cudaStream_t s, int region) {
   static int gd[MDR_MAXDEV] = {0};  // full occupancy of the (latency-bound) generic evaluator
   int &g = gd[cur_dev()];
-  if (!g) g = grid_for(k_eval_g<WIN>);
-  k_eval_g<WIN><<<g, 256, 0, s>>>(I, P, L, region);
+  if (!g) g = grid_for(k_eval_g<WIN, -1>);
+  // per-producer regions 1 / 2 hold only same-route relocate / swap candidates
+  static int generic = -1;  // MDR_G_GENERIC: the generic form for every region (A/B)
+  if (generic < 0) generic = getenv("MDR_G_GENERIC") ? 1 : 0;
+  const bool spec = P.gbase[1] > 0 && region > 0 && !generic;
+  if (spec && region == 1) k_eval_g<WIN, 0><<<g, 256, 0, s>>>(I, P, L, region);
+  else if (spec) k_eval_g<WIN, 1><<<g, 256, 0, s>>>(I, P, L, region);
+  else k_eval_g<WIN, -1><<<g, 256, 0, s>>>(I, P, L, region);
 }
 
 // the three staged evaluators of one (CU, CT) shape on the side streams
@@ -1437,7 +1686,9 @@ static void launch_op(const DevInst &I, const DevPop &P, const LsParams &L, cuda
     int pct = (int)((MINB * (sm + stat) * 100 + 228 * 1024 - 1) / (228 * 1024));
     if (getenv("MDR_CARVEOUT")) pct = atoi(getenv("MDR_CARVEOUT"));
     cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, pct > 100 ? 100 : pct);
-    cudaFuncSetAttribute(k_eval_g<WIN>, cudaFuncAttributePreferredSharedMemoryCarveout, 0);
+    cudaFuncSetAttribute(k_eval_g<WIN, -1>, cudaFuncAttributePreferredSharedMemoryCarveout, 0);
+    cudaFuncSetAttribute(k_eval_g<WIN, 0>, cudaFuncAttributePreferredSharedMemoryCarveout, 0);
+    cudaFuncSetAttribute(k_eval_g<WIN, 1>, cudaFuncAttributePreferredSharedMemoryCarveout, 0);
     gridd[dv] = 0;
   }
   if (!gridd[dv]) {

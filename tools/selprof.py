@@ -29,3 +29,10 @@ rounds = pop.timing()["rounds"] // 2
 print(f"pop {pop_n}: rounds {rounds}, k_select CTA-cycles {tot:.3e}")
 for i, n in enumerate(names):
     print(f"  {n:22s} {100 * (buf[i] - base[i]) / tot:5.1f}%  {(buf[i] - base[i]) / max(rounds, 1) / 1.965e3:8.1f} us-CTA per round")
+act, full = buf[8] - base[8], buf[9] - base[9]
+print(f"  active CTA-rounds {act}, full rebuilds {full} ({100 * full / max(act, 1):.1f}%), "
+      f"{(buf[3] - base[3]) / max(full, 1) / 1.965e3:.1f} us each; mean CTA {tot / max(act, 1) / 1.965e3:.1f} us, "
+      f"max CTA {buf[10] / 1.965e3:.1f} us; of a full rebuild, the compaction {(buf[11] - base[11]) / max(full, 1) / 1.965e3:.1f} us")
+nb = buf[15] - base[15]
+print(f"  staged rebuilds: batches {nb}; per batch: scan {(buf[12] - base[12]) / max(nb, 1) / 1.965e3:.2f} us, "
+      f"stage {(buf[13] - base[13]) / max(nb, 1) / 1.965e3:.2f} us, fold {(buf[14] - base[14]) / max(nb, 1) / 1.965e3:.2f} us")
