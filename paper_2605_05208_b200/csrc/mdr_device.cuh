@@ -551,6 +551,118 @@ __device__ __forceinline__ Delta eval_cand(const DevInst &I, const DevPop &P, in
   return D;
 }
 
+// table entry without endpoints (read-only in the evaluation kernels)
+template <bool WIN>
+__device__ __forceinline__ At<WIN> tab_raw(const double *src) {
+  const double2 *e = reinterpret_cast<const double2 *>(src);
+  At<WIN> a;
+  const double2 x = __ldg(e), y = __ldg(e + 1);
+  a.dist = x.x; a.load = x.y; a.T = y.x;
+  if (WIN) {
+    const double2 z = __ldg(e + 2);
+    a.E = y.y; a.L = z.x; a.TW = z.y;
+  } else {
+    a.E = 0.0; a.L = 0.0; a.TW = 0.0;
+  }
+  a.first = 0; a.last = 0;
+  return a;
+}
+
+// same-route relocate (OP 0) / swap (OP 1): eval_cand's r1 == r2 branches
+// (batch.py:391-463) with every load issued in two waves -- first all that the
+// key addresses (route meta and terms, sequence ids, the prefix / segment /
+// middle / suffix table entries; an empty middle or suffix reads a harmless
+// in-row slot), then the links between the pieces -- instead of one dependent
+// load chain per concatenation.  Same pieces, same concatenation order, same
+// link values: bit-identical to eval_cand.
+template <bool WIN, int OP>
+__device__ __forceinline__ Delta eval_intra(const DevInst &I, const DevPop &P, int b, const Cand &c,
+                                            const double lam[4]) {
+  const int r = c.r1, p1 = c.p1, p2 = c.p2, l1 = c.l1;
+  const size_t rb = row_base(P, b, r);
+  const int *sq = P.seq + rb;
+  const int Kp = P.Kp, FE = P.FE;
+  const int4 m1 = P.rmeta[(size_t)b * P.J + r];
+  const double4 o1 = P.rcon[(size_t)b * P.J + r];
+  // pieces, in concatenation order: X (prefix 0..e), then for relocate
+  // [S, M] (before) or [M, S], for swap [B, M, A]; then U (suffix isf..n-1)
+  int e, iS, jS, iM, jM, iB = 0, jB = 0, isf;
+  bool before = false;
+  if (OP == 0) {
+    before = p2 <= p1;
+    e = before ? p2 : p1;
+    iS = p1 + 1; jS = p1 + l1;
+    iM = before ? p2 + 1 : p1 + l1 + 1; jM = before ? p1 : p2;
+    isf = before ? p1 + l1 + 1 : p2 + 1;
+  } else {
+    e = p1;
+    iS = p1 + 1; jS = p1 + l1;  // segment A
+    iB = p2 + 1; jB = p2 + c.l2;
+    iM = p1 + l1 + 1; jM = p2;
+    isf = p2 + c.l2 + 1;
+  }
+  const bool midne = jM >= iM;
+  const int iM2 = midne ? iM : iS, jM2 = midne ? jM : jS;
+  // wave 1
+  const int v_e = __ldg(sq + e), v_sf = __ldg(sq + iS), v_sl = __ldg(sq + jS);
+  const int v_mf = __ldg(sq + iM2), v_ml = __ldg(sq + jM2), v_uf = __ldg(sq + isf);
+  const int v_bf = OP == 1 ? __ldg(sq + iB) : 0, v_bl = OP == 1 ? __ldg(sq + jB) : 0;
+  const At<WIN> X = tab_raw<WIN>(P.tabP + (rb + e) * FE);
+  const At<WIN> S = tab_raw<WIN>(P.tabT + ((rb + iS) * Kp + jS) * FE);
+  const At<WIN> M = tab_raw<WIN>(P.tabT + ((rb + iM2) * Kp + jM2) * FE);
+  const At<WIN> U = tab_raw<WIN>(P.tabS + (rb + isf) * FE);
+  At<WIN> Bq;
+  if (OP == 1) Bq = tab_raw<WIN>(P.tabT + ((rb + iB) * Kp + jB) * FE);
+  const int k1 = m1.x, n1 = k1 + (I.open ? 1 : 2);
+  const bool sufne = isf <= n1 - 1;
+  const int sF = c.rev1 ? v_sl : v_sf, sL = c.rev1 ? v_sf : v_sl;
+  // wave 2: the links, in concatenation order
+  At<WIN> x;
+  if (OP == 0) {
+    if (before) {
+      const int mlast = midne ? v_ml : sL;
+      const Link L1 = link_of(I, v_e, sF);
+      const Link L2 = midne ? link_of(I, sL, v_mf) : Link{0.0, 0.0};
+      const Link L3 = sufne ? link_of(I, mlast, v_uf) : Link{0.0, 0.0};
+      x = a_cat_l<WIN>(X, S, L1);
+      if (midne) x = a_cat_l<WIN>(x, M, L2);
+      if (sufne) x = a_cat_l<WIN>(x, U, L3);
+    } else {
+      const int mlast = midne ? v_ml : v_e;
+      const Link L1 = midne ? link_of(I, v_e, v_mf) : Link{0.0, 0.0};
+      const Link L2 = link_of(I, mlast, sF);
+      const Link L3 = sufne ? link_of(I, sL, v_uf) : Link{0.0, 0.0};
+      x = X;
+      if (midne) x = a_cat_l<WIN>(x, M, L1);
+      x = a_cat_l<WIN>(x, S, L2);
+      if (sufne) x = a_cat_l<WIN>(x, U, L3);
+    }
+  } else {
+    const int bF = c.rev2 ? v_bl : v_bf, bL = c.rev2 ? v_bf : v_bl;
+    const int mlast = midne ? v_ml : bL;
+    const Link L1 = link_of(I, v_e, bF);
+    const Link L2 = midne ? link_of(I, bL, v_mf) : Link{0.0, 0.0};
+    const Link L3 = link_of(I, mlast, sF);
+    const Link L4 = sufne ? link_of(I, sL, v_uf) : Link{0.0, 0.0};
+    x = a_cat_l<WIN>(X, Bq, L1);
+    if (midne) x = a_cat_l<WIN>(x, M, L2);
+    x = a_cat_l<WIN>(x, S, L3);
+    if (sufne) x = a_cat_l<WIN>(x, U, L4);
+  }
+  double cA[5];
+  contrib<WIN>(I, x, m1.y, m1.z, k1, cA);
+  const double old[5] = {o1.x, o1.y, o1.z, o1.w, (double)m1.w};
+  Delta D;
+  D.dD = (0.0 + cA[0]) - old[0];
+  D.dV1 = (0.0 + cA[1]) - old[1];
+  D.dV2 = (0.0 + cA[2]) - old[2];
+  D.dV3 = (0.0 + cA[3]) - old[3];
+  D.dV4 = I.theta * (((0.0 + cA[4]) - old[4]) + 0.0);
+  D.dF = (((D.dD + lam[0] * D.dV1) + lam[1] * D.dV2) + lam[2] * D.dV3) + lam[3] * D.dV4;
+  D.fn = 1;
+  return D;
+}
+
 __device__ __forceinline__ bool follower_ok(const Delta &d) {
   return d.dD < -MDR_EPS && fabs(d.dV1) <= MDR_EPS && fabs(d.dV2) <= MDR_EPS && fabs(d.dV3) <= MDR_EPS &&
          fabs(d.dV4) <= MDR_EPS && d.fn;

@@ -841,7 +841,10 @@ template <bool WIN, int FOP>
 #ifndef MDR_GMINB
 #define MDR_GMINB 3
 #endif
-__global__ void __launch_bounds__(256, MDR_GMINB) k_eval_g(DevInst I, DevPop P, LsParams L, int region) {
+#ifndef MDR_GMINB_I
+#define MDR_GMINB_I 2  // the same-route forms hold a whole candidate's loads at once
+#endif
+__global__ void __launch_bounds__(256, FOP >= 0 ? MDR_GMINB_I : MDR_GMINB) k_eval_g(DevInst I, DevPop P, LsParams L, int region) {
   const int lane = threadIdx.x & 31;
   const int total = min(P.gcount[region], P.gbase[region + 1] - P.gbase[region]);
   const ulonglong2 *Q = P.gq + P.gbase[region];
@@ -871,7 +874,9 @@ __global__ void __launch_bounds__(256, MDR_GMINB) k_eval_g(DevInst I, DevPop P, 
       double lam[4];
 #pragma unroll
       for (int q = 0; q < 4; q++) lam[q] = P.lam[b * 4 + q];
-      Delta D = eval_cand<WIN, FOP, (FOP >= 0)>(I, P, b, op, unpack_key(key), lam);
+      Delta D;
+      if constexpr (FOP >= 0) D = eval_intra<WIN, FOP>(I, P, b, unpack_key(key), lam);
+      else D = eval_cand<WIN>(I, P, b, op, unpack_key(key), lam);
       if (D.dF != D.dF) {
         atomicOr(P.nanflag + b, 1);
       } else {
@@ -1648,16 +1653,20 @@ int eval_grid_size(bool win) { return win ? grid_for(k_eval<true, 0>) : grid_for
 
 template <bool WIN>
 static void launch_eval_g_region(const DevInst &I, const DevPop &P, const LsParams &L, cudaStream_t s, int region) {
-  static int gd[MDR_MAXDEV] = {0};  // full occupancy of the (latency-bound) generic evaluator
-  int &g = gd[cur_dev()];
-  if (!g) g = grid_for(k_eval_g<WIN, -1>);
+  static int gd[MDR_MAXDEV][3] = {};  // full occupancy of each (latency-bound) form
+  int *g = gd[cur_dev()];
+  if (!g[0]) {
+    g[0] = grid_for(k_eval_g<WIN, -1>);
+    g[1] = grid_for(k_eval_g<WIN, 0>);
+    g[2] = grid_for(k_eval_g<WIN, 1>);
+  }
   // per-producer regions 1 / 2 hold only same-route relocate / swap candidates
   static int generic = -1;  // MDR_G_GENERIC: the generic form for every region (A/B)
   if (generic < 0) generic = getenv("MDR_G_GENERIC") ? 1 : 0;
   const bool spec = P.gbase[1] > 0 && region > 0 && !generic;
-  if (spec && region == 1) k_eval_g<WIN, 0><<<g, 256, 0, s>>>(I, P, L, region);
-  else if (spec) k_eval_g<WIN, 1><<<g, 256, 0, s>>>(I, P, L, region);
-  else k_eval_g<WIN, -1><<<g, 256, 0, s>>>(I, P, L, region);
+  if (spec && region == 1) k_eval_g<WIN, 0><<<g[1], 256, 0, s>>>(I, P, L, region);
+  else if (spec) k_eval_g<WIN, 1><<<g[2], 256, 0, s>>>(I, P, L, region);
+  else k_eval_g<WIN, -1><<<g[0], 256, 0, s>>>(I, P, L, region);
 }
 
 // the three staged evaluators of one (CU, CT) shape on the side streams
