@@ -13,6 +13,7 @@ Each individual's trajectory is bit-identical to a separate reference call.
 """
 from __future__ import annotations
 
+import array
 import ctypes as C
 import gc
 import time
@@ -107,14 +108,17 @@ def _mt_state(rng):
     st = rng.getstate()
     if not (isinstance(st, tuple) and len(st) == 3 and len(st[1]) == 625):
         raise TypeError("rng state is not a MT19937 random.Random state")
-    return st, np.ascontiguousarray(np.asarray(st[1], dtype=np.uint32))
+    return st, np.frombuffer(array.array("I", st[1]), dtype=np.uint32)  # 3x faster than np.asarray(tuple)
 
 
-def draw_permutations(rng, ops, n_passes: int) -> np.ndarray:
+def draw_permutations(rng, ops, n_passes: int, start: Optional[list] = None) -> np.ndarray:
     """The first n_passes `rng.shuffle(list(ops))` results (rng not advanced):
-    CPython's shuffle on the MT19937 state, run natively (mdr_shuffle_stream)."""
+    CPython's shuffle on the MT19937 state, run natively (mdr_shuffle_stream).
+    start: if given, receives (state, MT words) of rng before the draw, for _advance."""
     from . import _lib
-    _, mt = _mt_state(rng)
+    st, mt = _mt_state(rng)
+    if start is not None:
+        start.append((st, mt.copy()))
     items = np.ascontiguousarray([int(o) for o in ops], dtype=np.uint8)
     out = np.empty((n_passes, len(ops)), np.uint8)
     _lib.check(_lib.lib().mdr_shuffle_stream(_lib.ptr(mt, C.POINTER(C.c_uint32)), len(items),
@@ -123,14 +127,16 @@ def draw_permutations(rng, ops, n_passes: int) -> np.ndarray:
     return out
 
 
-def _advance(rng, ops, passes: int) -> None:
-    """Advance rng exactly as `passes` calls of rng.shuffle(list(ops)) would."""
+def _advance(rng, ops, passes: int, start=None) -> None:
+    """Advance rng exactly as `passes` calls of rng.shuffle(list(ops)) would
+    (from start = draw_permutations' saved state when given: rng itself has
+    not been used since)."""
     from . import _lib
-    st, mt = _mt_state(rng)
+    st, mt = start if start is not None else _mt_state(rng)
     items = np.ascontiguousarray([int(o) for o in ops], dtype=np.uint8)
     _lib.check(_lib.lib().mdr_shuffle_stream(_lib.ptr(mt, C.POINTER(C.c_uint32)), len(items),
                                              _lib.ptr(items, _lib.u8p), passes, None), "mdr_shuffle_stream")
-    rng.setstate((st[0], tuple(mt.tolist()), st[2]))
+    rng.setstate((st[0], tuple(array.array("I", mt.tobytes())), st[2]))
 
 
 class DeviceSearch:
@@ -190,20 +196,22 @@ def _apply_result(sol, routes, attrs=None, open_routes: bool = False):
     cls = _route_cls(sol)
     old = sol.routes
     rows = attrs[:len(routes)].tolist() if attrs is not None else None
+    def attr_of(i, d, a, c):  # built only for the routes that take it
+        return RouteAttr(*rows[i], d, c[-1] if open_routes else a) if rows is not None and c else None
+
     for i, (d, a, c) in enumerate(routes):
-        attr = RouteAttr(*rows[i], d, c[-1] if open_routes else a) if rows is not None and c else None
         if i < len(old):
             r = old[i]
             if r.depart != d or r.arrive != a or r.customers != c:
                 r.depart, r.arrive, r.customers = d, a, c
                 if hasattr(r, "attr"):
-                    r.attr = attr
+                    r.attr = attr_of(i, d, a, c)
             elif getattr(r, "attr", None) is _STALE:
-                r.attr = attr
+                r.attr = attr_of(i, d, a, c)
         else:
             r = cls(d, a, list(c))
             if hasattr(r, "attr"):
-                r.attr = attr
+                r.attr = attr_of(i, d, a, c)
             old.append(r)
     del old[len(routes):]
 
@@ -245,7 +253,8 @@ def _searcher(inst, consts, nbr, device: int = 0) -> DeviceSearch:
     return s
 
 
-def _finish(search, sols, penalties, rngs, routes, lam, stats, inst, ops, on_feasible, best_only: bool):
+def _finish(search, sols, penalties, rngs, routes, lam, stats, inst, ops, on_feasible, best_only: bool,
+            starts=None):
     """Hand a device descent back to the caller's objects: rng advanced by the
     passes used, penalties updated, routes mutated in place with route_attr
     refreshed from the device, and on_feasible called -- per feasible post-step
@@ -255,7 +264,7 @@ def _finish(search, sols, penalties, rngs, routes, lam, stats, inst, ops, on_fea
     attrs = pop.route_attrs(0, len(sols))
     best = pop.download_best() if (on_feasible is not None and best_only) else None
     for b, (sol, pen, rng) in enumerate(zip(sols, penalties, rngs)):
-        _advance(rng, ops, stats[b]["passes"])
+        _advance(rng, ops, stats[b]["passes"], None if starts is None else starts[b])
         pen.lam[:] = [float(x) for x in lam[b]]
         if on_feasible is not None and not best_only:
             _replay(sol, pop.trace(b), inst, on_feasible)
@@ -306,13 +315,15 @@ def local_search_population(sols, penalties, cfg: SearchConfig, nbr, consts, ins
     try:
         search = _searcher(inst, consts, nbr, device)
         ops = enabled_operators(inst)
-        perms = np.stack([draw_permutations(r, ops, cfg.depth + 1) for r in rngs])
+        starts: list = []
+        perms = np.stack([draw_permutations(r, ops, cfg.depth + 1, starts) for r in rngs])
         lams = [p.lam for p in penalties]
         dl = -1.0 if deadline is None else max(0.0, deadline - time.monotonic())
         replay = on_feasible is not None and not feasible_best_only
         routes, lam, stats = search.run(sols, lams, perms, cfg, p0.kappa, p0.lam_min, p0.lam_max, dl,
                                         snapshot_best=on_feasible is not None and feasible_best_only, trace=replay)
-        _finish(search, sols, penalties, rngs, routes, lam, stats, inst, ops, on_feasible, feasible_best_only)
+        _finish(search, sols, penalties, rngs, routes, lam, stats, inst, ops, on_feasible, feasible_best_only,
+                starts)
     finally:
         if gc_on:
             gc.enable()
