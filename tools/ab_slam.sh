@@ -1,0 +1,17 @@
+# multipliers staged in shared memory per task individual (current) vs read per task (prev)
+set -x
+timeout 1500 python -m pytest tests/test_gpu_shapes.py tests/test_gpu_parity.py tests/test_large_golden.py -q -m gpu -x -p no:cacheprovider > gpurun_out/s_tests.log 2>&1; echo "tests exit $?" >> gpurun_out/s_tests.log
+run() {  # tag lib cfg pop
+  MDR_LIB=$PWD/paper_2605_05208_b200/$2 timeout 900 python bench.py --config $3 --pop $4 --steps 3 --warmup 3 --no-cpu-baseline --no-numpy-ref --no-e2e --no-repair > gpurun_out/s_$1_$3_$4.jsonl 2> gpurun_out/s_$1_$3_$4.err
+}
+for cfg in "C4 256" "C5 64" "C4 32"; do
+  set -- $cfg
+  for rep in 1 2; do
+    run prev$rep libmdr_prev.so $1 $2
+    run cur$rep libmdr_sm100.so $1 $2
+  done
+done
+for f in gpurun_out/s_*.jsonl; do python -c "
+import json
+d=json.loads(open('$f').read().strip().splitlines()[-1]); e=d['profile']['evaluators_ms']
+print('$f'.split('/')[-1].ljust(26), round(d['value']/1e9,3), 'G/s', round(d['ms_per_step'],1), 'ms', {k: round(v,1) for k,v in e.items()})" 2>&1 | tail -1; done | sort > gpurun_out/s_summary.txt
