@@ -68,6 +68,10 @@ struct mdr_pop {
   cudaEvent_t join[2];
   cudaStream_t side[4];          // fork/join branches of the per-operator evaluators ([3]: relocate boundary family)
   cudaEvent_t fev[6];
+  // the round-batch graph, kept across calls while the launch parameters it
+  // captured (instance, population, search parameters, rounds per batch) match
+  cudaGraphExec_t gx = nullptr;
+  std::vector<unsigned char> gkey;
   // repair scratch (mdr_repair), grown on demand
   char *rp_pre = nullptr, *rp_suf = nullptr;
   double *rp_c1 = nullptr, *rp_c2 = nullptr;
@@ -337,6 +341,7 @@ static int pop_build(mdr_pop *p, mdr_instance *inst, int32_t Bcap, int32_t J, in
 void mdr_pop_destroy(mdr_pop *p) {
   if (!p) return;
   cudaSetDevice(p->inst->device);
+  if (p->gx) cudaGraphExecDestroy(p->gx);
   for (void *q : p->allocs) cudaFree(q);
   if (p->d_perms) cudaFree(p->d_perms);
   if (p->d_xfer) cudaFree(p->d_xfer);
@@ -1042,6 +1047,7 @@ int mdr_local_search(mdr_pop *p, const mdr_ls_cfg *cfg, mdr_ls_stats *stats, voi
     CK(cudaMemsetAsync(P.best_m, 0, sizeof(int) * B, s));
   }
   LsParams L;
+  memset(&L, 0, sizeof(L));  // padding too: the bytes key the cached round graph
   L.depth = cfg->depth;
   L.multi_move = cfg->multi_move ? 1 : 0;
   L.kappa = cfg->kappa;
@@ -1064,7 +1070,8 @@ int mdr_local_search(mdr_pop *p, const mdr_ls_cfg *cfg, mdr_ls_stats *stats, voi
     P.tcap = per;
     p->tr_per = per;
   }
-  const int rps = cfg->rounds_per_sync > 0 ? cfg->rounds_per_sync : 8;
+  static const int rps_env = getenv("MDR_RPS") ? atoi(getenv("MDR_RPS")) : 0;  // A/B override
+  const int rps = rps_env > 0 ? rps_env : cfg->rounds_per_sync > 0 ? cfg->rounds_per_sync : 8;
   auto t0 = std::chrono::steady_clock::now();
   int prof = p->profiling;
   if (prof) CK(cudaEventRecord(p->ev[6], s));
@@ -1091,17 +1098,34 @@ int mdr_local_search(mdr_pop *p, const mdr_ls_cfg *cfg, mdr_ls_stats *stats, voi
   while (B > 0) {
     if (graph && batches > 0) {
       if (!gexec) {
-        cudaGraph_t gr;
-        CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
-        for (int r = 0; r < rps; r++) {
-          launch_plan(I, P, L, s);
-          launch_eval(I, P, L, p->grid, I.win, s, p->side, p->fev);
-          launch_eval_g(I, P, L, p->grid, I.win, s);
-          launch_select(I, P, L, I.win, s);
+        // the captured kernels hold (I, P, L) by value: reuse the previous call's
+        // graph when those bytes and the batch length are unchanged (instantiating
+        // it costs ~0.1 ms per round; a short descent is a few ms)
+        std::vector<unsigned char> key(sizeof(DevInst) + sizeof(DevPop) + sizeof(LsParams) + sizeof(int));
+        unsigned char *kp = key.data();
+        memcpy(kp, &I, sizeof(DevInst));
+        memcpy(kp + sizeof(DevInst), &P, sizeof(DevPop));
+        memcpy(kp + sizeof(DevInst) + sizeof(DevPop), &L, sizeof(LsParams));
+        memcpy(kp + sizeof(DevInst) + sizeof(DevPop) + sizeof(LsParams), &rps, sizeof(int));
+        if (p->gx && p->gkey == key) {
+          gexec = p->gx;
+        } else {
+          if (p->gx) cudaGraphExecDestroy(p->gx);
+          p->gx = nullptr;
+          cudaGraph_t gr;
+          CK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+          for (int r = 0; r < rps; r++) {
+            launch_plan(I, P, L, s);
+            launch_eval(I, P, L, p->grid, I.win, s, p->side, p->fev);
+            launch_eval_g(I, P, L, p->grid, I.win, s);
+            launch_select(I, P, L, I.win, s);
+          }
+          CK(cudaStreamEndCapture(s, &gr));
+          CK(cudaGraphInstantiate(&gexec, gr, 0));
+          cudaGraphDestroy(gr);
+          p->gx = gexec;
+          p->gkey.swap(key);
         }
-        CK(cudaStreamEndCapture(s, &gr));
-        CK(cudaGraphInstantiate(&gexec, gr, 0));
-        cudaGraphDestroy(gr);
       }
       CK(cudaGraphLaunch(gexec, s));
       rounds += rps;
@@ -1145,7 +1169,6 @@ int mdr_local_search(mdr_pop *p, const mdr_ls_cfg *cfg, mdr_ls_stats *stats, voi
       if (el > cfg->deadline_s) break;
     }
   }
-  if (gexec) cudaGraphExecDestroy(gexec);
   CK(cudaEventRecord(p->join[1], s));
   CK(cudaStreamWaitEvent(cs, p->join[1], 0));
   if (prof) {
