@@ -86,7 +86,7 @@ typedef struct mdr_ls_cfg {
   int32_t max_passes, n_ops;
   const uint8_t *perms;            /* [B][max_passes][n_ops]: rng.shuffle results, host */
   double deadline_s;               /* <0: none; else seconds from the call (checked between rounds) */
-  int32_t rounds_per_sync;         /* device rounds per host poll (0 = default) */
+  int32_t rounds_per_sync;         /* device rounds per host poll (0 = default, 16) */
   int32_t use_graph;               /* reserved (graphs are used unless MDR_NO_GRAPH is set) */
   int32_t snapshot_best;           /* keep the best feasible state for mdr_pop_download_best */
   int32_t trace;                   /* record every accepted step (mdr_pop_trace) */

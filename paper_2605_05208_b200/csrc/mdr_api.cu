@@ -1071,7 +1071,8 @@ int mdr_local_search(mdr_pop *p, const mdr_ls_cfg *cfg, mdr_ls_stats *stats, voi
     p->tr_per = per;
   }
   static const int rps_env = getenv("MDR_RPS") ? atoi(getenv("MDR_RPS")) : 0;  // A/B override
-  const int rps = rps_env > 0 ? rps_env : cfg->rounds_per_sync > 0 ? cfg->rounds_per_sync : 8;
+  // 16 rounds per host poll: with the graph kept across calls, +0.1-0.3 % over 8 at C2-C4 (C1 -2.5 %)
+  const int rps = rps_env > 0 ? rps_env : cfg->rounds_per_sync > 0 ? cfg->rounds_per_sync : 16;
   auto t0 = std::chrono::steady_clock::now();
   int prof = p->profiling;
   if (prof) CK(cudaEventRecord(p->ev[6], s));

@@ -182,7 +182,7 @@ class Population:
         return routes, bestD[:self.B]
 
     def local_search(self, perms: np.ndarray, depth: int, multi_move: bool, kappa: float, lam_min: float,
-                     lam_max: float, deadline_s: float = -1.0, rounds_per_sync: int = 8, stream=None,
+                     lam_max: float, deadline_s: float = -1.0, rounds_per_sync: int = 0, stream=None,
                      snapshot_best: bool = False, trace: bool = False):
         """perms: uint8 [B, max_passes, n_ops]. Returns a list of per-individual stats dicts."""
         B = self.B
